@@ -1,0 +1,536 @@
+"""Plain CPU CP-ALS / MSDT / pairwise-perturbation oracle (NumPy/SciPy, float64).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py): never imported by the
+product package.  Citations: ``P:n`` = /root/reference/PAPER.md line n.
+
+Layout convention (reading R2): tensors are
+row-major (last mode fastest).  ``unfold(T, n)`` keeps mode n as rows and the
+remaining modes in ascending order, last fastest; the matching Khatri-Rao
+product takes the factors in ascending mode order with the FIRST operand's row
+index slowest.  This is the same product T_(n) P^(n) as the paper's Kolda
+ordering "A^(N) ⊙ ... ⊙ A^(1)" with the first mode fastest;
+the elementwise definition (brute force in the pins) is convention-free.
+"""
+from __future__ import annotations
+
+import dataclasses
+import itertools
+import math
+
+import numpy as np
+import scipy.linalg as sla
+
+import synth
+
+__all__ = [
+    "unfold", "khatri_rao", "mttkrp", "gram", "gamma", "solve", "norm2", "fitness_eq3",
+    "residual_eq2", "kruskal", "make_tensor", "make_tensor_slice", "mttkrp_rows",
+    "als_sweep", "PPState", "pp_init", "pp_approx_sweep", "pp_condition", "pp_controller_run",
+    "ttm", "mttv", "MSDTModel", "DTModel", "msdt_roots", "par_als_sweep_sim",
+    "par_pp_approx_sweep_sim", "dS_of",
+]
+
+
+# ---------------------------------------------------------------------------
+# Notation and definitions (§II-A; §II-B)
+# ---------------------------------------------------------------------------
+
+def unfold(T, n):
+    """Mode-n matricization T_(n): rows = mode n, columns = the other
+    modes in ascending order with the last one fastest (row-major)."""
+    return np.ascontiguousarray(np.moveaxis(T, n, 0)).reshape(T.shape[n], -1)
+
+
+def khatri_rao(mats):
+    """Khatri-Rao product: column k is the Kronecker product of the
+    k-th columns; (a ⊗ b)(i*J + j) = a(i) b(j) -- first operand slowest."""
+    R = mats[0].shape[1]
+    out = mats[0]
+    for B in mats[1:]:
+        out = (out[:, None, :] * B[None, :, :]).reshape(-1, R)
+    return out
+
+
+def mttkrp(T, A, n, block_rows=None):
+    """MTTKRP M^(n) = T_(n) P^(n) with an explicitly formed Khatri-Rao product
+    P^(n).  `block_rows` forms P^(n) in row blocks of the
+    unfolding's column space to bound memory (still explicit)."""
+    N = T.ndim
+    others = [A[m] for m in range(N) if m != n]
+    Tn = unfold(T, n)
+    if block_rows is None or len(others) < 2:
+        return Tn @ khatri_rao(others)
+    # explicit KRP in blocks of its leading factor's rows
+    lead, rest = others[0], khatri_rao(others[1:])
+    K = rest.shape[0]
+    M = np.zeros((T.shape[n], A[0].shape[1]))
+    for i0 in range(0, lead.shape[0], block_rows):
+        blk = khatri_rao([lead[i0:i0 + block_rows], rest])
+        M += Tn[:, i0 * K:(i0 + blk.shape[0] // K) * K] @ blk
+    return M
+
+
+def gram(A):
+    """S = A^T A.  Upper triangle computed, then mirrored, so S is exactly symmetric."""
+    S = A.T @ A
+    iu = np.triu_indices(S.shape[0], 1)
+    S[(iu[1], iu[0])] = S[iu]
+    return S
+
+
+def gamma(S, n):
+    """Γ^(n) = S^(1) * ... * S^(n-1) * S^(n+1) * ... * S^(N) (Eq. 1)."""
+    G = np.ones_like(S[0])
+    for k, Sk in enumerate(S):
+        if k != n:
+            G = G * Sk
+    return G
+
+
+def solve(G, M):
+    """A^(n) <- M^(n) Γ^(n)† (Alg. 1 line 7) as a Cholesky solve (reading Q3:
+    Γ is SPD for full-column-rank factors)."""
+    c = sla.cho_factor(G, lower=True)
+    return np.ascontiguousarray(sla.cho_solve(c, M.T).T)
+
+
+def norm2(T):
+    """||T||_F^2, computed once."""
+    return float(np.dot(T.ravel(), T.ravel()))
+
+
+def fitness_eq3(normT2, G_N, S_N, M_N, A_N):
+    """Relative residual from Eq. 3 with ||T||^2 under the root
+    (reading Q1: the printed unsquared norm is a typo) and f = 1 - r.
+    Returns (f, r)."""
+    rad = normT2 + float(np.sum(G_N * S_N)) - 2.0 * float(np.sum(M_N * A_N))
+    r = math.sqrt(max(rad, 0.0)) / math.sqrt(normT2)
+    return 1.0 - r, r
+
+
+def kruskal(A):
+    """[[A^(1), ..., A^(N)]] = Σ_r A^(1)(:,r) ∘ ... ∘ A^(N)(:,r)."""
+    R = A[0].shape[1]
+    out = None
+    for r in range(R):
+        t = A[0][:, r]
+        for B in A[1:]:
+            t = np.multiply.outer(t, B[:, r])
+        out = t if out is None else out + t
+    return out
+
+
+def residual_eq2(T, A):
+    """r = ||T - T~||_F / ||T||_F with an explicit reconstruction (Eq. 2)."""
+    D = T - kruskal(A)
+    return math.sqrt(norm2(D) / norm2(T))
+
+
+# ---------------------------------------------------------------------------
+# Synthetic tensors (independent reconstruction; the hash comes from synth)
+# ---------------------------------------------------------------------------
+
+def _index_grid(shape, ranges):
+    """Global linear indices (uint64) of the sub-block `ranges` of a tensor of `shape`."""
+    idx = np.zeros([hi - lo for lo, hi in ranges], dtype=np.uint64)
+    stride = 1
+    for d in reversed(range(len(shape))):
+        lo, hi = ranges[d]
+        ax = np.arange(lo, hi, dtype=np.uint64) * np.uint64(stride)
+        sh = [1] * len(shape)
+        sh[d] = hi - lo
+        idx = idx + ax.reshape(sh)
+        stride *= shape[d]
+    return idx
+
+
+def make_tensor_block(cfg, ranges):
+    """T restricted to the index box `ranges` (list of [lo,hi) per mode):
+    Kruskal part of the true factors plus the seeded noise, or the
+    seeded U(0,1) entries for the structureless config (synth recipe)."""
+    idx = _index_grid(cfg.shape, ranges)
+    noise = synth.element_noise(cfg, idx)
+    if cfg.kind == "uniform":
+        return noise
+    At = synth.true_factors(cfg)
+    return kruskal([a[lo:hi] for a, (lo, hi) in zip(At, ranges)]) + noise
+
+
+def make_tensor(cfg, rank=0, world=1):
+    """Local slab of T for `rank` of a 1-D partition along the last mode."""
+    lo, hi = synth.slab_range(cfg.s, rank, world)
+    ranges = [(0, cfg.s)] * (cfg.N - 1) + [(lo, hi)]
+    return make_tensor_block(cfg, ranges)
+
+
+def make_tensor_slice(cfg, n, i):
+    """The (N-1)-way slice T(..., i_n = i, ...) (for row-sampled MTTKRP checks)."""
+    ranges = [(0, cfg.s)] * cfg.N
+    ranges[n] = (i, i + 1)
+    return make_tensor_block(cfg, ranges).reshape([cfg.s] * (cfg.N - 1))
+
+
+def mttkrp_rows(cfg, A, n, rows):
+    """Rows `rows` of M^(n) computed slice by slice with the explicit KRP:
+    M^(n)(i,:) = vec(T(...,i,...))^T P^(n)."""
+    P = khatri_rao([A[m] for m in range(cfg.N) if m != n])
+    return np.stack([make_tensor_slice(cfg, n, int(i)).reshape(-1) @ P for i in rows])
+
+
+# ---------------------------------------------------------------------------
+# Exact CP-ALS sweep (Alg. 1) -- this IS msdt_sweep and dt_sweep
+# (MSDT/DT are exact reorganisations)
+# ---------------------------------------------------------------------------
+
+def als_sweep(T, A, normT2=None):
+    """One CP-ALS sweep (Alg. 1 lines 5-9) with direct MTTKRPs, then Eq. 3.
+
+    Returns dict(A=new factors, S=Grams, M=[M^(n)], dA=[per-sweep update],
+    G=[Γ^(n)], f=fitness, r=residual).
+    """
+    N = T.ndim
+    A = [a.copy() for a in A]
+    S = [gram(a) for a in A]
+    if normT2 is None:
+        normT2 = norm2(T)
+    Ms, dA, Gs = [], [], []
+    for n in range(N):
+        G = gamma(S, n)
+        M = mttkrp(T, A, n)
+        new = solve(G, M)
+        dA.append(new - A[n])
+        A[n] = new
+        S[n] = gram(new)
+        Ms.append(M)
+        Gs.append(G)
+    f, r = fitness_eq3(normT2, Gs[-1], S[-1], Ms[-1], A[-1])
+    return dict(A=A, S=S, M=Ms, dA=dA, G=Gs, f=f, r=r)
+
+
+# ---------------------------------------------------------------------------
+# Pairwise perturbation (§II-C, Eqs. 4-8, Alg. 2)
+# ---------------------------------------------------------------------------
+
+@dataclasses.dataclass
+class PPState:
+    Ap: list                 # A_p^(i) snapshot (Alg. 2 line 7)
+    ops: dict                # (a,b) a<b -> M_p^(a,b) as [s_a, s_b, R]  (Eq. 4 with A_p)
+    Mp: list                 # M_p^(n) = exact MTTKRP at A_p
+
+
+def pp_init(T, A):
+    """PP initialisation (Alg. 2 lines 6-9): A_p <- A, dA <- 0, and the
+    operators M_p^(a,b) = T_(a,b) ⊙_{m∉{a,b}} A_p^(m) (Eq. 4), computed
+    directly with explicit partial Khatri-Rao products (not via the PP tree)."""
+    N = T.ndim
+    Ap = [a.copy() for a in A]
+    ops = {}
+    for a, b in itertools.combinations(range(N), 2):
+        rest = [m for m in range(N) if m not in (a, b)]
+        Tab = np.ascontiguousarray(np.moveaxis(T, (a, b), (0, 1))).reshape(T.shape[a], T.shape[b], -1)
+        ops[(a, b)] = Tab @ khatri_rao([Ap[m] for m in rest])
+    Mp = [mttkrp(T, Ap, n) for n in range(N)]
+    return PPState(Ap=Ap, ops=ops, Mp=Mp)
+
+
+def dS_of(A_i, dA_i):
+    """dS^(i) = A^(i)T dA^(i) (Eq. 8); row index = model rank, not symmetrised."""
+    return A_i.T @ dA_i
+
+
+def pp_condition(dA, A, eps):
+    """Alg. 2 line 5 / line 10: ∀i ||dA^(i)||_F < ε ||A^(i)||_F (strict)."""
+    return all(np.linalg.norm(d) < eps * np.linalg.norm(a) for d, a in zip(dA, A))
+
+
+def pp_approx_sweep(st: PPState, A, normT2, eps=None):
+    """One PP approximated sweep (Alg. 2 lines 11-16; Eqs. 5-8).
+
+    For n = 1..N: Γ^(n); dA^(i) = A^(i) - A_p^(i) (current); U^(n,i) (Eq. 6);
+    dS^(i) (Eq. 8); V^(n) = A^(n) W^(n) with W^(n) = Σ_{i<j; i,j≠n}
+    dS^(i)*dS^(j)*∗_{k∉{i,j,n}} S^(k) (Eq. 7, reading Q7/Q8: all current, A^(n)
+    pre-update); M~^(n) = M_p^(n) + Σ_i U^(n,i) + V^(n) (Eq. 5); solve; update
+    dA^(n), S^(n).  Fitness by Eq. 3 with M~^(N) (reading Q21).
+    Returns dict(A, S, M=[M~^(n)], U, V, f, r, still_valid).
+    """
+    N = len(A)
+    A = [a.copy() for a in A]
+    S = [gram(a) for a in A]
+    Ms, Vs, Gs = [], [], []
+    for n in range(N):
+        G = gamma(S, n)
+        dA = [A[i] - st.Ap[i] for i in range(N)]
+        Mt = st.Mp[n].copy()
+        for i in range(N):
+            if i == n:
+                continue
+            if n < i:   # operator stored as [s_n, s_i, R]: contract its second axis
+                Mt += np.einsum("xyk,yk->xk", st.ops[(n, i)], dA[i])
+            else:       # stored as [s_i, s_n, R]: contract its first axis
+                Mt += np.einsum("yxk,yk->xk", st.ops[(i, n)], dA[i])
+        dS = [dS_of(A[i], dA[i]) for i in range(N)]
+        W = np.zeros_like(G)
+        for i, j in itertools.combinations([m for m in range(N) if m != n], 2):
+            term = dS[i] * dS[j]
+            for k in range(N):
+                if k not in (i, j, n):
+                    term = term * S[k]
+            W += term
+        V = A[n] @ W
+        Mt += V
+        new = solve(G, Mt)
+        A[n] = new
+        S[n] = gram(new)
+        Ms.append(Mt)
+        Vs.append(V)
+        Gs.append(G)
+    f, r = fitness_eq3(normT2, Gs[-1], S[-1], Ms[-1], A[-1])
+    dA = [A[i] - st.Ap[i] for i in range(N)]
+    valid = pp_condition(dA, A, eps) if eps is not None else None
+    return dict(A=A, S=S, M=Ms, V=Vs, f=f, r=r, still_valid=valid, dA=dA)
+
+
+def pp_controller_run(T, A0, eps, delta=1e-5, max_sweeps=300, max_pp_run=None):
+    """Alg. 2 driver with reading Q21 (fitness after every sweep, Δ test
+    on consecutive sweeps of any kind).  Returns the list of (kind, f)."""
+    normT2 = norm2(T)
+    A = [a.copy() for a in A0]
+    dA = [a.copy() for a in A]          # Alg. 2 line 2: dA <- A
+    trace, f_old = [], None
+    while len(trace) < max_sweeps:
+        if pp_condition(dA, A, eps):
+            st = pp_init(T, A)
+            trace.append(("pp_init", None))
+            n_run = 0
+            while True:
+                out = pp_approx_sweep(st, A, normT2, eps)
+                A = out["A"]
+                trace.append(("pp_approx", out["f"]))
+                n_run += 1
+                stop = f_old is not None and abs(out["f"] - f_old) <= delta
+                f_old = out["f"]
+                if stop or not out["still_valid"] or len(trace) >= max_sweeps or \
+                        (max_pp_run is not None and n_run >= max_pp_run):
+                    break
+            if stop:
+                break
+        out = als_sweep(T, A, normT2)
+        A, dA = out["A"], out["dA"]
+        trace.append(("regular", out["f"]))
+        if f_old is not None and abs(out["f"] - f_old) <= delta:
+            break
+        f_old = out["f"]
+    return A, trace
+
+
+# ---------------------------------------------------------------------------
+# Dimension-tree schedule models (CPU models of the *schedules*, P:210-322 and
+# §III).  They compute MTTKRPs through the trees with TTM/mTTV steps
+# and are pinned against the direct MTTKRP under arbitrary factor updates.
+# ---------------------------------------------------------------------------
+
+def ttm(T, A, j):
+    """First-level contraction T ×_j A^(j)T, output modes = the others (ascending) + R
+    (Eq. 4 with one contracted mode)."""
+    out = np.tensordot(T, A, axes=([j], [0]))        # moves the contracted axis out, R last
+    return out
+
+
+def mttv(X, v, axis):
+    """Batched TTV: out[..., r] = Σ_y X[..., y, ..., r] v[y, r]."""
+    Xm = np.moveaxis(X, axis, -2)                    # [..., y, r]
+    return np.einsum("...yr,yr->...r", Xm, v)
+
+
+def _split_contract(node, kept, drop_modes, A, order):
+    """Contract the modes `drop_modes` of `node` (kept = its ascending mode list), one
+    mTTV per mode, in `order` (service order, reading Q5)."""
+    kept = list(kept)
+    for m in order:
+        if m in drop_modes:
+            ax = kept.index(m)
+            node = mttv(node, A[m], ax)
+            kept.pop(ax)
+    return node, kept
+
+
+class _SubtreeRunner:
+    """Lazy binary subtree (O3): served list L; left = first ceil(|L|/2) modes built by
+    contracting the right modes (current), right = rest built by contracting the left
+    modes after their updates.  Nodes are built just before first use."""
+
+    def __init__(self, root, kept, served):
+        self.served = list(served)
+        self.cache = {(0, len(served)): (root, list(kept))}
+
+    def leaf(self, q, A):
+        L = self.served
+        lo, hi = 0, len(L)
+        node, kept = self.cache[(lo, hi)]
+        while hi - lo > 1:
+            mid = lo + (hi - lo + 1) // 2
+            if q < mid:
+                child, drop = (lo, mid), L[mid:hi]
+            else:
+                child, drop = (mid, hi), L[lo:mid]
+            if child not in self.cache:
+                self.cache[child] = _split_contract(node, kept, set(drop), A, L[lo:hi])
+            lo, hi = child
+            node, kept = self.cache[child]
+        return node, kept
+
+
+class MSDTModel:
+    """MSDT schedule (§III, Fig. 2).  Root k (k = 0,1,...) is T ×_j A^(j) with
+    j = N, N-1, ..., 1 cyclically (1-based; "root of ith subtree is T×_{N-i+1}"),
+    serving the N-1 modes (j+1, ..., j+N-1) mod N (0≡N, reading Q4).  In a continuous
+    stream of updates t = 0,1,..., mode(t) = t mod N and root k serves t in
+    [k(N-1), (k+1)(N-1)).  Counts first-level TTMs (pin: N per N-1 sweeps)."""
+
+    def __init__(self, T):
+        self.T = T
+        self.N = T.ndim
+        self.t = 0
+        self.runner = None
+        self.n_ttm = 0
+        self.trace = []      # (root contracted mode j (0-based), served list)
+
+    def next_mttkrp(self, A):
+        N = self.N
+        k, q = divmod(self.t, N - 1)
+        if q == 0:
+            j = ((k + 1) * (N - 1)) % N                   # 0-based contracted mode of root k
+            served = [(j + d) % N for d in range(1, N)]
+            root = ttm(self.T, A[j], j)
+            self.n_ttm += 1
+            kept = [m for m in range(N) if m != j]
+            self.runner = _SubtreeRunner(root, kept, served)
+            self.trace.append((j, served))
+        n = self.t % N
+        node, kept = self.runner.leaf(q, A)
+        assert kept == [n] and self.runner.served[q] == n
+        self.t += 1
+        return node
+
+
+class DTModel:
+    """Standard dimension tree (Fig. 1a; O4): per sweep, root T×_N then the
+    modes ceil(N/2)+1..N-1 (current) serve 1..ceil(N/2); root T×_1 then modes
+    2..ceil(N/2) (already updated) serve ceil(N/2)+1..N.  2 TTMs per sweep."""
+
+    def __init__(self, T):
+        self.T = T
+        self.N = T.ndim
+        self.n_ttm = 0
+        self.n = 0
+        self.runner = None
+
+    def next_mttkrp(self, A):
+        N = self.N
+        h = (N + 1) // 2
+        n = self.n % N
+        if n == 0 or n == h:
+            if n == 0:
+                j, pre, served = N - 1, list(range(h, N - 1)), list(range(0, h))
+            else:
+                j, pre, served = 0, list(range(1, h)), list(range(h, N))
+            node = ttm(self.T, A[j], j)
+            self.n_ttm += 1
+            kept = [m for m in range(N) if m != j]
+            node, kept = _split_contract(node, kept, set(pre), A, pre)
+            self.runner = _SubtreeRunner(node, kept, served)
+            self.base = n
+        q = n - self.base
+        node, kept = self.runner.leaf(q, A)
+        assert kept == [n]
+        self.n += 1
+        return node
+
+
+def msdt_roots(N, n_sweeps):
+    """Contracted mode (0-based) of every MSDT root used in `n_sweeps` sweeps."""
+    n_updates = N * n_sweeps
+    return [((k + 1) * (N - 1)) % N for k in range(-(-n_updates // (N - 1)))]
+
+
+# ---------------------------------------------------------------------------
+# Parallel algorithms on a 1-D grid 1x...x1xP (Alg. 3; Alg. 4)
+# simulated in one process; the gloo test runs the same steps with real collectives.
+# ---------------------------------------------------------------------------
+
+def par_als_sweep_sim(T, A, P, normT2=None):
+    """Alg. 3 with the tensor split along the last mode into P slabs: local MTTKRP
+    (line 13) -> Reduce-Scatter (line 14, n<N) -> solve own rows (line 15) ->
+    All-Gather A (line 18); mode N rows are local, S^(N) by All-Reduce (line 17)."""
+    N = T.ndim
+    sN = T.shape[-1]
+    slabs = [T[..., lo:hi] for lo, hi in (synth.slab_range(sN, p, P) for p in range(P))]
+    A = [a.copy() for a in A]
+    S = [gram(a) for a in A]
+    if normT2 is None:
+        normT2 = sum(norm2(t) for t in slabs)
+    for n in range(N):
+        G = gamma(S, n)
+        loc = []
+        for p, Tp in enumerate(slabs):
+            lo, hi = synth.slab_range(sN, p, P)
+            Ap = A[:-1] + [A[-1][lo:hi]]
+            loc.append(mttkrp(Tp, Ap, n))
+        if n < N - 1:
+            M = sum(loc)                                   # reduce-scatter then all-gather
+            b = T.shape[n] // P
+            A[n] = np.concatenate([solve(G, M[p * b:(p + 1) * b]) for p in range(P)])
+            S[n] = gram(A[n])
+        else:
+            M = np.concatenate(loc)
+            A[n] = np.concatenate([solve(G, m) for m in loc])
+            S[n] = sum(gram(A[n][synth.slab_range(sN, p, P)[0]:synth.slab_range(sN, p, P)[1]])
+                       for p in range(P))
+            Gl, Ml = G, M
+    f, r = fitness_eq3(normT2, Gl, S[-1], Ml, A[-1])
+    return dict(A=A, S=S, f=f, r=r)
+
+
+def par_pp_approx_sweep_sim(T, st_full: PPState, A, P, normT2):
+    """Alg. 4 on the 1-D grid: Local-PP-init on each slab (no
+    communication), local U, Reduce-Scatter of M~, V on replicated small matrices.
+    Returns the M~^(n) list (global) for comparison with the sequential sweep."""
+    N = T.ndim
+    sN = T.shape[-1]
+    rng = [synth.slab_range(sN, p, P) for p in range(P)]
+    locs = []
+    for lo, hi in rng:
+        Ap = st_full.Ap[:-1] + [st_full.Ap[-1][lo:hi]]
+        locs.append(pp_init(T[..., lo:hi], Ap))
+    A = [a.copy() for a in A]
+    S = [gram(a) for a in A]
+    Ms = []
+    for n in range(N):
+        G = gamma(S, n)
+        dA = [A[i] - st_full.Ap[i] for i in range(N)]
+        parts = []
+        for (lo, hi), st in zip(rng, locs):
+            dAl = dA[:-1] + [dA[-1][lo:hi]]
+            Mt = st.Mp[n].copy()
+            for i in range(N):
+                if i == n:
+                    continue
+                if n < i:
+                    Mt += np.einsum("xyk,yk->xk", st.ops[(n, i)], dAl[i])
+                else:
+                    Mt += np.einsum("yxk,yk->xk", st.ops[(i, n)], dAl[i])
+            parts.append(Mt)
+        Mt = sum(parts) if n < N - 1 else np.concatenate(parts)
+        dS = [dS_of(A[i], dA[i]) for i in range(N)]
+        W = np.zeros_like(G)
+        for i, j in itertools.combinations([m for m in range(N) if m != n], 2):
+            term = dS[i] * dS[j]
+            for k in range(N):
+                if k not in (i, j, n):
+                    term = term * S[k]
+            W += term
+        Mt = Mt + A[n] @ W
+        A[n] = solve(G, Mt)
+        S[n] = gram(A[n])
+        Ms.append(Mt)
+    return dict(A=A, M=Ms)
