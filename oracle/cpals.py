@@ -173,8 +173,14 @@ def make_tensor_slice(cfg, n, i):
 def mttkrp_rows(cfg, A, n, rows):
     """Rows `rows` of M^(n) computed slice by slice with the explicit KRP:
     M^(n)(i,:) = vec(T(...,i,...))^T P^(n)."""
-    P = khatri_rao([A[m] for m in range(cfg.N) if m != n])
-    return np.stack([make_tensor_slice(cfg, n, int(i)).reshape(-1) @ P for i in rows])
+    others = [A[m] for m in range(cfg.N) if m != n]
+    lead, rest = others[0], khatri_rao(others[1:])   # explicit KRP, formed per lead row
+    K = rest.shape[0]
+    out = []
+    for i in rows:
+        sl = make_tensor_slice(cfg, n, int(i)).reshape(lead.shape[0], K)
+        out.append(sum(sl[a] @ khatri_rao([lead[a:a + 1], rest]) for a in range(lead.shape[0])))
+    return np.stack(out)
 
 
 # ---------------------------------------------------------------------------

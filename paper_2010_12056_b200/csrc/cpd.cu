@@ -1,0 +1,1076 @@
+// libcpd.so: C ABI (include/cpd.h), device state, the MSDT / DT / PP schedulers and
+// the 1-D-grid collectives.  Citations: P:n = PAPER.md line n.
+//
+// Host-side scheduling:
+//  * MSDT (§III, Fig. 2): a continuous stream of factor updates t = 0,1,...
+//    (mode t mod N); root k = T x_j A^(j) with j = ((k+1)(N-1)) mod N (0-based, i.e.
+//    T x_N, T x_{N-1}, ..., T x_1 cyclically) serves updates t in
+//    [k(N-1), (k+1)(N-1)), i.e. modes (j+1, ..., j+N-1) mod N.  Inside a subtree the
+//    served list L is split binary: left = first ceil(|L|/2) modes built by contracting
+//    the right ones (not yet updated), right = the rest built after the left updates
+//    (reading Q5; reproduces Fig. 2 for N=4).  Nodes are built lazily, just before first
+//    use, and freed when no longer an ancestor of the next leaf.
+//  * DT (Fig. 1a): per sweep root T x_N (then modes ceil(N/2)+1..N-1) serves
+//    1..ceil(N/2), root T x_1 (then 2..ceil(N/2), already updated) serves the rest.
+//  * PP (Alg. 2, Eqs. 4-8; Alg. 4): pp_init builds every pair operator from three
+//    first-level roots (one reused from the live MSDT root when still valid, P:384
+//    footnote); pp_approx_sweep streams the N-1 operators of each mode (Eq. 6) and adds
+//    the second-order term V (Eq. 7).
+//  * Multi-GPU (Alg. 3 / Alg. 4 on the grid 1x..x1xP): local contractions, NCCL
+//    reduce-scatter of the partial M^(n) (n < N-1), solve on own rows, all-gather of
+//    A^(n); the last mode's rows are local, S^(N), dS^(N) and the scalars all-reduced.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/cpd.h"
+#include "kernels.h"
+
+namespace {
+
+thread_local std::string g_init_error;
+
+enum Phase { PH_TTM = 0, PH_MTTV = 1, PH_SOLVE = 2, PH_HAD = 3, PH_OTHER = 4 };
+
+struct Node {
+  double* buf = nullptr;
+  std::vector<int> kept;  // ascending modes; dims = ext(k)..., R
+};
+
+struct Subtree {
+  int j = -1;                              // contracted mode of the root
+  std::vector<int> served;                 // service order
+  std::map<std::pair<int, int>, Node> cache;
+  bool active = false;
+};
+
+struct PhaseRec {
+  cudaEvent_t a, b;
+  int phase;
+};
+
+}  // namespace
+
+struct cpd_ctx {
+  int N = 0, R = 0;
+  int64_t shape[CPD_MAX_ORDER] = {0};
+  int rank = 0, world = 1;
+  int64_t sN_loc = 0, lo = 0;
+  int dev = 0;
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  ncclComm_t comm = nullptr;
+  const double* T = nullptr;
+  int64_t T_elems = 0;
+  cpd_opts opts{};
+  // factors: mode N-1 holds only the local slab rows
+  std::vector<double*> A, Aold, dA, Mlast, Ap, Mp;
+  double* S_all = nullptr;   // N x R x R
+  double* dS_all = nullptr;  // N x R x R
+  double* Lp = nullptr;      // packed Cholesky factor
+  double* W = nullptr;       // R x R
+  double* scal = nullptr;    // device scalars (see SC_*)
+  double* partial = nullptr;
+  int* status = nullptr;     // N ints, Cholesky status per mode
+  double* hscal = nullptr;   // pinned mirror of scal
+  int* hstatus = nullptr;
+  double* gather_tmp = nullptr;  // s_N x R for get_factor of the last mode
+  // scheduler state
+  int64_t t = 0;             // MSDT update stream position
+  Subtree sub;               // live subtree (MSDT or DT)
+  bool sub_is_msdt = false;
+  std::map<std::pair<int, int>, double*> ops;  // PP operators
+  bool pp_valid = false;
+  bool pp_regime = false;    // dA = A - A_p (PP) vs one-sweep update (regular)
+  bool have_fit = false;
+  double last_f = 0.0, last_r = 0.0;
+  bool have_dA = false;
+  double dA2[CPD_MAX_ORDER] = {0}, A2[CPD_MAX_ORDER] = {0};
+  // diagnostics
+  bool poisoned = false;
+  std::string err;
+  double phase_ms[5] = {0};
+  double counters[5] = {0};
+  std::vector<PhaseRec> pending;
+  std::vector<cudaEvent_t> free_events;
+};
+
+// scalar slots
+enum { SC_NT2 = 0, SC_MA = 1, SC_GS = 2, SC_DA2 = 3 /* N */, SC_A2 = 3 + CPD_MAX_ORDER /* N */,
+       SC_LASTN2 = 3 + 2 * CPD_MAX_ORDER, SC_COUNT = 8 + 2 * CPD_MAX_ORDER };
+
+namespace {
+
+cpd_status fail(cpd_ctx* c, cpd_status s, const std::string& msg) {
+  if (c) {
+    c->err = msg;
+    if (s == CPD_ERR_CUDA || s == CPD_ERR_NCCL) c->poisoned = true;
+  } else {
+    g_init_error = msg;
+  }
+  return s;
+}
+
+#define CU(x)                                                                                 \
+  do {                                                                                        \
+    cudaError_t e_ = (x);                                                                     \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(ctx, e_ == cudaErrorMemoryAllocation ? CPD_ERR_OOM : CPD_ERR_CUDA,          \
+                  std::string(#x) + ": " + cudaGetErrorString(e_));                          \
+  } while (0)
+#define NC(x)                                                                                 \
+  do {                                                                                        \
+    ncclResult_t r_ = (x);                                                                    \
+    if (r_ != ncclSuccess)                                                                    \
+      return fail(ctx, CPD_ERR_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_));       \
+  } while (0)
+#define TRY(x)                        \
+  do {                                \
+    cpd_status s_ = (x);              \
+    if (s_ != CPD_OK) return s_;      \
+  } while (0)
+
+inline int64_t ext(const cpd_ctx* c, int m) { return m == c->N - 1 ? c->sN_loc : c->shape[m]; }
+inline int64_t rows_own(const cpd_ctx* c, int n) {
+  return n == c->N - 1 ? c->sN_loc : c->shape[n] / c->world;
+}
+inline int64_t own_off(const cpd_ctx* c, int n) {  // row offset of own rows in the local buffer
+  return n == c->N - 1 ? 0 : c->rank * (c->shape[n] / c->world);
+}
+inline int64_t node_elems(const cpd_ctx* c, const std::vector<int>& kept) {
+  int64_t e = c->R;
+  for (int k : kept) e *= ext(c, k);
+  return e;
+}
+
+// ---------------- phase timers ----------------
+cudaEvent_t get_event(cpd_ctx* c) {
+  if (!c->free_events.empty()) {
+    cudaEvent_t e = c->free_events.back();
+    c->free_events.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+struct PhaseScope {
+  cpd_ctx* c;
+  PhaseRec rec;
+  bool on;
+  PhaseScope(cpd_ctx* ctx, int phase) : c(ctx), on(ctx->opts.profile_phases != 0) {
+    if (on) {
+      rec.a = get_event(c);
+      rec.b = get_event(c);
+      rec.phase = phase;
+      cudaEventRecord(rec.a, c->st);
+    }
+  }
+  ~PhaseScope() {
+    if (on) {
+      cudaEventRecord(rec.b, c->st);
+      c->pending.push_back(rec);
+    }
+  }
+};
+void drain_timers(cpd_ctx* c) {  // call after a stream sync
+  for (auto& r : c->pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) c->phase_ms[r.phase] += ms;
+    c->free_events.push_back(r.a);
+    c->free_events.push_back(r.b);
+  }
+  c->pending.clear();
+}
+
+// ---------------- memory ----------------
+cpd_status dalloc(cpd_ctx* ctx, double** p, int64_t elems) {
+  *p = nullptr;
+  if (elems <= 0) elems = 1;
+  CU(cudaMallocAsync((void**)p, sizeof(double) * (size_t)elems, ctx->st));
+  return CPD_OK;
+}
+void dfree(cpd_ctx* c, double*& p) {
+  if (p) cudaFreeAsync(p, c->st);
+  p = nullptr;
+}
+
+// ---------------- kernels with accounting ----------------
+cpd_status ttm(cpd_ctx* ctx, int j, double* out) {
+  // T x_j A^(j): T viewed as [pre, ext(j), post]
+  int64_t pre = 1, post = 1;
+  for (int m = 0; m < j; m++) pre *= ext(ctx, m);
+  for (int m = j + 1; m < ctx->N; m++) post *= ext(ctx, m);
+  PhaseScope ps(ctx, PH_TTM);
+  CU(cpd::launch_ttm(ctx->T, pre, ext(ctx, j), post, ctx->A[j], ctx->R, out, 0, ctx->st));
+  ctx->counters[0] += 2.0 * (double)pre * post * ext(ctx, j) * ctx->R;
+  ctx->counters[1] += 1;
+  ctx->counters[4] += 1;
+  return CPD_OK;
+}
+
+// out = beta*out + contraction of node X (kept) over mode m with v (ext(m) x R)
+cpd_status mttv(cpd_ctx* ctx, const double* X, const std::vector<int>& kept, int m,
+                const double* v, double* out, int beta) {
+  int a = (int)(std::find(kept.begin(), kept.end(), m) - kept.begin());
+  if (a >= (int)kept.size()) return fail(ctx, CPD_ERR_INTERNAL, "mttv: mode not kept");
+  int64_t pre = 1, post = 1;
+  for (int q = 0; q < a; q++) pre *= ext(ctx, kept[q]);
+  for (int q = a + 1; q < (int)kept.size(); q++) post *= ext(ctx, kept[q]);
+  int64_t K = ext(ctx, m);
+  PhaseScope ps(ctx, PH_MTTV);
+  CU(cpd::launch_mttv(X, pre, K, post, ctx->R, v, out, beta, ctx->st));
+  double C = (double)post * ctx->R;
+  ctx->counters[2] += 8.0 * ((double)pre * K * C + (double)pre * C * (beta ? 2 : 1) + (double)K * ctx->R);
+  ctx->counters[3] += 1;
+  return CPD_OK;
+}
+
+// contract the modes `drop` of a node in `order`, returning a new node (input not freed)
+cpd_status contract_modes(cpd_ctx* ctx, const Node& in, const std::vector<int>& drop,
+                          const std::vector<int>& order, Node* out) {
+  Node cur;
+  cur.buf = in.buf;
+  cur.kept = in.kept;
+  bool owned = false;
+  for (int m : order) {
+    if (std::find(drop.begin(), drop.end(), m) == drop.end()) continue;
+    Node nx;
+    for (int k : cur.kept)
+      if (k != m) nx.kept.push_back(k);
+    TRY(dalloc(ctx, &nx.buf, node_elems(ctx, nx.kept)));
+    TRY(mttv(ctx, cur.buf, cur.kept, m, ctx->A[m], nx.buf, 0));
+    if (owned) dfree(ctx, cur.buf);
+    cur = nx;
+    owned = true;
+  }
+  if (!owned) return fail(ctx, CPD_ERR_INTERNAL, "contract_modes: nothing to contract");
+  *out = cur;
+  return CPD_OK;
+}
+
+void clear_subtree(cpd_ctx* c) {
+  for (auto& kv : c->sub.cache) dfree(c, kv.second.buf);
+  c->sub.cache.clear();
+  c->sub.active = false;
+  c->sub.j = -1;
+}
+
+// start a subtree: root T x_j, then contract `pre` (in order), served list
+cpd_status start_subtree(cpd_ctx* ctx, int j, const std::vector<int>& pre, const std::vector<int>& served) {
+  clear_subtree(ctx);
+  Node root;
+  for (int m = 0; m < ctx->N; m++)
+    if (m != j) root.kept.push_back(m);
+  TRY(dalloc(ctx, &root.buf, node_elems(ctx, root.kept)));
+  TRY(ttm(ctx, j, root.buf));
+  if (!pre.empty()) {
+    Node nx;
+    TRY(contract_modes(ctx, root, pre, pre, &nx));
+    dfree(ctx, root.buf);
+    root = nx;
+  }
+  ctx->sub.j = j;
+  ctx->sub.served = served;
+  ctx->sub.cache[{0, (int)served.size()}] = root;
+  ctx->sub.active = true;
+  return CPD_OK;
+}
+
+// leaf q of the live subtree (lazy binary descent, O3)
+cpd_status subtree_leaf(cpd_ctx* ctx, int q, const double** leaf) {
+  auto& sub = ctx->sub;
+  const auto& L = sub.served;
+  int lo = 0, hi = (int)L.size();
+  auto it = sub.cache.find({lo, hi});
+  if (it == sub.cache.end()) return fail(ctx, CPD_ERR_INTERNAL, "subtree root missing");
+  while (hi - lo > 1) {
+    int mid = lo + (hi - lo + 1) / 2;
+    std::pair<int, int> child;
+    std::vector<int> drop;
+    if (q < mid) {
+      child = {lo, mid};
+      drop.assign(L.begin() + mid, L.begin() + hi);
+    } else {
+      child = {mid, hi};
+      drop.assign(L.begin() + lo, L.begin() + mid);
+    }
+    if (!sub.cache.count(child)) {
+      // free finished nodes: everything that is not an ancestor of `child`
+      for (auto c2 = sub.cache.begin(); c2 != sub.cache.end();) {
+        bool anc = c2->first.first <= child.first && child.second <= c2->first.second;
+        if (!anc) {
+          dfree(ctx, c2->second.buf);
+          c2 = sub.cache.erase(c2);
+        } else {
+          ++c2;
+        }
+      }
+      const Node& parent = sub.cache[{lo, hi}];
+      std::vector<int> order(L.begin() + lo, L.begin() + hi);
+      Node nx;
+      TRY(contract_modes(ctx, parent, drop, order, &nx));
+      sub.cache[child] = nx;
+    }
+    lo = child.first;
+    hi = child.second;
+  }
+  const Node& leafn = sub.cache[{lo, hi}];
+  if (leafn.kept.size() != 1 || leafn.kept[0] != L[q])
+    return fail(ctx, CPD_ERR_INTERNAL, "stale or wrong leaf");
+  *leaf = leafn.buf;
+  return CPD_OK;
+}
+
+cpd_status allreduce_lastmode(cpd_ctx* ctx, bool with_dS) {
+  if (ctx->world == 1) return CPD_OK;
+  const int64_t RR = (int64_t)ctx->R * ctx->R;
+  PhaseScope ps(ctx, PH_OTHER);
+  NC(ncclGroupStart());
+  NC(ncclAllReduce(ctx->S_all + (ctx->N - 1) * RR, ctx->S_all + (ctx->N - 1) * RR, RR, ncclDouble,
+                   ncclSum, ctx->comm, ctx->st));
+  if (with_dS)
+    NC(ncclAllReduce(ctx->dS_all + (ctx->N - 1) * RR, ctx->dS_all + (ctx->N - 1) * RR, RR, ncclDouble,
+                     ncclSum, ctx->comm, ctx->st));
+  NC(ncclAllReduce(ctx->scal + SC_MA, ctx->scal + SC_MA, 1, ncclDouble, ncclSum, ctx->comm, ctx->st));
+  NC(ncclAllReduce(ctx->scal + SC_DA2 + ctx->N - 1, ctx->scal + SC_DA2 + ctx->N - 1, 1, ncclDouble,
+                   ncclSum, ctx->comm, ctx->st));
+  NC(ncclAllReduce(ctx->scal + SC_A2 + ctx->N - 1, ctx->scal + SC_A2 + ctx->N - 1, 1, ncclDouble,
+                   ncclSum, ctx->comm, ctx->st));
+  NC(ncclGroupEnd());
+  return CPD_OK;
+}
+
+// <Γ^(N), S^(N)> = Σ_e (∗_{k<N-1} S_k)[e] S_{N-1}[e]  (after S_{N-1} is final)
+__global__ void gamma_dot_kernel(const double* __restrict__ S_all, int N, int R, double* dst) {
+  __shared__ double red[32];
+  const int64_t RR = (int64_t)R * R;
+  double s = 0.0;
+  for (int64_t e = threadIdx.x; e < RR; e += blockDim.x) {
+    double gv = S_all[e];
+    for (int k = 1; k < N - 1; k++) gv *= S_all[k * RR + e];
+    s = fma(gv, S_all[(N - 1) * RR + e], s);
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = (threadIdx.x < blockDim.x / 32) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) dst[0] = s;
+  }
+}
+
+// Solve-and-update for mode n given the local (partial for n<N-1) MTTKRP Mloc
+// (ext(n) x R, may be overwritten).  pp: dA = A - A_p and dS maintained; Vterm: add
+// V = A^(n) W before the solve (Eq. 7).
+cpd_status update_mode(cpd_ctx* ctx, int n, double* Mloc, bool pp) {
+  const int R = ctx->R;
+  const int64_t RR = (int64_t)R * R;
+  const int64_t ro = rows_own(ctx, n), off = own_off(ctx, n);
+  const int64_t rows_full = ext(ctx, n);
+  double* Mown = Mloc + off * R;
+  if (n < ctx->N - 1 && ctx->world > 1) {
+    PhaseScope ps(ctx, PH_OTHER);
+    NC(ncclReduceScatter(Mloc, Mown, ro * R, ncclDouble, ncclSum, ctx->comm, ctx->st));
+  }
+  if (pp) {
+    // V^(n) = A^(n) W^(n) with the current (pre-update) A^(n): Eq. 7; M~ += V (Eq. 5)
+    {
+      PhaseScope ps(ctx, PH_HAD);
+      CU(cpd::launch_pp_w(ctx->S_all, ctx->dS_all, ctx->N, n, R, ctx->W, ctx->st));
+    }
+    PhaseScope ps(ctx, PH_SOLVE);
+    CU(cpd::launch_ttm(ctx->A[n] + off * R, ro, R, 1, ctx->W, R, Mown, 1, ctx->st));
+  }
+  {
+    PhaseScope ps(ctx, PH_OTHER);
+    CU(cudaMemcpyAsync(ctx->Mlast[n] + off * R, Mown, sizeof(double) * ro * R, cudaMemcpyDeviceToDevice,
+                       ctx->st));
+    if (!pp)
+      CU(cudaMemcpyAsync(ctx->Aold[n], ctx->A[n], sizeof(double) * rows_full * R,
+                         cudaMemcpyDeviceToDevice, ctx->st));
+  }
+  {
+    PhaseScope ps(ctx, PH_SOLVE);
+    CU(cpd::launch_gamma_chol(ctx->S_all, ctx->N, n, R, ctx->Lp, ctx->status + n, ctx->st));
+    CU(cpd::launch_trisolve(ctx->Lp, Mown, ro, R, ctx->A[n] + off * R, ctx->st));
+  }
+  if (n < ctx->N - 1 && ctx->world > 1) {
+    PhaseScope ps(ctx, PH_OTHER);
+    NC(ncclAllGather(ctx->A[n] + off * R, ctx->A[n], ro * R, ncclDouble, ctx->comm, ctx->st));
+  }
+  {
+    PhaseScope ps(ctx, PH_HAD);
+    const double* base = pp ? ctx->Ap[n] : ctx->Aold[n];
+    CU(cpd::launch_sub(ctx->A[n], base, ctx->dA[n], rows_full * R, ctx->st));
+    CU(cpd::launch_gram(ctx->A[n], ctx->A[n], rows_full, R, ctx->S_all + n * RR, ctx->st));
+    if (pp) CU(cpd::launch_gram(ctx->A[n], ctx->dA[n], rows_full, R, ctx->dS_all + n * RR, ctx->st));
+    CU(cpd::launch_dot(ctx->dA[n], nullptr, rows_full * R, ctx->scal + SC_DA2 + n, ctx->st));
+    CU(cpd::launch_dot(ctx->A[n], nullptr, rows_full * R, ctx->scal + SC_A2 + n, ctx->st));
+  }
+  if (n == ctx->N - 1) {
+    {
+      PhaseScope ps(ctx, PH_OTHER);
+      CU(cpd::launch_dot(Mown, ctx->A[n], ro * R, ctx->scal + SC_MA, ctx->st));
+    }
+    TRY(allreduce_lastmode(ctx, pp));
+    PhaseScope ps(ctx, PH_OTHER);
+    cpd::g_launches++;
+    gamma_dot_kernel<<<1, 1024, 0, ctx->st>>>(ctx->S_all, ctx->N, R, ctx->scal + SC_GS);
+    CU(cudaGetLastError());
+  }
+  return CPD_OK;
+}
+
+// after a sweep: one D2H of the scalars, fitness (Eq. 3), PP condition
+cpd_status finish_sweep(cpd_ctx* ctx, double* f_out) {
+  CU(cudaMemcpyAsync(ctx->hscal, ctx->scal, sizeof(double) * SC_COUNT, cudaMemcpyDeviceToHost, ctx->st));
+  CU(cudaMemcpyAsync(ctx->hstatus, ctx->status, sizeof(int) * ctx->N, cudaMemcpyDeviceToHost, ctx->st));
+  CU(cudaStreamSynchronize(ctx->st));
+  drain_timers(ctx);
+  for (int n = 0; n < ctx->N; n++)
+    if (ctx->hstatus[n] != 0) return fail(ctx, CPD_ERR_NUMERIC, "Gamma not SPD (Cholesky failed)");
+  const double nt2 = ctx->hscal[SC_NT2];
+  const double rad = nt2 + ctx->hscal[SC_GS] - 2.0 * ctx->hscal[SC_MA];
+  if (!std::isfinite(rad)) return fail(ctx, CPD_ERR_NUMERIC, "non-finite residual");
+  ctx->last_r = std::sqrt(std::max(rad, 0.0)) / std::sqrt(nt2);
+  ctx->last_f = 1.0 - ctx->last_r;
+  ctx->have_fit = true;
+  for (int n = 0; n < ctx->N; n++) {
+    ctx->dA2[n] = ctx->hscal[SC_DA2 + n];
+    ctx->A2[n] = ctx->hscal[SC_A2 + n];
+  }
+  ctx->have_dA = true;
+  if (f_out) *f_out = ctx->last_f;
+  return CPD_OK;
+}
+
+bool pp_cond(const cpd_ctx* c) {
+  for (int n = 0; n < c->N; n++)
+    if (!(std::sqrt(c->dA2[n]) < c->opts.pp_eps * std::sqrt(c->A2[n]))) return false;
+  return true;
+}
+
+void free_pp(cpd_ctx* c) {
+  for (auto& kv : c->ops) dfree(c, kv.second);
+  c->ops.clear();
+  for (auto& p : c->Mp) dfree(c, p);
+  c->pp_valid = false;
+}
+
+cpd_status check_ctx(cpd_ctx* ctx) {
+  if (!ctx) return CPD_ERR_INVALID_ARG;
+  if (ctx->poisoned) return CPD_ERR_STATE;
+  cudaError_t e = cudaSetDevice(ctx->dev);
+  if (e != cudaSuccess) return fail(ctx, CPD_ERR_CUDA, cudaGetErrorString(e));
+  return CPD_OK;
+}
+
+cpd_status regular_sweep(cpd_ctx* ctx, bool msdt, double* f_out) {
+  const int N = ctx->N;
+  if (ctx->pp_regime || !ctx->sub_is_msdt || !msdt) {
+    // any factor change not made by msdt_sweep restarts the MSDT cycle
+    if (msdt && (ctx->pp_regime || !ctx->sub_is_msdt)) {
+      clear_subtree(ctx);
+      ctx->t = 0;
+    }
+  }
+  ctx->pp_regime = false;
+  if (msdt) {
+    ctx->sub_is_msdt = true;
+    for (int n = 0; n < N; n++) {
+      int64_t k = ctx->t / (N - 1);
+      int q = (int)(ctx->t % (N - 1));
+      if (q == 0 || !ctx->sub.active) {
+        int j = (int)(((k + 1) * (N - 1)) % N);
+        std::vector<int> served;
+        for (int d = 1; d < N; d++) served.push_back((j + d) % N);
+        TRY(start_subtree(ctx, j, {}, served));
+      }
+      if (ctx->sub.served[q] != n) return fail(ctx, CPD_ERR_INTERNAL, "MSDT schedule out of phase");
+      const double* leaf;
+      TRY(subtree_leaf(ctx, q, &leaf));
+      TRY(update_mode(ctx, n, const_cast<double*>(leaf), false));
+      ctx->t++;
+    }
+  } else {
+    ctx->sub_is_msdt = false;
+    clear_subtree(ctx);
+    ctx->t = 0;
+    const int h = (N + 1) / 2;
+    for (int n = 0; n < N; n++) {
+      if (n == 0) {
+        std::vector<int> pre, served;
+        for (int m = h; m < N - 1; m++) pre.push_back(m);
+        for (int m = 0; m < h; m++) served.push_back(m);
+        TRY(start_subtree(ctx, N - 1, pre, served));
+      } else if (n == h) {
+        std::vector<int> pre, served;
+        for (int m = 1; m < h; m++) pre.push_back(m);
+        for (int m = h; m < N; m++) served.push_back(m);
+        TRY(start_subtree(ctx, 0, pre, served));
+      }
+      int q = n < h ? n : n - h;
+      const double* leaf;
+      TRY(subtree_leaf(ctx, q, &leaf));
+      TRY(update_mode(ctx, n, const_cast<double*>(leaf), false));
+    }
+    clear_subtree(ctx);
+  }
+  TRY(finish_sweep(ctx, f_out));
+  return CPD_OK;
+}
+
+// produce all pair operators in `targets` (subsets of node.kept) from `node` (greedy
+// shared descent); node buffer is not freed here
+cpd_status pp_descend(cpd_ctx* ctx, const Node& node, std::vector<std::pair<int, int>> targets) {
+  if (node.kept.size() == 2) {
+    // the node is itself the operator (copy unless the caller hands over ownership)
+    return fail(ctx, CPD_ERR_INTERNAL, "pp_descend on a pair");
+  }
+  while (!targets.empty()) {
+    // choose the mode m whose removal keeps the most targets
+    int best = -1, bestc = -1;
+    for (int m : node.kept) {
+      int cnt = 0;
+      for (auto& pr : targets)
+        if (pr.first != m && pr.second != m) cnt++;
+      if (cnt > bestc) {
+        bestc = cnt;
+        best = m;
+      }
+    }
+    std::vector<std::pair<int, int>> sub, rest;
+    for (auto& pr : targets) (pr.first != best && pr.second != best ? sub : rest).push_back(pr);
+    Node child;
+    TRY(contract_modes(ctx, node, {best}, {best}, &child));
+    if (child.kept.size() == 2) {
+      ctx->ops[{child.kept[0], child.kept[1]}] = child.buf;
+    } else {
+      TRY(pp_descend(ctx, child, sub));
+      dfree(ctx, child.buf);
+    }
+    targets = rest;
+  }
+  return CPD_OK;
+}
+
+}  // namespace
+
+// ============================== C ABI ==============================================
+
+extern "C" {
+
+cpd_status cpd_opts_default(cpd_opts* o) {
+  if (!o) return CPD_ERR_INVALID_ARG;
+  std::memset(o, 0, sizeof(*o));
+  o->struct_size = sizeof(cpd_opts);
+  o->device = 0;
+  o->rank = 0;
+  o->world = 1;
+  o->nccl_unique_id = nullptr;
+  o->stream = nullptr;
+  o->pp_eps = 0.1;
+  o->reuse_root_in_pp_init = 1;
+  o->profile_phases = 0;
+  return CPD_OK;
+}
+
+cpd_status cpd_nccl_unique_id(void* out) {
+  if (!out) return CPD_ERR_INVALID_ARG;
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) {
+    g_init_error = ncclGetErrorString(r);
+    return CPD_ERR_NCCL;
+  }
+  static_assert(sizeof(ncclUniqueId) == CPD_NCCL_ID_BYTES, "nccl id size");
+  std::memcpy(out, &id, sizeof(id));
+  return CPD_OK;
+}
+
+const char* cpd_last_error(const cpd_ctx* c) { return c ? c->err.c_str() : g_init_error.c_str(); }
+
+cpd_status cpd_destroy(cpd_ctx* c) {
+  if (!c) return CPD_OK;
+  cudaSetDevice(c->dev);
+  clear_subtree(c);
+  free_pp(c);
+  for (auto* v : {&c->A, &c->Aold, &c->dA, &c->Mlast, &c->Ap, &c->Mp})
+    for (auto& p : *v) dfree(c, p);
+  dfree(c, c->S_all);
+  dfree(c, c->dS_all);
+  dfree(c, c->Lp);
+  dfree(c, c->W);
+  dfree(c, c->scal);
+  dfree(c, c->partial);
+  dfree(c, c->gather_tmp);
+  if (c->status) cudaFreeAsync(c->status, c->st);
+  cudaStreamSynchronize(c->st);
+  for (auto& r : c->pending) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : c->free_events) cudaEventDestroy(e);
+  if (c->hscal) cudaFreeHost(c->hscal);
+  if (c->hstatus) cudaFreeHost(c->hstatus);
+  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->own_stream && c->st) cudaStreamDestroy(c->st);
+  delete c;
+  return CPD_OK;
+}
+
+cpd_status cp_als_init(cpd_ctx** out, int N, const int64_t* shape, int R, const double* T_local_dev,
+                       const double* const* A0_host, const cpd_opts* opts) {
+  cpd_ctx* ctx = nullptr;
+  if (!out || !shape || !T_local_dev || !A0_host) return fail(ctx, CPD_ERR_INVALID_ARG, "null argument");
+  *out = nullptr;
+  if (N < 3 || N > CPD_MAX_ORDER) return fail(ctx, CPD_ERR_INVALID_ARG, "N must be in [3, 8]");
+  if (R < 1 || R > CPD_MAX_RANK) return fail(ctx, CPD_ERR_INVALID_ARG, "R must be in [1, 232]");
+  cpd_opts o;
+  cpd_opts_default(&o);
+  if (opts) {
+    if (opts->struct_size != sizeof(cpd_opts)) return fail(ctx, CPD_ERR_INVALID_ARG, "cpd_opts size mismatch");
+    o = *opts;
+  }
+  if (!(o.pp_eps > 0.0 && o.pp_eps < 1.0)) return fail(ctx, CPD_ERR_INVALID_ARG, "pp_eps must be in (0,1)");
+  if (o.world < 1 || o.rank < 0 || o.rank >= o.world) return fail(ctx, CPD_ERR_INVALID_ARG, "bad rank/world");
+  if (o.world > 1 && !o.nccl_unique_id) return fail(ctx, CPD_ERR_INVALID_ARG, "world > 1 needs nccl_unique_id");
+  for (int n = 0; n < N; n++)
+    if (shape[n] < 1 || !A0_host[n]) return fail(ctx, CPD_ERR_INVALID_ARG, "bad shape or factor");
+  if (shape[N - 1] % o.world != 0) return fail(ctx, CPD_ERR_INVALID_ARG, "s_N must be divisible by world");
+  for (int n = 0; n < N - 1; n++)
+    if (shape[n] % o.world != 0)
+      return fail(ctx, CPD_ERR_INVALID_ARG, "s_n must be divisible by world (reduce-scatter blocks)");
+
+  ctx = new cpd_ctx();
+  ctx->N = N;
+  ctx->R = R;
+  for (int n = 0; n < N; n++) ctx->shape[n] = shape[n];
+  ctx->rank = o.rank;
+  ctx->world = o.world;
+  ctx->sN_loc = shape[N - 1] / o.world;
+  ctx->lo = o.rank * ctx->sN_loc;
+  ctx->dev = o.device;
+  ctx->opts = o;
+  ctx->T = T_local_dev;
+  ctx->T_elems = ctx->sN_loc;
+  for (int n = 0; n < N - 1; n++) ctx->T_elems *= shape[n];
+
+  auto bail = [&](cpd_status s) {
+    g_init_error = ctx->err;
+    cpd_destroy(ctx);
+    return s;
+  };
+#define ICU(x)                                                                   \
+  do {                                                                           \
+    cudaError_t e_ = (x);                                                        \
+    if (e_ != cudaSuccess) {                                                     \
+      fail(ctx, CPD_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+      return bail(CPD_ERR_CUDA);                                                 \
+    }                                                                            \
+  } while (0)
+#define ITRY(x)                   \
+  do {                            \
+    cpd_status s_ = (x);          \
+    if (s_ != CPD_OK) return bail(s_); \
+  } while (0)
+
+  ICU(cudaSetDevice(ctx->dev));
+  {
+    int major = 0;
+    ICU(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, ctx->dev));
+    if (major != 10) {
+      fail(ctx, CPD_ERR_CUDA, "libcpd.so is built for sm_100a (B200) only");
+      return bail(CPD_ERR_CUDA);
+    }
+  }
+  if (o.stream) {
+    ctx->st = (cudaStream_t)o.stream;
+  } else {
+    ICU(cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking));
+    ctx->own_stream = true;
+  }
+  {
+    cudaMemPool_t pool;
+    ICU(cudaDeviceGetDefaultMemPool(&pool, ctx->dev));
+    uint64_t thr = UINT64_MAX;
+    ICU(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  }
+  if (o.world > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, o.nccl_unique_id, sizeof(id));
+    ncclResult_t r = ncclCommInitRank(&ctx->comm, o.world, id, o.rank);
+    if (r != ncclSuccess) {
+      fail(ctx, CPD_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+      return bail(CPD_ERR_NCCL);
+    }
+  }
+  const int64_t RR = (int64_t)R * R;
+  ctx->A.assign(N, nullptr);
+  ctx->Aold.assign(N, nullptr);
+  ctx->dA.assign(N, nullptr);
+  ctx->Mlast.assign(N, nullptr);
+  ctx->Ap.assign(N, nullptr);
+  ctx->Mp.assign(N, nullptr);
+  for (int n = 0; n < N; n++) {
+    int64_t e = ext(ctx, n) * R;
+    ITRY(dalloc(ctx, &ctx->A[n], e));
+    ITRY(dalloc(ctx, &ctx->Aold[n], e));
+    ITRY(dalloc(ctx, &ctx->dA[n], e));
+    ITRY(dalloc(ctx, &ctx->Mlast[n], e));
+    ITRY(dalloc(ctx, &ctx->Ap[n], e));
+  }
+  ITRY(dalloc(ctx, &ctx->S_all, N * RR));
+  ITRY(dalloc(ctx, &ctx->dS_all, N * RR));
+  ITRY(dalloc(ctx, &ctx->Lp, RR));
+  ITRY(dalloc(ctx, &ctx->W, RR));
+  ITRY(dalloc(ctx, &ctx->scal, SC_COUNT));
+  ITRY(dalloc(ctx, &ctx->partial, cpd::kNormBlocks));
+  ICU(cudaMallocAsync((void**)&ctx->status, sizeof(int) * CPD_MAX_ORDER, ctx->st));
+  ICU(cudaMemsetAsync(ctx->status, 0, sizeof(int) * CPD_MAX_ORDER, ctx->st));
+  ICU(cudaMemsetAsync(ctx->scal, 0, sizeof(double) * SC_COUNT, ctx->st));
+  ICU(cudaMemsetAsync(ctx->dS_all, 0, sizeof(double) * N * RR, ctx->st));
+  ICU(cudaMallocHost((void**)&ctx->hscal, sizeof(double) * SC_COUNT));
+  ICU(cudaMallocHost((void**)&ctx->hstatus, sizeof(int) * CPD_MAX_ORDER));
+  *out = ctx;  // provisional for cpd_set_factors
+  // ||T||^2 once, all-reduced
+  ICU(cpd::launch_norm2(ctx->T, ctx->T_elems, ctx->partial, ctx->scal + SC_NT2, ctx->st));
+  if (ctx->world > 1) {
+    ncclResult_t r = ncclAllReduce(ctx->scal + SC_NT2, ctx->scal + SC_NT2, 1, ncclDouble, ncclSum, ctx->comm, ctx->st);
+    if (r != ncclSuccess) {
+      *out = nullptr;
+      fail(ctx, CPD_ERR_NCCL, ncclGetErrorString(r));
+      return bail(CPD_ERR_NCCL);
+    }
+  }
+  cpd_status s = cpd_set_factors(ctx, A0_host);
+  if (s != CPD_OK) {
+    *out = nullptr;
+    return bail(s);
+  }
+  ICU(cudaStreamSynchronize(ctx->st));
+  ICU(cudaMemcpy(ctx->hscal, ctx->scal, sizeof(double) * SC_COUNT, cudaMemcpyDeviceToHost));
+  if (!(ctx->hscal[SC_NT2] > 0.0) || !std::isfinite(ctx->hscal[SC_NT2])) {
+    *out = nullptr;
+    fail(ctx, CPD_ERR_NUMERIC, "||T||^2 is zero or not finite");
+    return bail(CPD_ERR_NUMERIC);
+  }
+  // dA <- A (Alg. 2 line 2): the first regular sweep always precedes PP
+  for (int n = 0; n < N; n++) {
+    ctx->dA2[n] = 1.0;
+    ctx->A2[n] = 1.0;
+  }
+  ctx->have_dA = false;
+  return CPD_OK;
+#undef ICU
+#undef ITRY
+}
+
+cpd_status cpd_set_factors(cpd_ctx* ctx, const double* const* A_host) {
+  TRY(check_ctx(ctx));
+  if (!A_host) return fail(ctx, CPD_ERR_INVALID_ARG, "null factors");
+  const int R = ctx->R;
+  const int64_t RR = (int64_t)R * R;
+  for (int n = 0; n < ctx->N; n++) {
+    if (!A_host[n]) return fail(ctx, CPD_ERR_INVALID_ARG, "null factor");
+    const double* src = A_host[n] + (n == ctx->N - 1 ? ctx->lo * R : 0);
+    CU(cudaMemcpyAsync(ctx->A[n], src, sizeof(double) * ext(ctx, n) * R, cudaMemcpyHostToDevice, ctx->st));
+    CU(cpd::launch_gram(ctx->A[n], ctx->A[n], ext(ctx, n), R, ctx->S_all + n * RR, ctx->st));
+  }
+  if (ctx->world > 1) {
+    NC(ncclAllReduce(ctx->S_all + (ctx->N - 1) * RR, ctx->S_all + (ctx->N - 1) * RR, RR, ncclDouble,
+                     ncclSum, ctx->comm, ctx->st));
+  }
+  clear_subtree(ctx);
+  ctx->t = 0;
+  ctx->sub_is_msdt = false;
+  free_pp(ctx);
+  ctx->pp_regime = false;
+  ctx->have_dA = false;
+  CU(cudaStreamSynchronize(ctx->st));
+  return CPD_OK;
+}
+
+cpd_status msdt_sweep(cpd_ctx* ctx, double* fitness_out) {
+  TRY(check_ctx(ctx));
+  return regular_sweep(ctx, true, fitness_out);
+}
+
+cpd_status dt_sweep(cpd_ctx* ctx, double* fitness_out) {
+  TRY(check_ctx(ctx));
+  return regular_sweep(ctx, false, fitness_out);
+}
+
+cpd_status pp_init(cpd_ctx* ctx) {
+  TRY(check_ctx(ctx));
+  const int N = ctx->N;
+  free_pp(ctx);
+  // A_p <- A, dA <- 0 (Alg. 2 line 7)
+  for (int n = 0; n < N; n++) {
+    CU(cudaMemcpyAsync(ctx->Ap[n], ctx->A[n], sizeof(double) * ext(ctx, n) * ctx->R,
+                       cudaMemcpyDeviceToDevice, ctx->st));
+    CU(cudaMemsetAsync(ctx->dA[n], 0, sizeof(double) * ext(ctx, n) * ctx->R, ctx->st));
+  }
+  CU(cudaMemsetAsync(ctx->dS_all, 0, sizeof(double) * N * ctx->R * ctx->R, ctx->st));
+  // three first-level roots; reuse the live MSDT root when valid (P:384 footnote)
+  std::vector<int> js;
+  int live = (ctx->opts.reuse_root_in_pp_init && ctx->sub_is_msdt && ctx->sub.active && !ctx->pp_regime)
+                 ? ctx->sub.j
+                 : -1;
+  Node live_root;
+  if (live >= 0) {
+    auto it = ctx->sub.cache.find({0, (int)ctx->sub.served.size()});
+    if (it != ctx->sub.cache.end() && (int)it->second.kept.size() == N - 1) {
+      live_root = it->second;
+      ctx->sub.cache.erase(it);
+      js.push_back(live);
+    } else {
+      live = -1;
+    }
+  }
+  clear_subtree(ctx);
+  ctx->t = 0;
+  ctx->sub_is_msdt = false;
+  for (int j : {N - 1, 1, 0, 2, 3})
+    if ((int)js.size() < 3 && std::find(js.begin(), js.end(), j) == js.end()) js.push_back(j);
+  std::map<int, std::vector<std::pair<int, int>>> assign;
+  for (int a = 0; a < N; a++)
+    for (int b = a + 1; b < N; b++)
+      for (int j : js)
+        if (j != a && j != b) {
+          assign[j].push_back({a, b});
+          break;
+        }
+  // factors used for the operators are A_p (== A now)
+  for (int j : js) {
+    Node root;
+    if (j == live) {
+      root = live_root;
+    } else {
+      for (int m = 0; m < N; m++)
+        if (m != j) root.kept.push_back(m);
+      TRY(dalloc(ctx, &root.buf, node_elems(ctx, root.kept)));
+      TRY(ttm(ctx, j, root.buf));
+    }
+    if (root.kept.size() == 2) {
+      ctx->ops[{root.kept[0], root.kept[1]}] = root.buf;  // N = 3: the root is the operator
+    } else {
+      TRY(pp_descend(ctx, root, assign[j]));
+      dfree(ctx, root.buf);
+    }
+  }
+  if ((int)ctx->ops.size() != N * (N - 1) / 2) return fail(ctx, CPD_ERR_INTERNAL, "missing PP operators");
+  // M_p^(n) from a pair operator containing n
+  for (int n = 0; n < N; n++) {
+    int o = n == 0 ? 1 : 0;
+    int a = std::min(n, o), b = std::max(n, o);
+    TRY(dalloc(ctx, &ctx->Mp[n], ext(ctx, n) * ctx->R));
+    TRY(mttv(ctx, ctx->ops[{a, b}], {a, b}, o, ctx->Ap[o], ctx->Mp[n], 0));
+  }
+  CU(cudaStreamSynchronize(ctx->st));
+  drain_timers(ctx);
+  ctx->pp_valid = true;
+  ctx->pp_regime = true;
+  for (int n = 0; n < N; n++) ctx->dA2[n] = 0.0;
+  ctx->have_dA = true;
+  return CPD_OK;
+}
+
+cpd_status pp_approx_sweep(cpd_ctx* ctx, double* fitness_out, int* still_valid) {
+  TRY(check_ctx(ctx));
+  if (!ctx->pp_valid || !ctx->pp_regime) return fail(ctx, CPD_ERR_STATE, "pp_approx_sweep needs a valid pp_init");
+  const int N = ctx->N;
+  for (int n = 0; n < N; n++) {
+    double* Mt = nullptr;
+    TRY(dalloc(ctx, &Mt, ext(ctx, n) * ctx->R));
+    {
+      PhaseScope ps(ctx, PH_OTHER);
+      CU(cudaMemcpyAsync(Mt, ctx->Mp[n], sizeof(double) * ext(ctx, n) * ctx->R, cudaMemcpyDeviceToDevice,
+                         ctx->st));
+    }
+    for (int i = 0; i < N; i++) {
+      if (i == n) continue;
+      int a = std::min(n, i), b = std::max(n, i);
+      // U^(n,i) (Eq. 6): contract the operator's axis of mode i with dA^(i)
+      TRY(mttv(ctx, ctx->ops[{a, b}], {a, b}, i, ctx->dA[i], Mt, 1));
+    }
+    cpd_status s = update_mode(ctx, n, Mt, true);
+    dfree(ctx, Mt);
+    if (s != CPD_OK) return s;
+  }
+  TRY(finish_sweep(ctx, fitness_out));
+  if (still_valid) *still_valid = pp_cond(ctx) ? 1 : 0;
+  return CPD_OK;
+}
+
+cpd_status fitness(cpd_ctx* ctx, double* f_out) {
+  if (!ctx || !f_out) return CPD_ERR_INVALID_ARG;
+  if (!ctx->have_fit) return fail(ctx, CPD_ERR_STATE, "no completed sweep");
+  *f_out = ctx->last_f;
+  return CPD_OK;
+}
+
+cpd_status cpd_pp_condition(cpd_ctx* ctx, int* ok) {
+  if (!ctx || !ok) return CPD_ERR_INVALID_ARG;
+  *ok = ctx->have_dA ? (pp_cond(ctx) ? 1 : 0) : 0;
+  return CPD_OK;
+}
+
+static cpd_status gather_rows(cpd_ctx* ctx, int n0, const double* src_local, double* host_out) {
+  // src_local: for n0 < N-1 a full-size buffer whose own rows are valid after RS (Mlast)
+  // or fully valid (A); for N-1 the local slab rows.
+  const int R = ctx->R;
+  if (n0 == ctx->N - 1) {
+    if (ctx->world == 1) {
+      CU(cudaMemcpyAsync(host_out, src_local, sizeof(double) * ctx->sN_loc * R, cudaMemcpyDeviceToHost, ctx->st));
+    } else {
+      if (!ctx->gather_tmp) TRY(dalloc(ctx, &ctx->gather_tmp, ctx->shape[n0] * R));
+      NC(ncclAllGather(src_local, ctx->gather_tmp, ctx->sN_loc * R, ncclDouble, ctx->comm, ctx->st));
+      CU(cudaMemcpyAsync(host_out, ctx->gather_tmp, sizeof(double) * ctx->shape[n0] * R, cudaMemcpyDeviceToHost,
+                         ctx->st));
+    }
+  } else {
+    CU(cudaMemcpyAsync(host_out, src_local, sizeof(double) * ctx->shape[n0] * R, cudaMemcpyDeviceToHost, ctx->st));
+  }
+  CU(cudaStreamSynchronize(ctx->st));
+  return CPD_OK;
+}
+
+cpd_status cpd_get_factor(cpd_ctx* ctx, int n0, double* host_out) {
+  TRY(check_ctx(ctx));
+  if (n0 < 0 || n0 >= ctx->N || !host_out) return fail(ctx, CPD_ERR_INVALID_ARG, "bad mode");
+  return gather_rows(ctx, n0, ctx->A[n0], host_out);
+}
+
+cpd_status cpd_get_last_mttkrp(cpd_ctx* ctx, int n0, double* host_out) {
+  TRY(check_ctx(ctx));
+  if (n0 < 0 || n0 >= ctx->N || !host_out) return fail(ctx, CPD_ERR_INVALID_ARG, "bad mode");
+  if (n0 < ctx->N - 1 && ctx->world > 1) {
+    int64_t ro = rows_own(ctx, n0);
+    NC(ncclAllGather(ctx->Mlast[n0] + own_off(ctx, n0) * ctx->R, ctx->Mlast[n0], ro * ctx->R, ncclDouble,
+                     ctx->comm, ctx->st));
+  }
+  return gather_rows(ctx, n0, ctx->Mlast[n0], host_out);
+}
+
+cpd_status cpd_get_phase_ms(cpd_ctx* ctx, double out[5]) {
+  if (!ctx || !out) return CPD_ERR_INVALID_ARG;
+  cudaStreamSynchronize(ctx->st);
+  drain_timers(ctx);
+  for (int i = 0; i < 5; i++) out[i] = ctx->phase_ms[i];
+  return CPD_OK;
+}
+
+cpd_status cpd_get_counters(cpd_ctx* ctx, double out[6]) {
+  if (!ctx || !out) return CPD_ERR_INVALID_ARG;
+  for (int i = 0; i < 5; i++) out[i] = ctx->counters[i];
+  out[5] = (double)cpd::g_launches.load();
+  return CPD_OK;
+}
+
+cpd_status cpd_reset_counters(cpd_ctx* ctx) {
+  if (!ctx) return CPD_ERR_INVALID_ARG;
+  cudaStreamSynchronize(ctx->st);
+  drain_timers(ctx);
+  for (int i = 0; i < 5; i++) ctx->phase_ms[i] = ctx->counters[i] = 0.0;
+  return CPD_OK;
+}
+
+cpd_status cpd_debug_get_pp_operator(cpd_ctx* ctx, int a0, int b0, double* host_out) {
+  TRY(check_ctx(ctx));
+  if (!ctx->pp_valid) return fail(ctx, CPD_ERR_STATE, "no PP operators");
+  if (a0 < 0 || b0 <= a0 || b0 >= ctx->N || !host_out) return fail(ctx, CPD_ERR_INVALID_ARG, "bad pair");
+  auto it = ctx->ops.find({a0, b0});
+  if (it == ctx->ops.end()) return fail(ctx, CPD_ERR_INTERNAL, "operator missing");
+  int64_t e = ext(ctx, a0) * ext(ctx, b0) * ctx->R;
+  CU(cudaMemcpyAsync(host_out, it->second, sizeof(double) * e, cudaMemcpyDeviceToHost, ctx->st));
+  CU(cudaStreamSynchronize(ctx->st));
+  return CPD_OK;
+}
+
+// ---------------- generators and single-kernel entry points ----------------
+
+cpd_status cpd_gen_tensor(double* T_dev, int N, const int64_t* shape, int64_t lo, int64_t hi, int kind,
+                          const double* const* At_host, int Rt, double noise_std, uint64_t seed,
+                          void* stream) {
+  cpd_ctx* ctx = nullptr;
+  if (!T_dev || !shape || N < 1 || N > CPD_MAX_ORDER || lo < 0 || hi <= lo || hi > shape[N - 1])
+    return fail(ctx, CPD_ERR_INVALID_ARG, "bad generator arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t Q = 1;
+  for (int n = 0; n < N - 1; n++) Q *= shape[n];
+  const int64_t w = hi - lo;
+  auto cuerr = [&](cudaError_t e) {
+    g_init_error = cudaGetErrorString(e);
+    return CPD_ERR_CUDA;
+  };
+  cudaError_t e;
+  if (kind == 0 && Rt > 0) {
+    if (!At_host) return fail(ctx, CPD_ERR_INVALID_ARG, "kind 0 needs factors");
+    std::vector<double*> Ad(N - 1, nullptr);
+    double *KR = nullptr, *Bt = nullptr;
+    for (int n = 0; n < N - 1; n++) {
+      if ((e = cudaMalloc(&Ad[n], sizeof(double) * shape[n] * Rt)) != cudaSuccess) return cuerr(e);
+      if ((e = cudaMemcpy(Ad[n], At_host[n], sizeof(double) * shape[n] * Rt, cudaMemcpyHostToDevice)) != cudaSuccess)
+        return cuerr(e);
+    }
+    // B = A_N[lo:hi]^T  (Rt x w) so that T[q, z] = Σ_r KR[q, r] B[r, z]
+    std::vector<double> bt((size_t)Rt * w);
+    for (int64_t z = 0; z < w; z++)
+      for (int r = 0; r < Rt; r++) bt[(size_t)r * w + z] = At_host[N - 1][(lo + z) * Rt + r];
+    if ((e = cudaMalloc(&Bt, sizeof(double) * bt.size())) != cudaSuccess) return cuerr(e);
+    if ((e = cudaMemcpy(Bt, bt.data(), sizeof(double) * bt.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
+      return cuerr(e);
+    if ((e = cudaMalloc(&KR, sizeof(double) * Q * Rt)) != cudaSuccess) return cuerr(e);
+    if ((e = cpd::launch_krp(Ad.data(), shape, N - 1, Rt, KR, st)) != cudaSuccess) return cuerr(e);
+    if ((e = cpd::launch_ttm(KR, Q, Rt, 1, Bt, (int)w, T_dev, 0, st)) != cudaSuccess) return cuerr(e);
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuerr(e);
+    cudaFree(KR);
+    cudaFree(Bt);
+    for (auto p : Ad) cudaFree(p);
+  } else if (kind == 0) {
+    if ((e = cudaMemsetAsync(T_dev, 0, sizeof(double) * Q * w, st)) != cudaSuccess) return cuerr(e);
+  }
+  if (kind == 1 || noise_std != 0.0) {
+    if ((e = cpd::launch_noise(T_dev, Q, w, shape[N - 1], lo, kind, noise_std, seed, st)) != cudaSuccess)
+      return cuerr(e);
+  }
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuerr(e);
+  return CPD_OK;
+}
+
+cpd_status cpd_ttm(const double* T_dev, int64_t pre, int64_t K, int64_t post, const double* A_dev, int R,
+                   double* out_dev, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cpd::launch_ttm(T_dev, pre, K, post, A_dev, R, out_dev, 0, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    g_init_error = cudaGetErrorString(e);
+    return CPD_ERR_CUDA;
+  }
+  return CPD_OK;
+}
+
+cpd_status cpd_mttv(const double* X_dev, int64_t pre, int64_t K, int64_t post, int R, const double* v_dev,
+                    double* out_dev, int beta, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cpd::launch_mttv(X_dev, pre, K, post, R, v_dev, out_dev, beta, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    g_init_error = cudaGetErrorString(e);
+    return CPD_ERR_CUDA;
+  }
+  return CPD_OK;
+}
+
+}  // extern "C"

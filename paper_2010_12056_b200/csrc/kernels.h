@@ -1,0 +1,58 @@
+// Internal launchers of libcpd.so (sm_100a).  Citations: P:n = PAPER.md line n.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+
+namespace cpd {
+
+// number of kernels libcpd.so has launched (all launchers add to it)
+extern std::atomic<long long> g_launches;
+
+// ---- first-level TTM on FP64 tensor cores (DMMA, mma.sync .f64), P:320-322 ----------
+// out[i, n] = beta*out[i, n] + Σ_y X[addr(i, y)] * B[y, n],   i < pre*post, n < ncols
+// addr(i, y) = (i / post) * K * post + (i % post) + y * post   (X viewed as [pre, K, post])
+// B is K x ncols row-major (ld = ncols); out is (pre*post) x ncols row-major.
+cudaError_t launch_ttm(const double* X, int64_t pre, int64_t K, int64_t post, const double* B,
+                       int ncols, double* out, int beta, cudaStream_t st);
+
+// ---- batched TTV (mTTV) stream, P:320-322 ----------------------------------------------
+// out[p, c] = beta*out[p, c] + Σ_y X[(p*K + y)*C + c] * v[y*R + c % R],  C = post*R
+cudaError_t launch_mttv(const double* X, int64_t pre, int64_t K, int64_t post, int R,
+                        const double* v, double* out, int beta, cudaStream_t st);
+
+// ---- synthetic tensor (synth/__init__.py recipe) ------------------------------------
+// T[q, z] += std*normal(seed, g) (kind 0) or T = uniform(seed, g) (kind 1) with
+// g = q*sN + lo + z the global index, T viewed as [Q, w] (w = hi - lo).
+cudaError_t launch_noise(double* T, int64_t Q, int64_t w, int64_t sN, int64_t lo, int kind,
+                         double stdv, uint64_t seed, cudaStream_t st);
+// KR[q, r] = Π_{n<N-1} A_n[i_n(q), r]  (Khatri-Rao rows, first mode slowest)
+cudaError_t launch_krp(const double* const* A_dev, const int64_t* shape, int nf, int R,
+                       double* KR, cudaStream_t st);
+
+// ---- reductions ---------------------------------------------------------------------------
+// dst[0] = Σ x_i^2 over n elements (deterministic two-pass; partial needs kNormBlocks doubles)
+constexpr int kNormBlocks = 148 * 4;
+cudaError_t launch_norm2(const double* x, int64_t n, double* partial, double* dst, cudaStream_t st);
+// dst[0] = Σ x_i y_i (single CTA, fixed order) for small arrays; y == nullptr -> Σ x_i^2
+cudaError_t launch_dot(const double* x, const double* y, int64_t n, double* dst, cudaStream_t st);
+
+// ---- small dense R x R work (latency-bound) -----------------------------------------------
+// G[a][b] = Σ_i X[i][a] Y[i][b]  (S = A^T A; dS = A^T dA, Eq. 8)
+cudaError_t launch_gram(const double* X, const double* Y, int64_t rows, int R, double* G,
+                        cudaStream_t st);
+// Γ^(n) = ∗_{k≠n} S^(k) (Eq. 1) and its Cholesky factor, packed column-major lower, into
+// Lp (R(R+1)/2).  status[0] = 0 ok, 1 not SPD / non-finite.
+cudaError_t launch_gamma_chol(const double* S_all, int N, int n, int R, double* Lp, int* status,
+                              cudaStream_t st);
+// X[i,:] = M[i,:] Γ^{-1} via L (forward + backward substitution per row), rows x R.
+cudaError_t launch_trisolve(const double* Lp, const double* M, int64_t rows, int R, double* X,
+                            cudaStream_t st);
+// W = Σ_{i<j; i,j≠n} dS_i ∗ dS_j ∗ ∗_{k∉{i,j,n}} S_k (Eq. 7)
+cudaError_t launch_pp_w(const double* S_all, const double* dS_all, int N, int n, int R, double* W,
+                        cudaStream_t st);
+// z = x - y (n elements)
+cudaError_t launch_sub(const double* x, const double* y, double* z, int64_t n, cudaStream_t st);
+
+}  // namespace cpd

@@ -1,0 +1,259 @@
+// HBM-bound streams: batched TTV (mTTV) levels of the dimension trees and the PP
+// first-order corrections, the synthetic-tensor generator, and reductions.
+//
+// "Other contractions (transforming one intermediate into another
+// intermediate) are done via batched TTV"; "the mTTV kernel is vertical
+// communication (memory bandwidth) bound"; Eq. 6:
+// U^(n,i)(x,k) = Σ_y M_p^(n,i)(x,y,k) dA^(i)(y,k) is the same contraction.
+//
+// B200 design: intermediates are stored [kept modes..., R] with R
+// innermost, so contracting any kept mode reads X as [pre, K, C = post*R] and every
+// warp load is a contiguous 512-byte row segment (double2 per lane).  A CTA owns one
+// p and 64 columns; its 8 warps split the K rows (fixed interleave) and reduce through
+// shared memory in a fixed order (deterministic, no atomics).
+#include "kernels.h"
+
+namespace cpd {
+std::atomic<long long> g_launches{0};
+namespace {
+
+constexpr int MT_THREADS = 256;
+constexpr int MT_COLS = 64;  // columns per CTA (32 lanes x double2)
+
+template <bool VEC2>
+__global__ void __launch_bounds__(MT_THREADS)
+    mttv_kernel(const double* __restrict__ X, int64_t pre, int64_t K, int64_t C, int R,
+                const double* __restrict__ v, double* __restrict__ out, int beta, int nchunks) {
+  __shared__ double red[8][MT_COLS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t p = blockIdx.x / nchunks;
+  const int chunk = blockIdx.x % nchunks;
+  const int64_t cA = (int64_t)chunk * MT_COLS + (VEC2 ? 2 * lane : lane);
+  const int64_t cB = VEC2 ? cA + 1 : cA + 32;
+  const bool okA = cA < C, okB = cB < C;
+  const int rA = okA ? (int)(cA % R) : 0, rB = okB ? (int)(cB % R) : 0;
+  const double* Xp = X + p * K * C;
+  double sA = 0.0, sB = 0.0;
+  if (okA) {
+    int64_t y = warp;
+    // 4 independent rows in flight per warp
+    for (; y + 24 < K; y += 32) {
+      double a0, a1, a2, a3, b0, b1, b2, b3;
+      if (VEC2 && okB) {
+        double2 x0 = __ldcs(reinterpret_cast<const double2*>(Xp + (y)*C + cA));
+        double2 x1 = __ldcs(reinterpret_cast<const double2*>(Xp + (y + 8) * C + cA));
+        double2 x2 = __ldcs(reinterpret_cast<const double2*>(Xp + (y + 16) * C + cA));
+        double2 x3 = __ldcs(reinterpret_cast<const double2*>(Xp + (y + 24) * C + cA));
+        a0 = x0.x; b0 = x0.y; a1 = x1.x; b1 = x1.y; a2 = x2.x; b2 = x2.y; a3 = x3.x; b3 = x3.y;
+      } else {
+        a0 = __ldcs(Xp + (y)*C + cA);
+        a1 = __ldcs(Xp + (y + 8) * C + cA);
+        a2 = __ldcs(Xp + (y + 16) * C + cA);
+        a3 = __ldcs(Xp + (y + 24) * C + cA);
+        b0 = okB ? __ldcs(Xp + (y)*C + cB) : 0.0;
+        b1 = okB ? __ldcs(Xp + (y + 8) * C + cB) : 0.0;
+        b2 = okB ? __ldcs(Xp + (y + 16) * C + cB) : 0.0;
+        b3 = okB ? __ldcs(Xp + (y + 24) * C + cB) : 0.0;
+      }
+      sA = fma(a0, __ldg(v + (y)*R + rA), sA);
+      sA = fma(a1, __ldg(v + (y + 8) * R + rA), sA);
+      sA = fma(a2, __ldg(v + (y + 16) * R + rA), sA);
+      sA = fma(a3, __ldg(v + (y + 24) * R + rA), sA);
+      if (okB) {
+        sB = fma(b0, __ldg(v + (y)*R + rB), sB);
+        sB = fma(b1, __ldg(v + (y + 8) * R + rB), sB);
+        sB = fma(b2, __ldg(v + (y + 16) * R + rB), sB);
+        sB = fma(b3, __ldg(v + (y + 24) * R + rB), sB);
+      }
+    }
+    for (; y < K; y += 8) {
+      sA = fma(Xp[y * C + cA], v[y * R + rA], sA);
+      if (okB) sB = fma(Xp[y * C + cB], v[y * R + rB], sB);
+    }
+  }
+  if (VEC2) {
+    red[warp][2 * lane] = sA;
+    red[warp][2 * lane + 1] = sB;
+  } else {
+    red[warp][lane] = sA;
+    red[warp][lane + 32] = sB;
+  }
+  __syncthreads();
+  if (threadIdx.x < MT_COLS) {
+    int64_t c = (int64_t)chunk * MT_COLS + threadIdx.x;
+    if (c < C) {
+      double s = red[0][threadIdx.x];
+#pragma unroll
+      for (int w = 1; w < 8; w++) s += red[w][threadIdx.x];
+      double* o = out + p * C + c;
+      *o = beta ? *o + s : s;
+    }
+  }
+}
+
+// ---- SplitMix64 counter hash (spec in synth/__init__.py) ----
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ double hash_u(uint64_t key, uint64_t idx, uint64_t lane) {
+  return (double)(splitmix64(key ^ (2ull * idx + lane)) >> 11) * 0x1.0p-53;
+}
+
+__global__ void noise_kernel(double* __restrict__ T, int64_t Q, int64_t w, int64_t sN, int64_t lo,
+                             int kind, double stdv, uint64_t key) {
+  const int64_t n = Q * w;
+  for (int64_t li = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; li < n;
+       li += (int64_t)gridDim.x * blockDim.x) {
+    int64_t q = li / w, z = li - q * w;
+    uint64_t gidx = (uint64_t)(q * sN + lo + z);
+    if (kind == 1) {
+      T[li] = hash_u(key, gidx, 0);
+    } else {
+      double u1 = hash_u(key, gidx, 0), u2 = hash_u(key, gidx, 1);
+      double zn = sqrt(-2.0 * log1p(-u1)) * cos(2.0 * 3.141592653589793 * u2);
+      T[li] += stdv * zn;
+    }
+  }
+}
+
+struct KrpArgs {
+  const double* A[8];
+  int64_t s[8];
+};
+
+__global__ void krp_kernel(KrpArgs a, int nf, int R, int64_t rows, double* __restrict__ KR) {
+  const int64_t n = rows * R;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t q = e / R;
+    int r = (int)(e - q * R);
+    // decode q with the first mode slowest; multiply in ascending mode order
+    int64_t idx[8];
+    int64_t rem = q;
+    for (int m = nf - 1; m >= 0; m--) {
+      idx[m] = rem % a.s[m];
+      rem /= a.s[m];
+    }
+    double pr = a.A[0][idx[0] * R + r];
+    for (int m = 1; m < nf; m++) pr *= a.A[m][idx[m] * R + r];
+    KR[e] = pr;
+  }
+}
+
+__global__ void norm2_partial_kernel(const double* __restrict__ x, int64_t n, double* partial) {
+  __shared__ double red[32];
+  double s = 0.0;
+  const int64_t n2 = n / 2;
+  const double2* x2 = reinterpret_cast<const double2*>(x);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += stride) {
+    double2 v = __ldcs(x2 + i);
+    s = fma(v.x, v.x, s);
+    s = fma(v.y, v.y, s);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) s = fma(x[n - 1], x[n - 1], s);
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = (threadIdx.x < blockDim.x / 32) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) partial[blockIdx.x] = s;
+  }
+}
+
+// single CTA, fixed order: mode 0: dst = Σ x*y; mode 1: Σ x*x; mode 2: Σ x
+__global__ void dot_kernel(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
+                           double* dst, int mode) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+    s = mode == 2 ? s + x[i] : fma(x[i], mode == 0 ? y[i] : x[i], s);
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = (threadIdx.x < blockDim.x / 32) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) dst[0] = s;
+  }
+}
+
+__global__ void sub_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                           double* __restrict__ z, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    z[i] = x[i] - y[i];
+}
+
+}  // namespace
+
+cudaError_t launch_mttv(const double* X, int64_t pre, int64_t K, int64_t post, int R,
+                        const double* v, double* out, int beta, cudaStream_t st) {
+  const int64_t C = post * R;
+  if (pre <= 0 || C <= 0) return cudaSuccess;
+  if (K <= 0) return cudaErrorInvalidValue;
+  const bool vec2 = (C % 2) == 0 && ((uintptr_t)X % 16) == 0;
+  const int nchunks = (int)((C + MT_COLS - 1) / MT_COLS);
+  int64_t grid = pre * nchunks;
+  if (grid > 0x7fffffff) return cudaErrorInvalidConfiguration;
+  g_launches++;
+  if (vec2)
+    mttv_kernel<true><<<(unsigned)grid, MT_THREADS, 0, st>>>(X, pre, K, C, R, v, out, beta, nchunks);
+  else
+    mttv_kernel<false><<<(unsigned)grid, MT_THREADS, 0, st>>>(X, pre, K, C, R, v, out, beta, nchunks);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_noise(double* T, int64_t Q, int64_t w, int64_t sN, int64_t lo, int kind,
+                         double stdv, uint64_t seed, cudaStream_t st) {
+  // key = splitmix64(seed), computed on the host with the same mix
+  uint64_t z = seed + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  uint64_t key = z ^ (z >> 31);
+  g_launches++;
+  noise_kernel<<<148 * 8, 256, 0, st>>>(T, Q, w, sN, lo, kind, stdv, key);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_krp(const double* const* A_dev, const int64_t* shape, int nf, int R, double* KR,
+                       cudaStream_t st) {
+  KrpArgs a{};
+  int64_t rows = 1;
+  for (int m = 0; m < nf; m++) {
+    a.A[m] = A_dev[m];
+    a.s[m] = shape[m];
+    rows *= shape[m];
+  }
+  g_launches++;
+  krp_kernel<<<148 * 8, 256, 0, st>>>(a, nf, R, rows, KR);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_norm2(const double* x, int64_t n, double* partial, double* dst, cudaStream_t st) {
+  g_launches += 2;
+  norm2_partial_kernel<<<kNormBlocks, 512, 0, st>>>(x, n, partial);
+  dot_kernel<<<1, 1024, 0, st>>>(partial, nullptr, kNormBlocks, dst, 2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dot(const double* x, const double* y, int64_t n, double* dst, cudaStream_t st) {
+  g_launches++;
+  dot_kernel<<<1, 1024, 0, st>>>(x, y, n, dst, y ? 0 : 1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sub(const double* x, const double* y, double* z, int64_t n, cudaStream_t st) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) return cudaSuccess;
+  g_launches++;
+  sub_kernel<<<(unsigned)blocks, 256, 0, st>>>(x, y, z, n);
+  return cudaGetLastError();
+}
+
+}  // namespace cpd

@@ -1,0 +1,131 @@
+"""Python view of a cpd_ctx: the C-ABI entry points of include/cpd.h as methods.
+
+Names follow the ABI (cp_als_init, msdt_sweep, dt_sweep, pp_init, pp_approx_sweep,
+fitness, ...).  Only marshalling happens here.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, dptr, dptr_array, load_library
+
+
+class CPDecomposition:
+    """One rank's CP-ALS state on the device (a cpd_ctx).
+
+    T: torch CUDA float64 contiguous tensor = this rank's slab [s_1..s_{N-1}, s_N/world]
+       (borrowed: keep it alive as long as this object).
+    shape: global mode sizes; R: rank; A0: N global s_n x R host arrays.
+    """
+
+    def __init__(self, T, shape, R, A0, *, device=0, rank=0, world=1, nccl_id=None, stream=None,
+                 pp_eps=0.1, reuse_root_in_pp_init=True, profile_phases=False):
+        lib = load_library()
+        self.N = len(shape)
+        self.shape = tuple(int(s) for s in shape)
+        self.R = int(R)
+        self.world = world
+        self._T = T  # keep alive
+        o = _lib.cpd_opts()
+        check(lib.cpd_opts_default(C.byref(o)))
+        o.device, o.rank, o.world = device, rank, world
+        self._nccl_buf = None
+        if nccl_id is not None:
+            self._nccl_buf = C.create_string_buffer(bytes(nccl_id), _lib.CPD_NCCL_ID_BYTES)
+            o.nccl_unique_id = C.cast(self._nccl_buf, C.c_void_p)
+        o.stream = _lib._stream_ptr(stream)
+        o.pp_eps = float(pp_eps)
+        o.reuse_root_in_pp_init = int(bool(reuse_root_in_pp_init))
+        o.profile_phases = int(bool(profile_phases))
+        A0 = [np.ascontiguousarray(a, dtype=np.float64) for a in A0]
+        shp = (C.c_int64 * self.N)(*self.shape)
+        ctx = C.c_void_p()
+        check(lib.cp_als_init(C.byref(ctx), self.N, shp, self.R, C.c_void_p(T.data_ptr()),
+                              dptr_array(A0), C.byref(o)))
+        self._ctx = ctx
+        self._lib = lib
+
+    # -- sweeps ---------------------------------------------------------------------------
+    def msdt_sweep(self) -> float:
+        f = C.c_double()
+        check(self._lib.msdt_sweep(self._ctx, C.byref(f)), self._ctx)
+        return f.value
+
+    def dt_sweep(self) -> float:
+        f = C.c_double()
+        check(self._lib.dt_sweep(self._ctx, C.byref(f)), self._ctx)
+        return f.value
+
+    def pp_init(self):
+        check(self._lib.pp_init(self._ctx), self._ctx)
+
+    def pp_approx_sweep(self):
+        f, v = C.c_double(), C.c_int()
+        check(self._lib.pp_approx_sweep(self._ctx, C.byref(f), C.byref(v)), self._ctx)
+        return f.value, bool(v.value)
+
+    def fitness(self) -> float:
+        f = C.c_double()
+        check(self._lib.fitness(self._ctx, C.byref(f)), self._ctx)
+        return f.value
+
+    def pp_condition(self) -> bool:
+        v = C.c_int()
+        check(self._lib.cpd_pp_condition(self._ctx, C.byref(v)), self._ctx)
+        return bool(v.value)
+
+    # -- accessors ------------------------------------------------------------------------
+    def get_factor(self, n, out=None):
+        out = np.empty((self.shape[n], self.R)) if out is None else out
+        check(self._lib.cpd_get_factor(self._ctx, n, dptr(out)), self._ctx)
+        return out
+
+    def get_last_mttkrp(self, n):
+        out = np.empty((self.shape[n], self.R))
+        check(self._lib.cpd_get_last_mttkrp(self._ctx, n, dptr(out)), self._ctx)
+        return out
+
+    def set_factors(self, A):
+        A = [np.ascontiguousarray(a, dtype=np.float64) for a in A]
+        check(self._lib.cpd_set_factors(self._ctx, dptr_array(A)), self._ctx)
+
+    def phase_ms(self):
+        out = np.zeros(5)
+        check(self._lib.cpd_get_phase_ms(self._ctx, dptr(out)), self._ctx)
+        return dict(zip(["ttm", "mttv", "solve", "hadamard", "other"], out.tolist()))
+
+    def counters(self):
+        out = np.zeros(6)
+        check(self._lib.cpd_get_counters(self._ctx, dptr(out)), self._ctx)
+        return dict(zip(["ttm_flops", "ttm_launches", "stream_bytes", "stream_launches", "roots",
+                         "kernel_launches"],
+                        out.tolist()))
+
+    def reset_counters(self):
+        check(self._lib.cpd_reset_counters(self._ctx), self._ctx)
+
+    def debug_pp_operator(self, a, b):
+        sb = self.shape[b] // (self.world if b == self.N - 1 else 1)
+        sa = self.shape[a]
+        out = np.empty((sa, sb, self.R))
+        check(self._lib.cpd_debug_get_pp_operator(self._ctx, a, b, dptr(out)), self._ctx)
+        return out
+
+    def close(self):
+        if getattr(self, "_ctx", None) is not None and self._ctx.value:
+            self._lib.cpd_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def cp_als_init(T, shape, R, A0, **kw) -> CPDecomposition:
+    """cp_als_init of include/cpd.h returning the ctx wrapper."""
+    return CPDecomposition(T, shape, R, A0, **kw)

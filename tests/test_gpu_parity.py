@@ -1,0 +1,318 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle (-m gpu).
+
+Tolerance (north_star): 1e-10 relative, norm-wise per MTTKRP / factor (reading Q18)
+and relative per-sweep fitness.  Inputs: the seeded synth recipe on both sides.
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def cpd():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2010_12056_b200 as pkg
+    from paper_2010_12056_b200 import build
+    build.build()
+    pkg.load_library()
+    return pkg
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(np.asarray(b)), 1e-300)
+
+
+def dev_tensor(cpd, cfg, rank=0, world=1):
+    lo, hi = synth.slab_range(cfg.s, rank, world)
+    shp = [cfg.s] * (cfg.N - 1) + [hi - lo]
+    T = torch.empty(shp, dtype=torch.float64, device="cuda")
+    if cfg.kind == "uniform":
+        cpd.cpd_gen_tensor(T, cfg.shape, lo, hi, 1, None, 0.0, cfg.seed_noise)
+    else:
+        cpd.cpd_gen_tensor(T, cfg.shape, lo, hi, 0, synth.true_factors(cfg), np.sqrt(cfg.noise_var),
+                           cfg.seed_noise)
+    return T
+
+
+# ------------------------------- generator -----------------------------------------
+
+@pytest.mark.parametrize("cfg", [synth.config(1), synth.custom(4, 9, 3, seed=2), synth.custom(5, 5, 3, seed=3),
+                                 synth.custom(4, 7, 0, kind="uniform", true_rank=0, noise_var=0.0, seed=4),
+                                 synth.custom(5, 6, 4, noise_var=1e-3, collinearity=0.5, seed=6)])
+def test_generator_matches_oracle(cpd, cfg):
+    if cfg.kind == "uniform":
+        cfg = synth.Config(**{**cfg.__dict__, "R": 3})
+    T = dev_tensor(cpd, cfg).cpu().numpy()
+    To = O.make_tensor(cfg)
+    assert rel(T, To) <= 1e-14
+
+
+def test_generator_slabs(cpd):
+    cfg = synth.custom(3, 8, 3, noise_var=1e-2, seed=8)
+    full = dev_tensor(cpd, cfg).cpu().numpy()
+    parts = [dev_tensor(cpd, cfg, p, 4).cpu().numpy() for p in range(4)]
+    assert np.array_equal(np.concatenate(parts, axis=-1), full)
+
+
+# ------------------------------- single kernels --------------------------------------
+
+@pytest.mark.parametrize("shape,R", [((37, 29, 41), 8), ((16, 130, 12), 64), ((33, 20, 17), 13), ((9, 10, 11, 12), 100),
+                                     ((11, 7, 13), 200), ((6, 5, 3), 1), ((200, 3, 130), 33), ((5, 300, 4), 17)])
+def test_ttm_all_positions(cpd, shape, R):
+    rng = np.random.default_rng(sum(shape) + R)
+    Tn = rng.standard_normal(shape)
+    T = torch.from_numpy(Tn).cuda()
+    for j in range(len(shape)):
+        A = rng.standard_normal((shape[j], R))
+        pre = int(np.prod(shape[:j])) if j else 1
+        post = int(np.prod(shape[j + 1:])) if j < len(shape) - 1 else 1
+        out = torch.empty((pre * post, R), dtype=torch.float64, device="cuda")
+        cpd.cpd_ttm(T, pre, shape[j], post, torch.from_numpy(A).cuda(), R, out)
+        ref = O.ttm(Tn, A, j).reshape(pre * post, R)
+        assert rel(out.cpu().numpy(), ref) <= 1e-13, (j, rel(out.cpu().numpy(), ref))
+
+
+@pytest.mark.parametrize("shape,R", [((37, 29, 41), 8), ((16, 130), 64), ((33, 20, 17), 13), ((9, 10, 11, 5), 100),
+                                     ((3, 1000, 2), 7), ((4, 5), 200)])
+def test_mttv_all_axes(cpd, shape, R):
+    rng = np.random.default_rng(len(shape) * 7 + R)
+    Xn = rng.standard_normal(tuple(shape) + (R,))
+    X = torch.from_numpy(Xn).cuda()
+    for a in range(len(shape)):
+        v = rng.standard_normal((shape[a], R))
+        pre = int(np.prod(shape[:a])) if a else 1
+        post = int(np.prod(shape[a + 1:])) if a < len(shape) - 1 else 1
+        ref = O.mttv(Xn, v, a).reshape(pre, post * R)
+        out = torch.zeros((pre, post * R), dtype=torch.float64, device="cuda")
+        cpd.cpd_mttv(X, pre, shape[a], post, R, torch.from_numpy(v).cuda(), out, 0)
+        assert rel(out.cpu().numpy(), ref) <= 1e-13
+        # beta = 1 accumulates
+        cpd.cpd_mttv(X, pre, shape[a], post, R, torch.from_numpy(v).cuda(), out, 1)
+        assert rel(out.cpu().numpy(), 2 * ref) <= 1e-13
+
+
+# ------------------------------- sweeps ------------------------------------------------
+
+def _model(cpd, cfg, T, A0=None, **kw):
+    return cpd.cp_als_init(T, cfg.shape, cfg.R, synth.init_factors(cfg) if A0 is None else A0, **kw)
+
+
+def test_c1_full_trajectory(cpd):
+    """C1: 10 msdt_sweep, then pp_init + 5 forced pp_approx_sweep (reading Q14); every
+    M^(n) and every fitness compared with the oracle (full-trajectory parity)."""
+    cfg = synth.config(1)
+    T = dev_tensor(cpd, cfg)
+    To = O.make_tensor(cfg)
+    nt2 = O.norm2(To)
+    m = _model(cpd, cfg, T)
+    A = synth.init_factors(cfg)
+    for sweep in range(10):
+        f = m.msdt_sweep()
+        out = O.als_sweep(To, A, nt2)
+        for n in range(3):
+            assert rel(m.get_last_mttkrp(n), out["M"][n]) <= TOL, (sweep, n)
+        assert abs(f - out["f"]) <= TOL * abs(out["f"])
+        A = out["A"]
+    for n in range(3):
+        assert rel(m.get_factor(n), A[n]) <= TOL
+    m.pp_init()
+    st = O.pp_init(To, A)
+    for a, b in itertools.combinations(range(3), 2):
+        assert rel(m.debug_pp_operator(a, b), st.ops[(a, b)]) <= TOL
+    for k in range(5):
+        f, valid = m.pp_approx_sweep()
+        out = O.pp_approx_sweep(st, A, nt2, eps=0.1)
+        for n in range(3):
+            assert rel(m.get_last_mttkrp(n), out["M"][n]) <= TOL, (k, n)
+        assert abs(f - out["f"]) <= TOL * abs(out["f"])
+        assert valid == out["still_valid"]
+        A = out["A"]
+    m.close()
+
+
+@pytest.mark.parametrize("early", [1, 2, 3])
+def test_c1_early_pp_exercises_second_order(cpd, early):
+    """C1-early: pp_init after 1-3 sweeps, 3 forced PP sweeps (||V||/||M|| ~ 1e-2, so a
+    wrong Eq. 7/8 fails); state-synchronised: the oracle starts from the GPU factors."""
+    cfg = synth.config(1)
+    T = dev_tensor(cpd, cfg)
+    To = O.make_tensor(cfg)
+    nt2 = O.norm2(To)
+    m = _model(cpd, cfg, T)
+    for _ in range(early):
+        m.msdt_sweep()
+    A = [m.get_factor(n) for n in range(3)]
+    m.pp_init()
+    st = O.pp_init(To, A)
+    vmax = 0.0
+    for k in range(3):
+        Ag = [m.get_factor(n) for n in range(3)]
+        f, _ = m.pp_approx_sweep()
+        out = O.pp_approx_sweep(st, Ag, nt2)
+        for n in range(3):
+            assert rel(m.get_last_mttkrp(n), out["M"][n]) <= TOL, (k, n)
+            vmax = max(vmax, np.linalg.norm(out["V"][n]) / np.linalg.norm(out["M"][n]))
+        assert abs(f - out["f"]) <= TOL * abs(out["f"])
+    assert vmax > 1e-4  # the second-order term is really exercised
+    m.close()
+
+
+@pytest.mark.parametrize("N,s,R", [(4, 12, 5), (5, 6, 3), (3, 40, 24), (6, 4, 2)])
+def test_msdt_and_dt_sweeps_order_N(cpd, N, s, R):
+    cfg = synth.custom(N, s, R, noise_var=1e-4, seed=N * 10 + s)
+    T = dev_tensor(cpd, cfg)
+    To = O.make_tensor(cfg)
+    nt2 = O.norm2(To)
+    for kind in ("msdt", "dt"):
+        m = _model(cpd, cfg, T)
+        A = synth.init_factors(cfg)
+        for sweep in range(2 * (N - 1)):
+            f = m.msdt_sweep() if kind == "msdt" else m.dt_sweep()
+            out = O.als_sweep(To, A, nt2)
+            for n in range(N):
+                assert rel(m.get_last_mttkrp(n), out["M"][n]) <= TOL, (kind, sweep, n)
+            assert abs(f - out["f"]) <= TOL * abs(out["f"])
+            A = [m.get_factor(n) for n in range(N)]  # state-synchronised
+        c = m.counters()
+        roots = c["roots"]
+        if kind == "msdt":
+            assert roots == N * 2
+        else:
+            assert roots == 2 * 2 * (N - 1)
+        m.close()
+
+
+@pytest.mark.parametrize("N,s,R", [(4, 10, 4), (5, 6, 3)])
+def test_pp_order_N_state_synchronised(cpd, N, s, R):
+    cfg = synth.custom(N, s, R, noise_var=1e-3, seed=N + 40)
+    T = dev_tensor(cpd, cfg)
+    To = O.make_tensor(cfg)
+    nt2 = O.norm2(To)
+    m = _model(cpd, cfg, T)
+    for _ in range(2):
+        m.msdt_sweep()
+    A = [m.get_factor(n) for n in range(N)]
+    m.pp_init()
+    st = O.pp_init(To, A)
+    for a, b in itertools.combinations(range(N), 2):
+        assert rel(m.debug_pp_operator(a, b), st.ops[(a, b)]) <= TOL, (a, b)
+    for k in range(3):
+        Ag = [m.get_factor(n) for n in range(N)]
+        f, _ = m.pp_approx_sweep()
+        out = O.pp_approx_sweep(st, Ag, nt2)
+        for n in range(N):
+            assert rel(m.get_last_mttkrp(n), out["M"][n]) <= TOL, (k, n)
+        assert abs(f - out["f"]) <= TOL * abs(out["f"])
+    # back to a regular sweep after PP restarts the MSDT cycle and stays exact
+    Ag = [m.get_factor(n) for n in range(N)]
+    f = m.msdt_sweep()
+    out = O.als_sweep(To, Ag, nt2)
+    assert abs(f - out["f"]) <= TOL * abs(out["f"])
+    m.close()
+
+
+def test_pp_zero_perturbation_equals_exact(cpd):
+    """First mode of the first PP sweep sees dA = 0: M~^(1) = M^(1) at A_p exactly (Eq. 5)."""
+    cfg = synth.custom(3, 20, 4, noise_var=1e-4, seed=77)
+    T = dev_tensor(cpd, cfg)
+    To = O.make_tensor(cfg)
+    m = _model(cpd, cfg, T)
+    m.msdt_sweep()
+    A = [m.get_factor(n) for n in range(3)]
+    m.pp_init()
+    m.pp_approx_sweep()
+    assert rel(m.get_last_mttkrp(0), O.mttkrp(To, A, 0)) <= TOL
+    m.close()
+
+
+def test_pp_root_reuse_changes_only_rounding(cpd):
+    cfg = synth.custom(4, 10, 4, noise_var=1e-3, seed=91)
+    T = dev_tensor(cpd, cfg)
+    res = []
+    for reuse in (True, False):
+        m = _model(cpd, cfg, T, reuse_root_in_pp_init=reuse)
+        m.msdt_sweep()
+        m.pp_init()
+        c = m.counters()
+        f, _ = m.pp_approx_sweep()
+        res.append((f, c["roots"]))
+        m.close()
+    assert abs(res[0][0] - res[1][0]) <= TOL
+    assert res[0][1] == res[1][1] - 1   # one first-level TTM saved (P:384 footnote)
+
+
+def test_errors(cpd):
+    cfg = synth.custom(3, 8, 3, seed=5)
+    T = dev_tensor(cpd, cfg)
+    m = _model(cpd, cfg, T)
+    with pytest.raises(cpd.CPDError) as e:
+        m.pp_approx_sweep()
+    assert e.value.status == 2
+    with pytest.raises(cpd.CPDError) as e:
+        m.get_factor(7, out=np.empty((8, 3)))
+    assert e.value.status == 1
+    m.close()
+    with pytest.raises(cpd.CPDError) as e:
+        cpd.cp_als_init(T, cfg.shape, 300, synth.init_factors(cfg))
+    assert e.value.status == 1
+    # rank-deficient factors -> Γ not SPD
+    A0 = synth.init_factors(cfg)
+    A0 = [a.copy() for a in A0]
+    A0[1][:, 1] = 0.0
+    A0[2][:, 1] = 0.0
+    m = _model(cpd, cfg, T, A0=A0)
+    with pytest.raises(cpd.CPDError) as e:
+        m.msdt_sweep()
+    assert e.value.status == 3
+    m.close()
+
+
+def test_set_factors_restarts_cycle(cpd):
+    cfg = synth.custom(3, 16, 4, noise_var=1e-4, seed=12)
+    T = dev_tensor(cpd, cfg)
+    To = O.make_tensor(cfg)
+    m = _model(cpd, cfg, T)
+    m.msdt_sweep()
+    A = [a + 0.01 for a in synth.init_factors(cfg)]
+    m.set_factors(A)
+    f = m.msdt_sweep()
+    out = O.als_sweep(To, A)
+    assert abs(f - out["f"]) <= TOL * abs(out["f"])
+    m.close()
+
+
+# ------------------------------- full-size sampled checks --------------------------------
+
+@pytest.mark.parametrize("c", [2, 3, 4, 5])
+def test_full_size_sampled_rows(cpd, c):
+    """BASELINE configs at full size: one msdt_sweep; sampled rows of every M^(n) against
+    the oracle's slice-by-slice explicit-KRP rows with the GPU's input factors."""
+    cfg = synth.config(c)
+    free, total = torch.cuda.mem_get_info()
+    if free < 4 * 8 * cfg.numel:
+        pytest.skip("not enough device memory")
+    T = dev_tensor(cpd, cfg)
+    m = _model(cpd, cfg, T)
+    A0 = synth.init_factors(cfg)
+    m.msdt_sweep()
+    A1 = [m.get_factor(n) for n in range(cfg.N)]
+    rng = np.random.default_rng(c)
+    for n in range(cfg.N):
+        Ause = A1[:n] + A0[n:]   # modes < n already updated in this sweep
+        rows = rng.choice(cfg.s, 2 if c == 5 else 3, replace=False)
+        ref = O.mttkrp_rows(cfg, Ause, n, rows)
+        got = m.get_last_mttkrp(n)[rows]
+        assert rel(got, ref) <= TOL, (n, rel(got, ref))
+    m.close()
+    del T
+    torch.cuda.empty_cache()
