@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""Benchmark of the MSDT / PP CP-ALS hot path on B200 (one process per GPU).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+A STEP is one pass over every row of SURVEY §8(a) on the BASELINE workload
+(default configs[1] = C2: 1024^3 FP64, exact rank 64 + N(0,1e-4) noise, R = 64):
+    (N-1) msdt_sweep   = one full MSDT cycle (N roots for N-1 sweeps, §III)
+    pp_init            = PP operators (Alg. 2 lines 6-9)
+    (N-1) pp_approx_sweep (Alg. 2 lines 11-16, forced)
+    1 dt_sweep         = the standard dimension-tree baseline (Fig. 1a)
+`value` = device time per MSDT sweep (ms, the metric's first item); the PP-approx,
+PP-init and DT per-sweep times are reported beside it.  For N > 1 the tensor is
+split along its last mode (strong scaling, Alg. 3 / Alg. 4 on a 1-D grid); times
+are the max over ranks.  T (8.6 GB for C2) is far larger than L2, so no flush is
+needed between timed iterations.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "CP-ALS per-sweep time (MSDT, PP-approx) and TTM FP64-TC % / TTV HBM GB/s at 1-8 GPU"
+FP64_PEAK_TFLOPS = 37.1   # measured DMMA m8n8k4 (profiles/r01_peaks_fp64.json); MEASURED_PEAKS.json has no FP64 entry
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return json.load(open(p))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "_source": "fallback (B200_PROFILING.md)"}
+
+
+def fp64_peak():
+    p = os.path.join(ROOT, "profiles", "r01_peaks_fp64.json")
+    try:
+        d = json.load(open(p))
+        return max(v for k, v in d.items() if k.startswith("dmma")), "measured DMMA (profiles/r01_peaks_fp64.json)"
+    except Exception:
+        return FP64_PEAK_TFLOPS, "measured DMMA (DESIGN.md)"
+
+
+def ncu_traffic(name):
+    """dram bytes per launch from a committed `ncu --set full` summary, or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(p)).get(name)
+    except Exception:
+        return None
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                self.out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.out = ""
+
+    def summary(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], [], set()
+        for line in (self.out or "").strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def make_slab(cpd, torch, cfg, rank, world, stream):
+    lo, hi = synth.slab_range(cfg.s, rank, world)
+    T = torch.empty([cfg.s] * (cfg.N - 1) + [hi - lo], dtype=torch.float64, device="cuda")
+    if cfg.kind == "uniform":
+        cpd.cpd_gen_tensor(T, cfg.shape, lo, hi, 1, None, 0.0, cfg.seed_noise, stream)
+    else:
+        cpd.cpd_gen_tensor(T, cfg.shape, lo, hi, 0, synth.true_factors(cfg), math.sqrt(cfg.noise_var),
+                           cfg.seed_noise, stream)
+    return T
+
+
+def oracle_sample(cfg, w):
+    """Bounded CPU sample: one oracle als_sweep on a [s,..,s,w] slab of T (one piece of
+    the 1-D partition); a full sweep is s/w such pieces (Alg. 3 local MTTKRPs)."""
+    import oracle as O
+    T = O.make_tensor_block(cfg, [(0, cfg.s)] * (cfg.N - 1) + [(0, w)])
+    A = synth.init_factors(cfg)
+    A[-1] = np.ascontiguousarray(A[-1][:w])
+    return O, T, A
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def time_oracle(cfg, n_sweeps, w):
+    from threadpoolctl import threadpool_limits
+    cores = cpu_cores()
+    O, T, A = oracle_sample(cfg, w)
+    ts = []
+    with threadpool_limits(limits=cores):
+        for _ in range(n_sweeps):
+            t0 = time.perf_counter()
+            out = O.als_sweep(T, A)
+            ts.append(time.perf_counter() - t0)
+            A = out["A"]
+    return ts, cores
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle as it stands (the tier's reference arm)."""
+    if rank != 0:
+        return
+    cfg = synth.config(args.config)
+    w = args.oracle_slab
+    ts, cores = time_oracle(cfg, args.warmup + args.steps, w)
+    timed = ts[args.warmup:]
+    per_sweep_ms = 1e3 * statistics.mean(timed) * (cfg.s / w)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": per_sweep_ms, "unit": "ms/sweep (MSDT)",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": per_sweep_ms * (cfg.N - 1), "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "N": cfg.N, "s": cfg.s, "R": cfg.R, "l2": "inputs larger than L2"},
+        "cpu_baseline": {"value": per_sweep_ms, "unit": "ms/sweep (MSDT)", "cores": cores, "kind": "oracle",
+                         "sample": f"oracle als_sweep (explicit unfolding + explicit KRP + Cholesky) on a "
+                                   f"{'x'.join([str(cfg.s)] * (cfg.N - 1))}x{w} slab, x{cfg.s // w} slabs "
+                                   f"(1-D partition pieces; linear extrapolation)"},
+        "e2e": {"value": per_sweep_ms, "unit": "ms/sweep (MSDT)", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2, help="BASELINE.json configs[c-1]")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--presweeps", type=int, default=60, help="max untimed MSDT sweeps before the steps")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--oracle-slab", type=int, default=16)
+    args = ap.parse_args()
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2010_12056_b200 as cpd
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.Stream()
+    cfg = synth.config(args.config)
+    N = cfg.N
+    peaks = load_peaks()
+    fp64, fp64_src = fp64_peak()
+
+    nccl_id = None
+    if world > 1:
+        obj = [cpd.cpd_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+
+    with torch.cuda.stream(stream):
+        T = make_slab(cpd, torch, cfg, rank, world, stream)
+    torch.cuda.synchronize()
+    A0 = synth.init_factors(cfg)
+    m = cpd.cp_als_init(T, cfg.shape, cfg.R, A0, device=local, rank=rank, world=world, nccl_id=nccl_id,
+                        stream=stream, pp_eps=0.2 if args.config == 4 else 0.1, profile_phases=True)
+    # untimed: converge until the PP entry condition holds (Alg. 2 line 5), so the forced
+    # PP sweeps of each step run in their regime of validity
+    pre = 0
+    f = None
+    while pre < args.presweeps:
+        f = m.msdt_sweep()
+        pre += 1
+        if m.pp_condition():
+            break
+    pp_ok = m.pp_condition()
+
+    def ev():
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        return e
+
+    def one_step(rec):
+        e0 = ev()
+        for _ in range(N - 1):
+            m.msdt_sweep()
+        e1 = ev()
+        m.pp_init()
+        e2 = ev()
+        for _ in range(N - 1):
+            m.pp_approx_sweep()
+        e3 = ev()
+        m.dt_sweep()
+        e4 = ev()
+        rec.append((e0, e1, e2, e3, e4))
+
+    junk = []
+    clk = Clocks(local).__enter__()   # sampler starts before the warm-up so the timed region is covered
+    for _ in range(args.warmup):
+        one_step(junk)
+    torch.cuda.synchronize()
+    m.reset_counters()
+    launches0 = m.counters()["kernel_launches"]
+    recs = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    if True:
+        t_start = ev()
+        for _ in range(args.steps):
+            one_step(recs)
+        t_end = ev()
+        torch.cuda.synchronize()
+    clk.__exit__(None, None, None)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    total_ms = t_start.elapsed_time(t_end)
+    parts = np.array([[a.elapsed_time(b) for a, b in zip(r[:-1], r[1:])] for r in recs])  # steps x 4
+    ph = m.phase_ms()
+    ctr = m.counters()
+    launches = int(ctr["kernel_launches"] - launches0)
+    part_means = parts.mean(axis=0)
+    vals = np.array([total_ms, part_means[0] / (N - 1), part_means[1], part_means[2] / (N - 1), part_means[3]])
+    if world > 1:
+        t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        vals = t.cpu().numpy()
+    total_ms, msdt_ms, ppinit_ms, ppapprox_ms, dt_ms = vals.tolist()
+
+    # roofline of the dominant kernel (the first-level TTM on DMMA) and of the streams
+    ttm_launch_flops = ctr["ttm_flops"] / max(ctr["ttm_launches"], 1)
+    ttm_ms = ph["ttm"] / max(ctr["ttm_launches"], 1)
+    ttm_tf = ttm_launch_flops / (ttm_ms * 1e-3) / 1e12 if ttm_ms > 0 else None
+    st_launch_bytes = ctr["stream_bytes"] / max(ctr["stream_launches"], 1)
+    st_ms = ph["mttv"] / max(ctr["stream_launches"], 1)
+    st_gbs = st_launch_bytes / (st_ms * 1e-3) / 1e9 if st_ms > 0 else None
+    step_ms_dev = sum(ph.values()) / args.steps
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, cpd, torch, cfg, T, m, rank, world, local, nccl_id, stream)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ts, cores = time_oracle(cfg, 2, args.oracle_slab)
+        v = 1e3 * min(ts) * (cfg.s / args.oracle_slab)
+        cpu = {"value": v, "unit": "ms/sweep (MSDT)", "cores": cores, "kind": "oracle",
+               "sample": f"oracle als_sweep on a {'x'.join([str(cfg.s)] * (N - 1))}x{args.oracle_slab} slab "
+                         f"(best of 2), x{cfg.s // args.oracle_slab} slabs of the 1-D partition (linear extrapolation)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": msdt_ms, "unit": "ms/sweep (MSDT)", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "N": N, "s": cfg.s, "R": cfg.R,
+                       "tensor": f"exact rank {cfg.true_rank} + N(0,{cfg.noise_var}) noise" if cfg.kind == "kruskal"
+                       else "i.i.d. U(0,1)", "parallelism": f"1-D split of mode N over {world} GPU(s)",
+                       "step": f"{N - 1} msdt_sweep + pp_init + {N - 1} pp_approx_sweep + 1 dt_sweep",
+                       "l2": "inputs larger than L2 (no flush)", "presweeps": pre, "pp_condition_held": pp_ok,
+                       "fitness_before_steps": f},
+            "sweeps_ms": {"msdt": msdt_ms, "pp_approx": ppapprox_ms, "pp_init": ppinit_ms, "dt": dt_ms,
+                          "dt_over_msdt": dt_ms / msdt_ms, "dt_over_pp_approx": dt_ms / ppapprox_ms},
+            "phase_ms_per_step": {k: v / args.steps for k, v in ph.items()},
+            "roofline": {"kernel": "ttm_dmma (first-level TTM, DMMA.8x8x4)", "bound": "tensor", "achieved": ttm_tf,
+                         "peak": fp64, "peak_source": fp64_src, "unit": "TFLOP/s",
+                         "frac": (ttm_tf / fp64) if ttm_tf else None,
+                         "traffic": ncu_traffic("ttm_dmma"), "flops_per_launch": ttm_launch_flops,
+                         "avg_launch_ms": ttm_ms, "launches": int(ctr["ttm_launches"])},
+            "roofline_stream": {"kernel": "mttv (mTTV levels + PP U-stream)", "bound": "hbm", "achieved": st_gbs,
+                                "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                                "frac": (st_gbs / peaks["hbm_gbs"]) if st_gbs and peaks.get("hbm_gbs") else None,
+                                "traffic": ncu_traffic("mttv"), "bytes_per_launch": st_launch_bytes,
+                                "avg_launch_ms": st_ms, "launches": int(ctr["stream_launches"])},
+            "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
+            "device_ms_per_step_phases": step_ms_dev,
+        }
+        print(json.dumps(line), flush=True)
+    m.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, cpd, torch, cfg, T, m, rank, world, local, nccl_id, stream):
+    """Same metric through the public API with HOST buffers: per step, H2D of the
+    tensor slab and of the factors from pinned memory, one MSDT cycle ((N-1) sweeps),
+    D2H of every factor and the fitness.  e2e value = step time / (N-1) sweeps."""
+    import torch.distributed as dist
+    N = cfg.N
+    A_host = [m.get_factor(n) for n in range(N)]
+    T_host = torch.empty(T.shape, dtype=torch.float64, pin_memory=True)
+    T_host.copy_(T)
+    T_dev = torch.empty_like(T)
+    T_dev.copy_(T)
+    m2 = cpd.cp_als_init(T_dev, cfg.shape, cfg.R, A_host, device=local, rank=rank, world=world,
+                         nccl_id=nccl_id if world == 1 else _new_id(cpd, dist, rank), stream=stream)
+    outs = [np.empty((cfg.s, cfg.R)) for _ in range(N)]
+    pinned_A = [torch.from_numpy(a).pin_memory().numpy() for a in A_host]
+    ts = []
+    for it in range(args.warmup + args.steps):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        with torch.cuda.stream(stream):
+            T_dev.copy_(T_host, non_blocking=True)
+        m2.set_factors(pinned_A)
+        for _ in range(N - 1):
+            m2.msdt_sweep()
+        for n in range(N):
+            m2.get_factor(n, outs[n])
+        m2.fitness()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if it >= args.warmup:
+            ts.append(e0.elapsed_time(e1))
+    v = statistics.mean(ts) / (N - 1)
+    if world > 1:
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        v = float(t.item())
+    m2.close()
+    h2d = T_host.numel() * 8 + sum(a.size * 8 for a in A_host)
+    d2h = sum(a.size * 8 for a in A_host) + 8
+    return {"value": v, "unit": "ms/sweep (MSDT)", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "step": f"H2D T slab + factors (pinned), {N - 1} msdt_sweep, D2H factors + fitness"}
+
+
+def _new_id(cpd, dist, rank):
+    obj = [cpd.cpd_nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+if __name__ == "__main__":
+    main()

@@ -24,7 +24,7 @@ import synth
 
 __all__ = [
     "unfold", "khatri_rao", "mttkrp", "gram", "gamma", "solve", "norm2", "fitness_eq3",
-    "residual_eq2", "kruskal", "make_tensor", "make_tensor_slice", "mttkrp_rows",
+    "residual_eq2", "kruskal", "make_tensor", "make_tensor_block", "make_tensor_slice", "mttkrp_rows",
     "als_sweep", "PPState", "pp_init", "pp_approx_sweep", "pp_condition", "pp_controller_run",
     "ttm", "mttv", "MSDTModel", "DTModel", "msdt_roots", "par_als_sweep_sim",
     "par_pp_approx_sweep_sim", "dS_of",

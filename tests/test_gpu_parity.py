@@ -299,7 +299,7 @@ def test_full_size_sampled_rows(cpd, c):
     the oracle's slice-by-slice explicit-KRP rows with the GPU's input factors."""
     cfg = synth.config(c)
     free, total = torch.cuda.mem_get_info()
-    if free < 4 * 8 * cfg.numel:
+    if free < 1.5 * 8 * cfg.numel + 16e9:
         pytest.skip("not enough device memory")
     T = dev_tensor(cpd, cfg)
     m = _model(cpd, cfg, T)
