@@ -66,7 +66,7 @@ def ncu_traffic(name):
 class Clocks:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+    Q = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
@@ -76,7 +76,7 @@ class Clocks:
     def __enter__(self):
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.p = None
@@ -91,13 +91,22 @@ class Clocks:
             except Exception:
                 self.out = ""
 
-    def summary(self):
+    def summary(self, t0=None, t1=None):
+        """Samples whose timestamp falls inside [t0, t1] (wall clock of the timed region)."""
+        import datetime
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         sm, mx, reasons = [], [], set()
         for line in (self.out or "").strip().splitlines():
             f = [x.strip() for x in line.split(",")]
-            if len(f) < 6:
+            if len(f) < 7:
                 continue
+            try:
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                ts = None
+            if ts is not None and t0 is not None and not (t0 - 0.06 <= ts <= t1 + 0.06):
+                continue
+            f = f[1:]
             try:
                 sm.append(float(f[0]))
                 mx.append(float(f[1]))
@@ -188,7 +197,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=2, help="BASELINE.json configs[c-1]")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -269,11 +278,13 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     if True:
+        wall0 = time.time()
         t_start = ev()
         for _ in range(args.steps):
             one_step(recs)
         t_end = ev()
         torch.cuda.synchronize()
+        wall1 = time.time()
     clk.__exit__(None, None, None)
     if world > 1:
         dist.barrier()
@@ -336,7 +347,7 @@ def main():
                                 "frac": (st_gbs / peaks["hbm_gbs"]) if st_gbs and peaks.get("hbm_gbs") else None,
                                 "traffic": ncu_traffic("mttv"), "bytes_per_launch": st_launch_bytes,
                                 "avg_launch_ms": st_ms, "launches": int(ctr["stream_launches"])},
-            "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
+            "gpu_launches": launches, "clocks": clk.summary(wall0, wall1), "e2e": e2e, "cpu_baseline": cpu,
             "device_ms_per_step_phases": step_ms_dev,
         }
         print(json.dumps(line), flush=True)

@@ -38,6 +38,8 @@ namespace {
 
 thread_local std::string g_init_error;
 
+constexpr int64_t kMttvWs = 1 << 22;  // doubles (32 MB) of mTTV K-split partials
+
 enum Phase { PH_TTM = 0, PH_MTTV = 1, PH_SOLVE = 2, PH_HAD = 3, PH_OTHER = 4 };
 
 struct Node {
@@ -77,6 +79,10 @@ struct cpd_ctx {
   double* dS_all = nullptr;  // N x R x R
   double* Lp = nullptr;      // packed Cholesky factor
   double* W = nullptr;       // R x R
+  double* ws_gram = nullptr; // 2 x 16 x R x R Gram partials
+  double* ws_mttv = nullptr; // mTTV K-split partials
+  double* st_part = nullptr; // update-stats block partials
+  unsigned int* st_counter = nullptr;
   double* scal = nullptr;    // device scalars (see SC_*)
   double* partial = nullptr;
   int* status = nullptr;     // N ints, Cholesky status per mode
@@ -227,7 +233,7 @@ cpd_status mttv(cpd_ctx* ctx, const double* X, const std::vector<int>& kept, int
   for (int q = a + 1; q < (int)kept.size(); q++) post *= ext(ctx, kept[q]);
   int64_t K = ext(ctx, m);
   PhaseScope ps(ctx, PH_MTTV);
-  CU(cpd::launch_mttv(X, pre, K, post, ctx->R, v, out, beta, ctx->st));
+  CU(cpd::launch_mttv(X, pre, K, post, ctx->R, v, out, beta, ctx->ws_mttv, kMttvWs, ctx->st));
   double C = (double)post * ctx->R;
   ctx->counters[2] += 8.0 * ((double)pre * K * C + (double)pre * C * (beta ? 2 : 1) + (double)K * ctx->R);
   ctx->counters[3] += 1;
@@ -411,17 +417,15 @@ cpd_status update_mode(cpd_ctx* ctx, int n, double* Mloc, bool pp) {
   {
     PhaseScope ps(ctx, PH_HAD);
     const double* base = pp ? ctx->Ap[n] : ctx->Aold[n];
-    CU(cpd::launch_sub(ctx->A[n], base, ctx->dA[n], rows_full * R, ctx->st));
-    CU(cpd::launch_gram(ctx->A[n], ctx->A[n], rows_full, R, ctx->S_all + n * RR, ctx->st));
-    if (pp) CU(cpd::launch_gram(ctx->A[n], ctx->dA[n], rows_full, R, ctx->dS_all + n * RR, ctx->st));
-    CU(cpd::launch_dot(ctx->dA[n], nullptr, rows_full * R, ctx->scal + SC_DA2 + n, ctx->st));
-    CU(cpd::launch_dot(ctx->A[n], nullptr, rows_full * R, ctx->scal + SC_A2 + n, ctx->st));
+    // dA, ||dA||^2, ||A||^2 (and <M^(N), A^(N)> of Eq. 3 for the last mode) in one pass
+    const bool last = n == ctx->N - 1;
+    CU(cpd::launch_update_stats(ctx->A[n], base, ctx->dA[n], last ? Mown : nullptr, rows_full * R, ctx->st_part,
+                                ctx->st_counter, ctx->scal + SC_DA2 + n, ctx->scal + SC_A2 + n,
+                                ctx->scal + SC_MA, ctx->st));
+    CU(cpd::launch_gram(ctx->A[n], ctx->A[n], pp ? ctx->dA[n] : nullptr, rows_full, R, ctx->S_all + n * RR,
+                        pp ? ctx->dS_all + n * RR : nullptr, ctx->ws_gram, 32 * RR, ctx->st));
   }
   if (n == ctx->N - 1) {
-    {
-      PhaseScope ps(ctx, PH_OTHER);
-      CU(cpd::launch_dot(Mown, ctx->A[n], ro * R, ctx->scal + SC_MA, ctx->st));
-    }
     TRY(allreduce_lastmode(ctx, pp));
     PhaseScope ps(ctx, PH_OTHER);
     cpd::g_launches++;
@@ -611,6 +615,10 @@ cpd_status cpd_destroy(cpd_ctx* c) {
   dfree(c, c->dS_all);
   dfree(c, c->Lp);
   dfree(c, c->W);
+  dfree(c, c->ws_gram);
+  dfree(c, c->ws_mttv);
+  dfree(c, c->st_part);
+  if (c->st_counter) cudaFreeAsync(c->st_counter, c->st);
   dfree(c, c->scal);
   dfree(c, c->partial);
   dfree(c, c->gather_tmp);
@@ -732,7 +740,12 @@ cpd_status cp_als_init(cpd_ctx** out, int N, const int64_t* shape, int R, const 
   }
   ITRY(dalloc(ctx, &ctx->S_all, N * RR));
   ITRY(dalloc(ctx, &ctx->dS_all, N * RR));
-  ITRY(dalloc(ctx, &ctx->Lp, RR));
+  ITRY(dalloc(ctx, &ctx->Lp, RR + R));
+  ITRY(dalloc(ctx, &ctx->ws_gram, 32 * RR));
+  ITRY(dalloc(ctx, &ctx->ws_mttv, kMttvWs));
+  ITRY(dalloc(ctx, &ctx->st_part, 3 * 64));
+  ICU(cudaMallocAsync((void**)&ctx->st_counter, sizeof(unsigned int), ctx->st));
+  ICU(cudaMemsetAsync(ctx->st_counter, 0, sizeof(unsigned int), ctx->st));
   ITRY(dalloc(ctx, &ctx->W, RR));
   ITRY(dalloc(ctx, &ctx->scal, SC_COUNT));
   ITRY(dalloc(ctx, &ctx->partial, cpd::kNormBlocks));
@@ -785,7 +798,8 @@ cpd_status cpd_set_factors(cpd_ctx* ctx, const double* const* A_host) {
     if (!A_host[n]) return fail(ctx, CPD_ERR_INVALID_ARG, "null factor");
     const double* src = A_host[n] + (n == ctx->N - 1 ? ctx->lo * R : 0);
     CU(cudaMemcpyAsync(ctx->A[n], src, sizeof(double) * ext(ctx, n) * R, cudaMemcpyHostToDevice, ctx->st));
-    CU(cpd::launch_gram(ctx->A[n], ctx->A[n], ext(ctx, n), R, ctx->S_all + n * RR, ctx->st));
+    CU(cpd::launch_gram(ctx->A[n], ctx->A[n], nullptr, ext(ctx, n), R, ctx->S_all + n * RR, nullptr,
+                        ctx->ws_gram, 32 * RR, ctx->st));
   }
   if (ctx->world > 1) {
     NC(ncclAllReduce(ctx->S_all + (ctx->N - 1) * RR, ctx->S_all + (ctx->N - 1) * RR, RR, ncclDouble,
@@ -1064,7 +1078,10 @@ cpd_status cpd_ttm(const double* T_dev, int64_t pre, int64_t K, int64_t post, co
 cpd_status cpd_mttv(const double* X_dev, int64_t pre, int64_t K, int64_t post, int R, const double* v_dev,
                     double* out_dev, int beta, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  cudaError_t e = cpd::launch_mttv(X_dev, pre, K, post, R, v_dev, out_dev, beta, st);
+  double* ws = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&ws, sizeof(double) * kMttvWs, st);
+  if (e == cudaSuccess) e = cpd::launch_mttv(X_dev, pre, K, post, R, v_dev, out_dev, beta, ws, kMttvWs, st);
+  if (ws) cudaFreeAsync(ws, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) {
     g_init_error = cudaGetErrorString(e);

@@ -19,8 +19,10 @@ cudaError_t launch_ttm(const double* X, int64_t pre, int64_t K, int64_t post, co
 
 // ---- batched TTV (mTTV) stream, P:320-322 ----------------------------------------------
 // out[p, c] = beta*out[p, c] + Σ_y X[(p*K + y)*C + c] * v[y*R + c % R],  C = post*R
+// ws (ws_elems doubles, may be null): K-split partials when the (p, chunk) grid is too small
 cudaError_t launch_mttv(const double* X, int64_t pre, int64_t K, int64_t post, int R,
-                        const double* v, double* out, int beta, cudaStream_t st);
+                        const double* v, double* out, int beta, double* ws, int64_t ws_elems,
+                        cudaStream_t st);
 
 // ---- synthetic tensor (synth/__init__.py recipe) ------------------------------------
 // T[q, z] += std*normal(seed, g) (kind 0) or T = uniform(seed, g) (kind 1) with
@@ -39,11 +41,13 @@ cudaError_t launch_norm2(const double* x, int64_t n, double* partial, double* ds
 cudaError_t launch_dot(const double* x, const double* y, int64_t n, double* dst, cudaStream_t st);
 
 // ---- small dense R x R work (latency-bound) -----------------------------------------------
-// G[a][b] = Σ_i X[i][a] Y[i][b]  (S = A^T A; dS = A^T dA, Eq. 8)
-cudaError_t launch_gram(const double* X, const double* Y, int64_t rows, int R, double* G,
-                        cudaStream_t st);
+// G1[a][b] = Σ_i X[i][a] Y1[i][b] (S = A^T A) and, if Y2, G2 = X^T Y2 (dS = A^T dA,
+// Eq. 8) in the same pass; rows split over up to 16 CTAs (ws: 2*16*R*R doubles),
+// partials summed in a fixed order.
+cudaError_t launch_gram(const double* X, const double* Y1, const double* Y2, int64_t rows, int R,
+                        double* G1, double* G2, double* ws, int64_t ws_elems, cudaStream_t st);
 // Γ^(n) = ∗_{k≠n} S^(k) (Eq. 1) and its Cholesky factor, packed column-major lower, into
-// Lp (R(R+1)/2).  status[0] = 0 ok, 1 not SPD / non-finite.
+// Lp (R(R+1)/2, then the R reciprocal diagonal entries).  status[0] = 0 ok, 1 not SPD.
 cudaError_t launch_gamma_chol(const double* S_all, int N, int n, int R, double* Lp, int* status,
                               cudaStream_t st);
 // X[i,:] = M[i,:] Γ^{-1} via L (forward + backward substitution per row), rows x R.
@@ -54,5 +58,10 @@ cudaError_t launch_pp_w(const double* S_all, const double* dS_all, int N, int n,
                         cudaStream_t st);
 // z = x - y (n elements)
 cudaError_t launch_sub(const double* x, const double* y, double* z, int64_t n, cudaStream_t st);
+// dA = A - base; *o_dA2 = Σ dA^2, *o_A2 = Σ A^2, *o_MA = Σ M A (if M); one launch, last-block
+// fixed-order reduction (part: 3*64 doubles, counter: zero-initialised, self-resetting)
+cudaError_t launch_update_stats(const double* A, const double* base, double* dA, const double* M, int64_t n,
+                                double* part, unsigned int* counter, double* o_dA2, double* o_A2, double* o_MA,
+                                cudaStream_t st);
 
 }  // namespace cpd

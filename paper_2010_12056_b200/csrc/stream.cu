@@ -20,14 +20,23 @@ namespace {
 constexpr int MT_THREADS = 256;
 constexpr int MT_COLS = 64;  // columns per CTA (32 lanes x double2)
 
-template <bool VEC2>
+// One CTA = one work item (p, 64-column chunk, K-split); 8 warps interleave the rows of
+// the split, 4 rows in flight per warp; fixed-order shared-memory reduction.  With
+// ks > 1 the partial sums go to ws[split][p*C + c] and mttv_reduce_kernel adds them in
+// split order (deterministic).
+template <bool VEC2, bool VV>
 __global__ void __launch_bounds__(MT_THREADS)
     mttv_kernel(const double* __restrict__ X, int64_t pre, int64_t K, int64_t C, int R,
-                const double* __restrict__ v, double* __restrict__ out, int beta, int nchunks) {
+                const double* __restrict__ v, double* __restrict__ out, int beta, int nchunks, int ks,
+                int64_t rps, double* __restrict__ ws) {
   __shared__ double red[8][MT_COLS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t p = blockIdx.x / nchunks;
-  const int chunk = blockIdx.x % nchunks;
+  const int split = blockIdx.x % ks;
+  const int64_t rest = blockIdx.x / ks;
+  const int64_t p = rest / nchunks;
+  const int chunk = (int)(rest % nchunks);
+  const int64_t k0 = split * rps;
+  const int64_t k1 = min(K, k0 + rps);
   const int64_t cA = (int64_t)chunk * MT_COLS + (VEC2 ? 2 * lane : lane);
   const int64_t cB = VEC2 ? cA + 1 : cA + 32;
   const bool okA = cA < C, okB = cB < C;
@@ -35,38 +44,44 @@ __global__ void __launch_bounds__(MT_THREADS)
   const double* Xp = X + p * K * C;
   double sA = 0.0, sB = 0.0;
   if (okA) {
-    int64_t y = warp;
-    // 4 independent rows in flight per warp
-    for (; y + 24 < K; y += 32) {
-      double a0, a1, a2, a3, b0, b1, b2, b3;
-      if (VEC2 && okB) {
-        double2 x0 = __ldcs(reinterpret_cast<const double2*>(Xp + (y)*C + cA));
-        double2 x1 = __ldcs(reinterpret_cast<const double2*>(Xp + (y + 8) * C + cA));
-        double2 x2 = __ldcs(reinterpret_cast<const double2*>(Xp + (y + 16) * C + cA));
-        double2 x3 = __ldcs(reinterpret_cast<const double2*>(Xp + (y + 24) * C + cA));
-        a0 = x0.x; b0 = x0.y; a1 = x1.x; b1 = x1.y; a2 = x2.x; b2 = x2.y; a3 = x3.x; b3 = x3.y;
+    int64_t y = k0 + warp;
+    for (; y + 24 < k1; y += 32) {
+      double a[4], b[4], va[4], vb[4];
+      if (VEC2) {
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          double2 x2 = __ldcs(reinterpret_cast<const double2*>(Xp + (y + 8 * u) * C + cA));
+          a[u] = x2.x;
+          b[u] = x2.y;
+        }
       } else {
-        a0 = __ldcs(Xp + (y)*C + cA);
-        a1 = __ldcs(Xp + (y + 8) * C + cA);
-        a2 = __ldcs(Xp + (y + 16) * C + cA);
-        a3 = __ldcs(Xp + (y + 24) * C + cA);
-        b0 = okB ? __ldcs(Xp + (y)*C + cB) : 0.0;
-        b1 = okB ? __ldcs(Xp + (y + 8) * C + cB) : 0.0;
-        b2 = okB ? __ldcs(Xp + (y + 16) * C + cB) : 0.0;
-        b3 = okB ? __ldcs(Xp + (y + 24) * C + cB) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          a[u] = __ldcs(Xp + (y + 8 * u) * C + cA);
+          b[u] = okB ? __ldcs(Xp + (y + 8 * u) * C + cB) : 0.0;
+        }
       }
-      sA = fma(a0, __ldg(v + (y)*R + rA), sA);
-      sA = fma(a1, __ldg(v + (y + 8) * R + rA), sA);
-      sA = fma(a2, __ldg(v + (y + 16) * R + rA), sA);
-      sA = fma(a3, __ldg(v + (y + 24) * R + rA), sA);
-      if (okB) {
-        sB = fma(b0, __ldg(v + (y)*R + rB), sB);
-        sB = fma(b1, __ldg(v + (y + 8) * R + rB), sB);
-        sB = fma(b2, __ldg(v + (y + 16) * R + rB), sB);
-        sB = fma(b3, __ldg(v + (y + 24) * R + rB), sB);
+      if (VV) {
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          double2 v2 = __ldg(reinterpret_cast<const double2*>(v + (y + 8 * u) * R + rA));
+          va[u] = v2.x;
+          vb[u] = v2.y;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          va[u] = __ldg(v + (y + 8 * u) * R + rA);
+          vb[u] = okB ? __ldg(v + (y + 8 * u) * R + rB) : 0.0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        sA = fma(a[u], va[u], sA);
+        sB = fma(b[u], vb[u], sB);
       }
     }
-    for (; y < K; y += 8) {
+    for (; y < k1; y += 8) {
       sA = fma(Xp[y * C + cA], v[y * R + rA], sA);
       if (okB) sB = fma(Xp[y * C + cB], v[y * R + rB], sB);
     }
@@ -85,9 +100,22 @@ __global__ void __launch_bounds__(MT_THREADS)
       double s = red[0][threadIdx.x];
 #pragma unroll
       for (int w = 1; w < 8; w++) s += red[w][threadIdx.x];
-      double* o = out + p * C + c;
-      *o = beta ? *o + s : s;
+      if (ks == 1) {
+        double* o = out + p * C + c;
+        *o = beta ? *o + s : s;
+      } else {
+        ws[split * pre * C + p * C + c] = s;
+      }
     }
+  }
+}
+
+__global__ void mttv_reduce_kernel(const double* __restrict__ ws, int ks, int64_t n, double* __restrict__ out,
+                                   int beta) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    double s = ws[e];
+    for (int k = 1; k < ks; k++) s += ws[k * n + e];
+    out[e] = beta ? out[e] + s : s;
   }
 }
 
@@ -192,19 +220,42 @@ __global__ void sub_kernel(const double* __restrict__ x, const double* __restric
 }  // namespace
 
 cudaError_t launch_mttv(const double* X, int64_t pre, int64_t K, int64_t post, int R,
-                        const double* v, double* out, int beta, cudaStream_t st) {
+                        const double* v, double* out, int beta, double* ws, int64_t ws_elems, cudaStream_t st) {
   const int64_t C = post * R;
   if (pre <= 0 || C <= 0) return cudaSuccess;
   if (K <= 0) return cudaErrorInvalidValue;
   const bool vec2 = (C % 2) == 0 && ((uintptr_t)X % 16) == 0;
+  const bool vv = vec2 && (R % 2) == 0 && ((uintptr_t)v % 16) == 0;
   const int nchunks = (int)((C + MT_COLS - 1) / MT_COLS);
-  int64_t grid = pre * nchunks;
+  const int64_t items0 = pre * nchunks;
+  // split K so that the grid is >= ~8 waves of 4 resident CTAs per SM (tail <= 1/8 wave)
+  int64_t ks = (148 * 4 * 8 + items0 - 1) / items0;
+  int64_t max_by_rows = K / 64;
+  if (ks > max_by_rows) ks = max_by_rows;
+  if (ks > 16) ks = 16;
+  if (ws == nullptr || ks * pre * C > ws_elems) ks = 1;
+  if (ks < 1) ks = 1;
+  const int64_t rps = (K + ks - 1) / ks;
+  int64_t grid = items0 * ks;
   if (grid > 0x7fffffff) return cudaErrorInvalidConfiguration;
   g_launches++;
-  if (vec2)
-    mttv_kernel<true><<<(unsigned)grid, MT_THREADS, 0, st>>>(X, pre, K, C, R, v, out, beta, nchunks);
+#define CPD_MTTV(V2, VV_)                                                                              \
+  mttv_kernel<V2, VV_><<<(unsigned)grid, MT_THREADS, 0, st>>>(X, pre, K, C, R, v, out, beta, nchunks, (int)ks, \
+                                                              rps, ws)
+  if (vec2 && vv)
+    CPD_MTTV(true, true);
+  else if (vec2)
+    CPD_MTTV(true, false);
   else
-    mttv_kernel<false><<<(unsigned)grid, MT_THREADS, 0, st>>>(X, pre, K, C, R, v, out, beta, nchunks);
+    CPD_MTTV(false, false);
+#undef CPD_MTTV
+  if (ks > 1) {
+    g_launches++;
+    int64_t n = pre * C;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    mttv_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(ws, (int)ks, n, out, beta);
+  }
   return cudaGetLastError();
 }
 

@@ -22,7 +22,6 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 16;
-constexpr int STAGES = 4;
 constexpr int THREADS = 256;
 constexpr int LDA_KC = BK + 4;   // [BM][BK+4]  : (g*20 + t) mod 16 distinct for g,t < 4
 constexpr int LDA_MC = BM + 4;   // [BK][BM+4]  : (t*132 + g) mod 16 distinct
@@ -51,6 +50,10 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 
 template <int NF>
 struct Smem {
+  // NF <= 8 (R <= 64 per tile, <= 128 registers): 3 stages so two CTAs (16 warps) fit
+  // per SM; wider tiles keep 4 stages at one CTA per SM.
+  static constexpr int STAGES = NF <= 8 ? 3 : 4;
+  static constexpr int MIN_BLOCKS = NF <= 8 ? 2 : 1;
   static constexpr int BN = 8 * NF;
   static constexpr int LDB = ((BN + 15) / 16) * 16 + 4;
   static constexpr int A_ELEMS = (BM * LDA_KC > BK * LDA_MC) ? BM * LDA_KC : BK * LDA_MC;
@@ -62,12 +65,13 @@ struct Smem {
 // MC: post > 1 (M-contiguous rows); VEC2: 16-byte chunks (requires post even for MC,
 // K even for KC, ncols even for B).
 template <int NF, bool MC, bool VEC2, bool BVEC2>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(THREADS, Smem<NF>::MIN_BLOCKS)
     ttm_dmma_kernel(const double* __restrict__ X, int64_t pre, int64_t K, int64_t post,
                     const double* __restrict__ B, int ncols, int ntiles_n,
                     double* __restrict__ out, int beta) {
   using S = Smem<NF>;
   constexpr int BN = S::BN;
+  constexpr int STAGES = S::STAGES;
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
