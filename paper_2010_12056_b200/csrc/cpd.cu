@@ -77,8 +77,13 @@ struct cpd_ctx {
   std::vector<double*> A, Aold, dA, Mlast, Ap, Mp;
   double* S_all = nullptr;   // N x R x R
   double* dS_all = nullptr;  // N x R x R
-  double* Lp = nullptr;      // packed Cholesky factor
-  double* W = nullptr;       // R x R
+  double* Lp[2] = {nullptr, nullptr};  // packed Cholesky factors (double-buffered)
+  double* Wb[2] = {nullptr, nullptr};  // PP second-order W (double-buffered)
+  int* pf_status = nullptr;            // Cholesky status per buffer
+  cudaStream_t st2 = nullptr;          // side stream: Γ factorisation / W ahead of their mode
+  cudaEvent_t ev_s = nullptr, ev_pf = nullptr;
+  int pf_mode = -1, pf_buf = 0;        // mode whose Γ factor (and W if pf_pp) is being prepared
+  bool pf_pp = false;
   double* ws_gram = nullptr; // 2 x 16 x R x R Gram partials
   double* ws_mttv = nullptr; // mTTV K-split partials
   double* st_part = nullptr; // update-stats block partials
@@ -375,6 +380,36 @@ __global__ void gamma_dot_kernel(const double* __restrict__ S_all, int N, int R,
   }
 }
 
+// Γ^(m) = ∗_{k≠m} S^(k) depends only on the Grams, so its Cholesky factorisation (and the
+// PP Hadamard sum W^(m) of Eq. 7) can run on a side stream as soon as the previous update
+// has produced its S, overlapping the latency-bound single-CTA factorisation with the
+// HBM-bound MTTKRP stream of mode m.  Buffers alternate so the side stream never
+// overwrites a factor the main stream still reads.
+cpd_status prefetch_solve(cpd_ctx* ctx, int m, bool pp) {
+  const int b = ctx->pf_buf ^ 1;
+  CU(cudaEventRecord(ctx->ev_s, ctx->st));
+  CU(cudaStreamWaitEvent(ctx->st2, ctx->ev_s, 0));
+  CU(cpd::launch_gamma_chol(ctx->S_all, ctx->N, m, ctx->R, ctx->Lp[b], ctx->pf_status + b, ctx->st2));
+  if (pp) CU(cpd::launch_pp_w(ctx->S_all, ctx->dS_all, ctx->N, m, ctx->R, ctx->Wb[b], ctx->st2));
+  CU(cudaEventRecord(ctx->ev_pf, ctx->st2));
+  ctx->pf_buf = b;
+  ctx->pf_mode = m;
+  ctx->pf_pp = pp;
+  return CPD_OK;
+}
+
+void invalidate_prefetch(cpd_ctx* ctx) { ctx->pf_mode = -1; }
+
+cpd_status acquire_solve(cpd_ctx* ctx, int n, bool pp, int* buf) {
+  if (!(ctx->pf_mode == n && (ctx->pf_pp || !pp))) TRY(prefetch_solve(ctx, n, pp));
+  CU(cudaStreamWaitEvent(ctx->st, ctx->ev_pf, 0));
+  *buf = ctx->pf_buf;
+  ctx->pf_mode = -1;
+  CU(cudaMemcpyAsync(ctx->status + n, ctx->pf_status + ctx->pf_buf, sizeof(int), cudaMemcpyDeviceToDevice,
+                     ctx->st));
+  return CPD_OK;
+}
+
 // Solve-and-update for mode n given the local (partial for n<N-1) MTTKRP Mloc
 // (ext(n) x R, may be overwritten).  pp: dA = A - A_p and dS maintained; Vterm: add
 // V = A^(n) W before the solve (Eq. 7).
@@ -388,14 +423,14 @@ cpd_status update_mode(cpd_ctx* ctx, int n, double* Mloc, bool pp) {
     PhaseScope ps(ctx, PH_OTHER);
     NC(ncclReduceScatter(Mloc, Mown, ro * R, ncclDouble, ncclSum, ctx->comm, ctx->st));
   }
+  // Γ^(n) factor (and W^(n) for PP): prepared on the side stream while the MTTKRP of
+  // mode n streamed, or computed here if no matching prefetch is pending
+  int b;
+  TRY(acquire_solve(ctx, n, pp, &b));
   if (pp) {
     // V^(n) = A^(n) W^(n) with the current (pre-update) A^(n): Eq. 7; M~ += V (Eq. 5)
-    {
-      PhaseScope ps(ctx, PH_HAD);
-      CU(cpd::launch_pp_w(ctx->S_all, ctx->dS_all, ctx->N, n, R, ctx->W, ctx->st));
-    }
-    PhaseScope ps(ctx, PH_SOLVE);
-    CU(cpd::launch_ttm(ctx->A[n] + off * R, ro, R, 1, ctx->W, R, Mown, 1, ctx->st));
+    PhaseScope ps(ctx, PH_HAD);
+    CU(cpd::launch_ttm(ctx->A[n] + off * R, ro, R, 1, ctx->Wb[b], R, Mown, 1, ctx->st));
   }
   {
     PhaseScope ps(ctx, PH_OTHER);
@@ -407,8 +442,7 @@ cpd_status update_mode(cpd_ctx* ctx, int n, double* Mloc, bool pp) {
   }
   {
     PhaseScope ps(ctx, PH_SOLVE);
-    CU(cpd::launch_gamma_chol(ctx->S_all, ctx->N, n, R, ctx->Lp, ctx->status + n, ctx->st));
-    CU(cpd::launch_trisolve(ctx->Lp, Mown, ro, R, ctx->A[n] + off * R, ctx->st));
+    CU(cpd::launch_trisolve(ctx->Lp[b], Mown, ro, R, ctx->A[n] + off * R, ctx->st));
   }
   if (n < ctx->N - 1 && ctx->world > 1) {
     PhaseScope ps(ctx, PH_OTHER);
@@ -432,6 +466,8 @@ cpd_status update_mode(cpd_ctx* ctx, int n, double* Mloc, bool pp) {
     gamma_dot_kernel<<<1, 1024, 0, ctx->st>>>(ctx->S_all, ctx->N, R, ctx->scal + SC_GS);
     CU(cudaGetLastError());
   }
+  // S^(n) is final: start Γ^(n+1) (the next update in every schedule) on the side stream
+  TRY(prefetch_solve(ctx, (n + 1) % ctx->N, pp));
   return CPD_OK;
 }
 
@@ -613,8 +649,12 @@ cpd_status cpd_destroy(cpd_ctx* c) {
     for (auto& p : *v) dfree(c, p);
   dfree(c, c->S_all);
   dfree(c, c->dS_all);
-  dfree(c, c->Lp);
-  dfree(c, c->W);
+  if (c->st2) cudaStreamSynchronize(c->st2);
+  for (int b = 0; b < 2; b++) {
+    dfree(c, c->Lp[b]);
+    dfree(c, c->Wb[b]);
+  }
+  if (c->pf_status) cudaFreeAsync(c->pf_status, c->st);
   dfree(c, c->ws_gram);
   dfree(c, c->ws_mttv);
   dfree(c, c->st_part);
@@ -632,6 +672,9 @@ cpd_status cpd_destroy(cpd_ctx* c) {
   if (c->hscal) cudaFreeHost(c->hscal);
   if (c->hstatus) cudaFreeHost(c->hstatus);
   if (c->comm) ncclCommDestroy(c->comm);
+  if (c->ev_s) cudaEventDestroy(c->ev_s);
+  if (c->ev_pf) cudaEventDestroy(c->ev_pf);
+  if (c->st2) cudaStreamDestroy(c->st2);
   if (c->own_stream && c->st) cudaStreamDestroy(c->st);
   delete c;
   return CPD_OK;
@@ -740,13 +783,20 @@ cpd_status cp_als_init(cpd_ctx** out, int N, const int64_t* shape, int R, const 
   }
   ITRY(dalloc(ctx, &ctx->S_all, N * RR));
   ITRY(dalloc(ctx, &ctx->dS_all, N * RR));
-  ITRY(dalloc(ctx, &ctx->Lp, RR + R));
+  for (int b2 = 0; b2 < 2; b2++) {
+    ITRY(dalloc(ctx, &ctx->Lp[b2], RR + R));
+    ITRY(dalloc(ctx, &ctx->Wb[b2], RR));
+  }
+  ICU(cudaMallocAsync((void**)&ctx->pf_status, sizeof(int) * 2, ctx->st));
+  ICU(cudaMemsetAsync(ctx->pf_status, 0, sizeof(int) * 2, ctx->st));
+  ICU(cudaStreamCreateWithFlags(&ctx->st2, cudaStreamNonBlocking));
+  ICU(cudaEventCreateWithFlags(&ctx->ev_s, cudaEventDisableTiming));
+  ICU(cudaEventCreateWithFlags(&ctx->ev_pf, cudaEventDisableTiming));
   ITRY(dalloc(ctx, &ctx->ws_gram, 32 * RR));
   ITRY(dalloc(ctx, &ctx->ws_mttv, kMttvWs));
   ITRY(dalloc(ctx, &ctx->st_part, 3 * 64));
   ICU(cudaMallocAsync((void**)&ctx->st_counter, sizeof(unsigned int), ctx->st));
   ICU(cudaMemsetAsync(ctx->st_counter, 0, sizeof(unsigned int), ctx->st));
-  ITRY(dalloc(ctx, &ctx->W, RR));
   ITRY(dalloc(ctx, &ctx->scal, SC_COUNT));
   ITRY(dalloc(ctx, &ctx->partial, cpd::kNormBlocks));
   ICU(cudaMallocAsync((void**)&ctx->status, sizeof(int) * CPD_MAX_ORDER, ctx->st));
@@ -811,6 +861,7 @@ cpd_status cpd_set_factors(cpd_ctx* ctx, const double* const* A_host) {
   free_pp(ctx);
   ctx->pp_regime = false;
   ctx->have_dA = false;
+  invalidate_prefetch(ctx);
   CU(cudaStreamSynchronize(ctx->st));
   return CPD_OK;
 }
@@ -836,6 +887,7 @@ cpd_status pp_init(cpd_ctx* ctx) {
     CU(cudaMemsetAsync(ctx->dA[n], 0, sizeof(double) * ext(ctx, n) * ctx->R, ctx->st));
   }
   CU(cudaMemsetAsync(ctx->dS_all, 0, sizeof(double) * N * ctx->R * ctx->R, ctx->st));
+  invalidate_prefetch(ctx);  // W depends on dS
   // three first-level roots; reuse the live MSDT root when valid (P:384 footnote)
   std::vector<int> js;
   int live = (ctx->opts.reuse_root_in_pp_init && ctx->sub_is_msdt && ctx->sub.active && !ctx->pp_regime)

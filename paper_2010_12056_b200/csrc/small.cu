@@ -7,6 +7,8 @@
 // All reductions run in a fixed order (deterministic; no floating-point atomics).
 #include "kernels.h"
 
+#define CPD_MAXR 232
+
 namespace cpd {
 namespace {
 
@@ -68,124 +70,223 @@ __global__ void gram_reduce_kernel(const double* __restrict__ P1, const double* 
 // the R reciprocals of the diagonal follow the packed factor.
 __device__ __forceinline__ int pk(int i, int j, int R) { return j * R - (j * (j - 1)) / 2 + (i - j); }
 
-__global__ void __launch_bounds__(1024)
+// Blocked (NB = 32) right-to-left panel Cholesky, one CTA.  Per panel [c0, c0+nb):
+//  (1) panel update  A(i,j) -= Σ_{m<c0} L(i,m) L(j,m)   (all threads, 4x2 register tiles)
+//  (2) diagonal block factorised by warp 0 in registers (lane r holds row r; column k is
+//      broadcast with shuffles whose source lane / register are compile-time constants)
+//  (3) rows below: L(i,c0+j) solved against the diagonal block (thread per row, registers)
+// Only step (2) is sequential, so a panel costs ~3 barriers instead of 32.
+constexpr int NB = 16;  // panel width: keeps the unrolled register code small (i-cache)
+constexpr int CH_THREADS = 256;
+__global__ void __launch_bounds__(CH_THREADS)
     gamma_chol_kernel(const double* __restrict__ S_all, int N, int n, int R, double* __restrict__ Lp,
                       int* status) {
   extern __shared__ double L[];
+  const int total = R * (R + 1) / 2;
+  double* iv = L + total;  // reciprocals of the diagonal
   __shared__ int bad;
   const int tid = threadIdx.x;
-  if (tid == 0) bad = 0;
-  const int total = R * (R + 1) / 2;
+  const int lane = tid & 31, warp = tid >> 5, nw = CH_THREADS / 32;
   const int64_t RR = (int64_t)R * R;
-  // Γ (lower part), Hadamard product in ascending k (Eq. 1); coalesced over j
-  for (int idx = tid; idx < R * R; idx += blockDim.x) {
-    int i = idx / R, j = idx - i * R;
-    if (j > i) continue;
-    double gv = 1.0;
-    bool first = true;
-    for (int k = 0; k < N; k++) {
-      if (k == n) continue;
-      double sv = S_all[k * RR + idx];
-      gv = first ? sv : gv * sv;
-      first = false;
+  if (tid == 0) bad = 0;
+  // Γ = ∗_{k≠n} S_k in ascending k (Eq. 1), lower part
+  for (int j = warp; j < R; j += nw) {
+    const int cs = pk(j, j, R);
+    for (int i = j + lane; i < R; i += 32) {
+      double gv = 1.0;
+      bool first = true;
+      for (int k = 0; k < N; k++) {
+        if (k == n) continue;
+        double sv = S_all[k * RR + (int64_t)i * R + j];
+        gv = first ? sv : gv * sv;
+        first = false;
+      }
+      L[cs + (i - j)] = gv;
     }
-    L[pk(i, j, R)] = gv;
   }
   __syncthreads();
-  const int tx = tid % 32, ty = tid / 32, nty = blockDim.x / 32;
-  for (int k = 0; k < R; k++) {
-    double d = L[pk(k, k, R)];
-    if (!(d > 0.0) || !isfinite(d)) {
-      if (tid == 0) bad = 1;
-      break;  // uniform: every thread read the same d
-    }
-    d = sqrt(d);
-    const double inv = 1.0 / d;
-    // column k below the diagonal: L(i,k) = A(i,k) * (1/L(k,k)) (LAPACK dpotf2 scales by
-    // the reciprocal); the trailing update recomputes the scaled L(i,k), L(j,k) it needs so
-    // the column can be scaled after the same barrier
-    for (int j = k + 1 + ty; j < R; j += nty) {
-      double ljk = L[pk(j, k, R)] * inv;
-      for (int i = j + tx; i < R; i += 32) {
-        double lik = L[pk(i, k, R)] * inv;
-        L[pk(i, j, R)] -= lik * ljk;
+  for (int c0 = 0; c0 < R; c0 += NB) {
+    const int nb = min(NB, R - c0);
+    // (1) panel update from the finished columns m < c0
+    if (c0 > 0) {
+      const int nti = (R - c0 + 3) / 4, ntj = (nb + 1) / 2;
+      for (int t = tid; t < nti * ntj; t += CH_THREADS) {
+        const int ti = t / ntj, tj = t - ti * ntj;
+        const int i0 = c0 + 4 * ti, j0 = c0 + 2 * tj;
+        if (i0 + 3 < j0) continue;
+        double acc[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+        int cs = -0;  // cs(m) = pk(m,m) - m: L(i,m) = L[cs + i]
+        for (int m = 0; m < c0; m++) {
+          const double lj0 = L[cs + j0];
+          const double lj1 = (j0 + 1 < c0 + nb) ? L[cs + j0 + 1] : 0.0;
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            const double li = (i0 + q < R) ? L[cs + i0 + q] : 0.0;
+            acc[q][0] = fma(li, lj0, acc[q][0]);
+            acc[q][1] = fma(li, lj1, acc[q][1]);
+          }
+          cs += R - m - 1;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+#pragma unroll
+          for (int c = 0; c < 2; c++) {
+            const int i = i0 + q, j = j0 + c;
+            if (i < R && j < c0 + nb && i >= j) L[pk(i, j, R)] -= acc[q][c];
+          }
       }
+      __syncthreads();
+    }
+    // (2) diagonal block: lane r holds row r (columns 0..r) of the block
+    if (warp == 0) {
+      double row[NB];
+      const int r = lane;
+#pragma unroll
+      for (int j = 0; j < NB; j++) row[j] = (j <= r && r < nb) ? L[pk(c0 + r, c0 + j, R)] : 0.0;
+      int badl = 0;
+#pragma unroll
+      for (int k = 0; k < NB; k++) {
+        if (k < nb) {
+          const double akk = __shfl_sync(0xffffffffu, row[k], k);
+          if (!(akk > 0.0) || !isfinite(akk)) badl = 1;
+          // one long-latency op per pivot on the sequential path: 1/sqrt, then sqrt = a * (1/sqrt a)
+          const double inv = rsqrt(akk), d = akk * inv;
+          const double lrk = (r > k) ? row[k] * inv : (r == k ? d : row[k]);
+          row[k] = lrk;
+#pragma unroll
+          for (int j = k + 1; j < NB; j++) {
+            const double ljk = __shfl_sync(0xffffffffu, row[k], j);  // L(j,k), on lane j
+            if (j <= r && j < nb) row[j] = fma(-lrk, ljk, row[j]);
+          }
+        }
+      }
+      if (r < nb) {
+#pragma unroll
+        for (int j = 0; j < NB; j++)
+          if (j <= r) L[pk(c0 + r, c0 + j, R)] = row[j];
+        iv[c0 + r] = 1.0 / row[r];  // off the sequential path
+      }
+      if (badl && lane == 0) bad = 1;
     }
     __syncthreads();
-    for (int i = k + 1 + tid; i < R; i += blockDim.x) L[pk(i, k, R)] *= inv;
-    if (tid == 0) {
-      L[pk(k, k, R)] = d;
-      Lp[total + k] = inv;
+    // (3) rows below the block: x L_blk^T = a  (thread per row, column-oriented)
+    for (int i = c0 + nb + tid; i < R; i += CH_THREADS) {
+      double x[NB];
+#pragma unroll
+      for (int j = 0; j < NB; j++) x[j] = j < nb ? L[pk(i, c0 + j, R)] : 0.0;
+#pragma unroll
+      for (int j = 0; j < NB; j++) {
+        if (j < nb) {
+          x[j] *= iv[c0 + j];
+          const int cj = pk(c0 + j, c0 + j, R);
+#pragma unroll
+          for (int m = j + 1; m < NB; m++)
+            if (m < nb) x[m] = fma(-L[cj + (m - j)], x[j], x[m]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < NB; j++)
+        if (j < nb) L[pk(i, c0 + j, R)] = x[j];
     }
     __syncthreads();
+    if (bad) break;
   }
-  for (int e = tid; e < total; e += blockDim.x) Lp[e] = L[e];
+  for (int e = tid; e < total + R; e += CH_THREADS) Lp[e] = L[e];
   if (tid == 0) status[0] = bad;
 }
 
-// --------- X[i,:] = M[i,:] Γ^{-1}: L y = m (column sweep), L^T x = y (dot sweep) ---------
-// One warp per row; lane holds entries j = lane + 32q.
-template <int RQ>
-__global__ void __launch_bounds__(1024)
-    trisolve_kernel(const double* __restrict__ Lp, const double* __restrict__ M, int64_t rows, int R,
-                    double* __restrict__ X) {
-  extern __shared__ double L[];
-  const int total = R * (R + 1) / 2 + R;
-  for (int e = threadIdx.x; e < total; e += blockDim.x) L[e] = Lp[e];
+// --------- X = M Γ^{-1} with Γ = L L^T, TR rows per CTA, blocked by 32 columns -------------
+// forward  Y L^T = M : Y(:,j) = (M(:,j) - Σ_{m<j} Y(:,m) L(j,m)) / L(j,j)
+// backward X L   = Y : X(:,j) = (Y(:,j) - Σ_{m>j} X(:,m) L(m,j)) / L(j,j)
+// Per panel: (a) the off-panel sums for every (row, column) pair in parallel, (b) the 32x32
+// diagonal block solved per row in registers (thread per row).
+__global__ void __launch_bounds__(256)
+    trisolve_tile_kernel(const double* __restrict__ Lp, const double* __restrict__ M, int64_t rows, int R,
+                         int TR, double* __restrict__ X) {
+  extern __shared__ double sm[];
+  const int total = R * (R + 1) / 2;
+  double* L = sm;
+  const double* iv = sm + total;
+  double* Ys = sm + total + R;  // TR x R, row-major: M, then Y, then X in place
+  const int tid = threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.x * TR;
+  const int tr = (int)min((int64_t)TR, rows - r0);
+  for (int e = tid; e < total + R; e += blockDim.x) sm[e] = Lp[e];
+  for (int e = tid; e < tr * R; e += blockDim.x) Ys[e] = M[r0 * R + e];
   __syncthreads();
-  const double* invd = L + (total - R);
-  const int lane = threadIdx.x & 31;
-  const int64_t wglob = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
-  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x / 32);
-  for (int64_t row = wglob; row < rows; row += wstride) {
-    double m[RQ];
-#pragma unroll
-    for (int q = 0; q < RQ; q++) {
-      int j = lane + 32 * q;
-      m[q] = j < R ? M[row * R + j] : 0.0;
+  // forward
+  for (int c0 = 0; c0 < R; c0 += NB) {
+    const int nb = min(NB, R - c0);
+    if (c0 > 0) {
+      for (int t = tid; t < tr * nb; t += blockDim.x) {
+        const int r = t / nb, j = c0 + (t - r * nb);
+        const double* yr = Ys + r * R;
+        double s = 0.0;
+        int cs = 0;  // L(j,m) = L[cs(m) + j]
+        for (int m = 0; m < c0; m++) {
+          s = fma(yr[m], L[cs + j], s);
+          cs += R - m - 1;
+        }
+        Ys[r * R + j] -= s;
+      }
+      __syncthreads();
     }
-    // forward: y_k = m_k / L_kk ; m_j -= L_jk y_k (j > k)
+    if (tid < tr) {
+      double* yr = Ys + tid * R;
+      double x[NB];
 #pragma unroll
-    for (int q = 0; q < RQ; q++) {
-      for (int kk = 0; kk < 32; kk++) {
-        int k = 32 * q + kk;
-        if (k >= R) break;
-        double yk = __shfl_sync(0xffffffffu, m[q], kk) * invd[k];
-        if (lane == kk) m[q] = yk;
-        const int cs = pk(k, k, R);
+      for (int j = 0; j < NB; j++) x[j] = j < nb ? yr[c0 + j] : 0.0;
 #pragma unroll
-        for (int q2 = q; q2 < RQ; q2++) {
-          int j = lane + 32 * q2;
-          if (j > k && j < R) m[q2] = fma(-L[cs + (j - k)], yk, m[q2]);
+      for (int j = 0; j < NB; j++) {
+        if (j < nb) {
+          x[j] *= iv[c0 + j];
+          const int cj = pk(c0 + j, c0 + j, R);
+#pragma unroll
+          for (int m = j + 1; m < NB; m++)
+            if (m < nb) x[m] = fma(-L[cj + (m - j)], x[j], x[m]);
         }
       }
+#pragma unroll
+      for (int j = 0; j < NB; j++)
+        if (j < nb) yr[c0 + j] = x[j];
     }
-    // backward: x_k = (y_k - Σ_{j>k} L_jk x_j) / L_kk
-#pragma unroll
-    for (int q = RQ - 1; q >= 0; q--) {
-      for (int kk = 31; kk >= 0; kk--) {
-        int k = 32 * q + kk;
-        if (k >= R) continue;
-        const int cs = pk(k, k, R);
-        double part = 0.0;
-#pragma unroll
-        for (int q2 = q; q2 < RQ; q2++) {
-          int j = lane + 32 * q2;
-          if (j > k && j < R) part = fma(L[cs + (j - k)], m[q2], part);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-        double yk = __shfl_sync(0xffffffffu, m[q], kk);
-        double xk = (yk - part) * invd[k];
-        if (lane == kk) m[q] = xk;
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < RQ; q++) {
-      int j = lane + 32 * q;
-      if (j < R) X[row * R + j] = m[q];
-    }
+    __syncthreads();
   }
+  // backward (panels in descending order)
+  const int npan = (R + NB - 1) / NB;
+  for (int p = npan - 1; p >= 0; p--) {
+    const int c0 = p * NB, nb = min(NB, R - c0), c1 = c0 + nb;
+    if (c1 < R) {
+      for (int t = tid; t < tr * nb; t += blockDim.x) {
+        const int r = t / nb, j = c0 + (t - r * nb);
+        const double* xr = Ys + r * R;
+        const int cj = pk(j, j, R) - j;  // L(m,j) = L[cj + m]
+        double s = 0.0;
+        for (int m = c1; m < R; m++) s = fma(xr[m], L[cj + m], s);
+        Ys[r * R + j] -= s;
+      }
+      __syncthreads();
+    }
+    if (tid < tr) {
+      double* xr = Ys + tid * R;
+      double x[NB];
+#pragma unroll
+      for (int j = 0; j < NB; j++) x[j] = j < nb ? xr[c0 + j] : 0.0;
+#pragma unroll
+      for (int j = NB - 1; j >= 0; j--) {
+        if (j < nb) {
+          x[j] *= iv[c0 + j];
+#pragma unroll
+          for (int m = 0; m < j; m++) x[m] = fma(-L[pk(c0 + j, c0 + m, R)], x[j], x[m]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < NB; j++)
+        if (j < nb) xr[c0 + j] = x[j];
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < tr * R; e += blockDim.x) X[r0 * R + e] = Ys[e];
 }
 
 // --------- W = Σ_{i<j; i,j≠n} dS_i ∗ dS_j ∗ ∗_{k∉{i,j,n}} S_k ---------------------------
@@ -260,6 +361,19 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// opt a kernel in to the largest dynamic shared memory the device allows
+template <typename K>
+cudaError_t opt_in_smem(K kern) {
+  int dev = 0, optin = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa;
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, kern);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+  return e;
+}
+
 }  // namespace
 
 cudaError_t launch_gram(const double* X, const double* Y1, const double* Y2, int64_t rows, int R,
@@ -291,47 +405,39 @@ cudaError_t launch_gram(const double* X, const double* Y1, const double* Y2, int
 
 cudaError_t launch_gamma_chol(const double* S_all, int N, int n, int R, double* Lp, int* status,
                               cudaStream_t st) {
-  size_t smem = sizeof(double) * (size_t)R * (R + 1) / 2;
-  cudaError_t e = cudaFuncSetAttribute(gamma_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
-  if (e != cudaSuccess) return e;
-  g_launches++;
-  gamma_chol_kernel<<<1, 1024, smem, st>>>(S_all, N, n, R, Lp, status);
-  return cudaGetLastError();
-}
-
-template <int RQ>
-static cudaError_t trisolve_rq(const double* Lp, const double* M, int64_t rows, int R, double* X,
-                               cudaStream_t st) {
   size_t smem = sizeof(double) * ((size_t)R * (R + 1) / 2 + R);
-  auto kern = trisolve_kernel<RQ>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  // spread rows over all SMs: warps per block chosen so that ~148 blocks cover the rows
-  int64_t wpb = (rows + 147) / 148;
-  if (wpb < 1) wpb = 1;
-  if (wpb > 32) wpb = 32;
-  int64_t blocks = (rows + wpb - 1) / wpb;
-  if (blocks > 148) blocks = 148;
+  static bool attr = false;  // one process per GPU: set the opt-in once
+  if (!attr) {
+    cudaError_t e = opt_in_smem(gamma_chol_kernel);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
   g_launches++;
-  kern<<<(unsigned)blocks, (unsigned)(32 * wpb), smem, st>>>(Lp, M, rows, R, X);
+  gamma_chol_kernel<<<1, CH_THREADS, smem, st>>>(S_all, N, n, R, Lp, status);
   return cudaGetLastError();
 }
 
 cudaError_t launch_trisolve(const double* Lp, const double* M, int64_t rows, int R, double* X,
                             cudaStream_t st) {
   if (rows <= 0) return cudaSuccess;
-  switch ((R + 31) / 32) {
-    case 1: return trisolve_rq<1>(Lp, M, rows, R, X, st);
-    case 2: return trisolve_rq<2>(Lp, M, rows, R, X, st);
-    case 3: return trisolve_rq<3>(Lp, M, rows, R, X, st);
-    case 4: return trisolve_rq<4>(Lp, M, rows, R, X, st);
-    case 5: return trisolve_rq<5>(Lp, M, rows, R, X, st);
-    case 6: return trisolve_rq<6>(Lp, M, rows, R, X, st);
-    case 7: return trisolve_rq<7>(Lp, M, rows, R, X, st);
-    case 8: return trisolve_rq<8>(Lp, M, rows, R, X, st);
+  const size_t lbytes = sizeof(double) * ((size_t)R * (R + 1) / 2 + R);
+  // rows per CTA: spread over the SMs, bounded by shared memory (227 KB)
+  int64_t tr = (rows + 147) / 148;
+  int64_t tr_max = ((int64_t)227 * 1024 - (int64_t)lbytes) / (8 * (int64_t)R);
+  if (tr > tr_max) tr = tr_max;
+  if (tr > 64) tr = 64;
+  if (tr < 1) tr = 1;
+  size_t smem = lbytes + sizeof(double) * tr * R;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = opt_in_smem(trisolve_tile_kernel);
+    if (e != cudaSuccess) return e;
+    attr = true;
   }
-  return cudaErrorInvalidValue;
+  int64_t blocks = (rows + tr - 1) / tr;
+  g_launches++;
+  trisolve_tile_kernel<<<(unsigned)blocks, 256, smem, st>>>(Lp, M, rows, R, (int)tr, X);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_pp_w(const double* S_all, const double* dS_all, int N, int n, int R, double* W,
