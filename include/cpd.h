@@ -67,7 +67,17 @@ typedef struct {
   double pp_eps;              /* ε in (0,1) for still_valid / cpd_pp_condition (Alg. 2 line 5) */
   int reuse_root_in_pp_init;  /* P:384 footnote: reuse a still-valid MSDT root in pp_init (default 1) */
   int profile_phases;         /* 1: CUDA-event timers per phase (TTM, mTTV, solve, hadamard, other) */
+  void* local_group;          /* NULL: NCCL (one process per GPU).  Else a cpd_local_group of `world`
+                                 ranks in ONE process on ONE device, each rank's calls made from its own
+                                 host thread (verification of the 1-D partition on a single GPU) */
 } cpd_opts;
+
+typedef struct cpd_local_group cpd_local_group;
+/* In-process group for `world` (1..8) ranks sharing one device (see cpd_opts.local_group):
+ * collectives become fixed-order device sums over the ranks' buffers.  Destroy after every
+ * ctx that uses it. */
+cpd_status cpd_local_group_create(int world, cpd_local_group** out);
+cpd_status cpd_local_group_destroy(cpd_local_group* g);
 
 /* Fill *o with defaults: device 0, rank 0, world 1, no NCCL id, library stream,
  * pp_eps 0.1, reuse_root_in_pp_init 1, profile_phases 0. */

@@ -20,7 +20,7 @@ EXPORTED_SYMBOLS = [
     "pp_approx_sweep", "fitness", "cpd_pp_condition", "cpd_get_factor", "cpd_get_last_mttkrp",
     "cpd_set_factors", "cpd_get_phase_ms", "cpd_get_counters", "cpd_reset_counters",
     "cpd_debug_get_pp_operator", "cpd_last_error", "cpd_destroy", "cpd_gen_tensor", "cpd_ttm",
-    "cpd_mttv",
+    "cpd_mttv", "cpd_local_group_create", "cpd_local_group_destroy",
 ]
 
 
@@ -33,7 +33,7 @@ class CPDError(RuntimeError):
 class cpd_opts(C.Structure):
     _fields_ = [("struct_size", C.c_uint32), ("device", C.c_int), ("rank", C.c_int), ("world", C.c_int),
                 ("nccl_unique_id", C.c_void_p), ("stream", C.c_void_p), ("pp_eps", C.c_double),
-                ("reuse_root_in_pp_init", C.c_int), ("profile_phases", C.c_int)]
+                ("reuse_root_in_pp_init", C.c_int), ("profile_phases", C.c_int), ("local_group", C.c_void_p)]
 
 
 _lib = None
@@ -73,6 +73,8 @@ def load_library():
                                      C.POINTER(_D), C.c_int, C.c_double, C.c_uint64, _P]),
         "cpd_ttm": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, _P, C.c_int, _P, _P]),
         "cpd_mttv": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, C.c_int, _P, _P, C.c_int, _P]),
+        "cpd_local_group_create": (C.c_int, [C.c_int, C.POINTER(_P)]),
+        "cpd_local_group_destroy": (C.c_int, [_P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -130,3 +132,13 @@ def cpd_ttm(T, pre, K, post, A, R, out, stream=None):
 def cpd_mttv(X, pre, K, post, R, v, out, beta=0, stream=None):
     check(load_library().cpd_mttv(C.c_void_p(X.data_ptr()), pre, K, post, R, C.c_void_p(v.data_ptr()),
                                   C.c_void_p(out.data_ptr()), beta, _stream_ptr(stream)))
+
+
+def cpd_local_group_create(world):
+    g = C.c_void_p()
+    check(load_library().cpd_local_group_create(world, C.byref(g)))
+    return g
+
+
+def cpd_local_group_destroy(g):
+    load_library().cpd_local_group_destroy(g)

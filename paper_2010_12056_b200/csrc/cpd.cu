@@ -32,6 +32,7 @@
 #include <vector>
 
 #include "../../include/cpd.h"
+#include "comm.h"
 #include "kernels.h"
 
 namespace {
@@ -70,6 +71,7 @@ struct cpd_ctx {
   cudaStream_t st = nullptr;
   bool own_stream = false;
   ncclComm_t comm = nullptr;
+  cpd::Comm cm;              // collective backend (NCCL or in-process local group)
   const double* T = nullptr;
   int64_t T_elems = 0;
   cpd_opts opts{};
@@ -142,6 +144,12 @@ cpd_status fail(cpd_ctx* c, cpd_status s, const std::string& msg) {
     ncclResult_t r_ = (x);                                                                    \
     if (r_ != ncclSuccess)                                                                    \
       return fail(ctx, CPD_ERR_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_));       \
+  } while (0)
+#define CM(call)                                                                              \
+  do {                                                                                        \
+    std::string m_;                                                                           \
+    int r_ = (call);                                                                          \
+    if (r_) return fail(ctx, r_ == 5 ? CPD_ERR_NCCL : CPD_ERR_CUDA, m_);                      \
   } while (0)
 #define TRY(x)                        \
   do {                                \
@@ -345,18 +353,13 @@ cpd_status allreduce_lastmode(cpd_ctx* ctx, bool with_dS) {
   if (ctx->world == 1) return CPD_OK;
   const int64_t RR = (int64_t)ctx->R * ctx->R;
   PhaseScope ps(ctx, PH_OTHER);
-  NC(ncclGroupStart());
-  NC(ncclAllReduce(ctx->S_all + (ctx->N - 1) * RR, ctx->S_all + (ctx->N - 1) * RR, RR, ncclDouble,
-                   ncclSum, ctx->comm, ctx->st));
-  if (with_dS)
-    NC(ncclAllReduce(ctx->dS_all + (ctx->N - 1) * RR, ctx->dS_all + (ctx->N - 1) * RR, RR, ncclDouble,
-                     ncclSum, ctx->comm, ctx->st));
-  NC(ncclAllReduce(ctx->scal + SC_MA, ctx->scal + SC_MA, 1, ncclDouble, ncclSum, ctx->comm, ctx->st));
-  NC(ncclAllReduce(ctx->scal + SC_DA2 + ctx->N - 1, ctx->scal + SC_DA2 + ctx->N - 1, 1, ncclDouble,
-                   ncclSum, ctx->comm, ctx->st));
-  NC(ncclAllReduce(ctx->scal + SC_A2 + ctx->N - 1, ctx->scal + SC_A2 + ctx->N - 1, 1, ncclDouble,
-                   ncclSum, ctx->comm, ctx->st));
-  NC(ncclGroupEnd());
+  CM(cpd::comm_group_start(ctx->cm, &m_));
+  CM(cpd::comm_all_reduce(ctx->cm, ctx->S_all + (ctx->N - 1) * RR, RR, &m_));
+  if (with_dS) CM(cpd::comm_all_reduce(ctx->cm, ctx->dS_all + (ctx->N - 1) * RR, RR, &m_));
+  CM(cpd::comm_all_reduce(ctx->cm, ctx->scal + SC_MA, 1, &m_));
+  CM(cpd::comm_all_reduce(ctx->cm, ctx->scal + SC_DA2 + ctx->N - 1, 1, &m_));
+  CM(cpd::comm_all_reduce(ctx->cm, ctx->scal + SC_A2 + ctx->N - 1, 1, &m_));
+  CM(cpd::comm_group_end(ctx->cm, &m_));
   return CPD_OK;
 }
 
@@ -421,7 +424,7 @@ cpd_status update_mode(cpd_ctx* ctx, int n, double* Mloc, bool pp) {
   double* Mown = Mloc + off * R;
   if (n < ctx->N - 1 && ctx->world > 1) {
     PhaseScope ps(ctx, PH_OTHER);
-    NC(ncclReduceScatter(Mloc, Mown, ro * R, ncclDouble, ncclSum, ctx->comm, ctx->st));
+    CM(cpd::comm_reduce_scatter(ctx->cm, Mloc, Mown, ro * R, &m_));
   }
   // Γ^(n) factor (and W^(n) for PP): prepared on the side stream while the MTTKRP of
   // mode n streamed, or computed here if no matching prefetch is pending
@@ -446,7 +449,7 @@ cpd_status update_mode(cpd_ctx* ctx, int n, double* Mloc, bool pp) {
   }
   if (n < ctx->N - 1 && ctx->world > 1) {
     PhaseScope ps(ctx, PH_OTHER);
-    NC(ncclAllGather(ctx->A[n] + off * R, ctx->A[n], ro * R, ncclDouble, ctx->comm, ctx->st));
+    CM(cpd::comm_all_gather(ctx->cm, ctx->A[n] + off * R, ctx->A[n], ro * R, &m_));
   }
   {
     PhaseScope ps(ctx, PH_HAD);
@@ -622,6 +625,7 @@ cpd_status cpd_opts_default(cpd_opts* o) {
   o->pp_eps = 0.1;
   o->reuse_root_in_pp_init = 1;
   o->profile_phases = 0;
+  o->local_group = nullptr;
   return CPD_OK;
 }
 
@@ -635,6 +639,17 @@ cpd_status cpd_nccl_unique_id(void* out) {
   }
   static_assert(sizeof(ncclUniqueId) == CPD_NCCL_ID_BYTES, "nccl id size");
   std::memcpy(out, &id, sizeof(id));
+  return CPD_OK;
+}
+
+cpd_status cpd_local_group_create(int world, cpd_local_group** out) {
+  if (!out || world < 1 || world > 8) return CPD_ERR_INVALID_ARG;
+  *out = (cpd_local_group*)cpd::local_group_create(world);
+  return *out ? CPD_OK : CPD_ERR_OOM;
+}
+
+cpd_status cpd_local_group_destroy(cpd_local_group* g) {
+  cpd::local_group_destroy((cpd::LocalGroup*)g);
   return CPD_OK;
 }
 
@@ -695,7 +710,10 @@ cpd_status cp_als_init(cpd_ctx** out, int N, const int64_t* shape, int R, const 
   }
   if (!(o.pp_eps > 0.0 && o.pp_eps < 1.0)) return fail(ctx, CPD_ERR_INVALID_ARG, "pp_eps must be in (0,1)");
   if (o.world < 1 || o.rank < 0 || o.rank >= o.world) return fail(ctx, CPD_ERR_INVALID_ARG, "bad rank/world");
-  if (o.world > 1 && !o.nccl_unique_id) return fail(ctx, CPD_ERR_INVALID_ARG, "world > 1 needs nccl_unique_id");
+  if (o.world > 1 && !o.nccl_unique_id && !o.local_group)
+    return fail(ctx, CPD_ERR_INVALID_ARG, "world > 1 needs nccl_unique_id or local_group");
+  if (o.local_group && cpd::local_group_world((cpd::LocalGroup*)o.local_group) != o.world)
+    return fail(ctx, CPD_ERR_INVALID_ARG, "local_group size != world");
   for (int n = 0; n < N; n++)
     if (shape[n] < 1 || !A0_host[n]) return fail(ctx, CPD_ERR_INVALID_ARG, "bad shape or factor");
   if (shape[N - 1] % o.world != 0) return fail(ctx, CPD_ERR_INVALID_ARG, "s_N must be divisible by world");
@@ -757,7 +775,7 @@ cpd_status cp_als_init(cpd_ctx** out, int N, const int64_t* shape, int R, const 
     uint64_t thr = UINT64_MAX;
     ICU(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
   }
-  if (o.world > 1) {
+  if (o.world > 1 && !o.local_group) {
     ncclUniqueId id;
     std::memcpy(&id, o.nccl_unique_id, sizeof(id));
     ncclResult_t r = ncclCommInitRank(&ctx->comm, o.world, id, o.rank);
@@ -766,6 +784,11 @@ cpd_status cp_als_init(cpd_ctx** out, int N, const int64_t* shape, int R, const 
       return bail(CPD_ERR_NCCL);
     }
   }
+  ctx->cm.nccl = ctx->comm;
+  ctx->cm.lg = (cpd::LocalGroup*)o.local_group;
+  ctx->cm.rank = o.rank;
+  ctx->cm.world = o.world;
+  ctx->cm.st = ctx->st;
   const int64_t RR = (int64_t)R * R;
   ctx->A.assign(N, nullptr);
   ctx->Aold.assign(N, nullptr);
@@ -808,12 +831,13 @@ cpd_status cp_als_init(cpd_ctx** out, int N, const int64_t* shape, int R, const 
   *out = ctx;  // provisional for cpd_set_factors
   // ||T||^2 once, all-reduced
   ICU(cpd::launch_norm2(ctx->T, ctx->T_elems, ctx->partial, ctx->scal + SC_NT2, ctx->st));
-  if (ctx->world > 1) {
-    ncclResult_t r = ncclAllReduce(ctx->scal + SC_NT2, ctx->scal + SC_NT2, 1, ncclDouble, ncclSum, ctx->comm, ctx->st);
-    if (r != ncclSuccess) {
+  {
+    std::string m_;
+    int r_ = cpd::comm_all_reduce(ctx->cm, ctx->scal + SC_NT2, 1, &m_);
+    if (r_) {
       *out = nullptr;
-      fail(ctx, CPD_ERR_NCCL, ncclGetErrorString(r));
-      return bail(CPD_ERR_NCCL);
+      fail(ctx, r_ == 5 ? CPD_ERR_NCCL : CPD_ERR_CUDA, m_);
+      return bail(r_ == 5 ? CPD_ERR_NCCL : CPD_ERR_CUDA);
     }
   }
   cpd_status s = cpd_set_factors(ctx, A0_host);
@@ -851,10 +875,7 @@ cpd_status cpd_set_factors(cpd_ctx* ctx, const double* const* A_host) {
     CU(cpd::launch_gram(ctx->A[n], ctx->A[n], nullptr, ext(ctx, n), R, ctx->S_all + n * RR, nullptr,
                         ctx->ws_gram, 32 * RR, ctx->st));
   }
-  if (ctx->world > 1) {
-    NC(ncclAllReduce(ctx->S_all + (ctx->N - 1) * RR, ctx->S_all + (ctx->N - 1) * RR, RR, ncclDouble,
-                     ncclSum, ctx->comm, ctx->st));
-  }
+  CM(cpd::comm_all_reduce(ctx->cm, ctx->S_all + (ctx->N - 1) * RR, RR, &m_));
   clear_subtree(ctx);
   ctx->t = 0;
   ctx->sub_is_msdt = false;
@@ -1001,7 +1022,7 @@ static cpd_status gather_rows(cpd_ctx* ctx, int n0, const double* src_local, dou
       CU(cudaMemcpyAsync(host_out, src_local, sizeof(double) * ctx->sN_loc * R, cudaMemcpyDeviceToHost, ctx->st));
     } else {
       if (!ctx->gather_tmp) TRY(dalloc(ctx, &ctx->gather_tmp, ctx->shape[n0] * R));
-      NC(ncclAllGather(src_local, ctx->gather_tmp, ctx->sN_loc * R, ncclDouble, ctx->comm, ctx->st));
+      CM(cpd::comm_all_gather(ctx->cm, src_local, ctx->gather_tmp, ctx->sN_loc * R, &m_));
       CU(cudaMemcpyAsync(host_out, ctx->gather_tmp, sizeof(double) * ctx->shape[n0] * R, cudaMemcpyDeviceToHost,
                          ctx->st));
     }
@@ -1023,8 +1044,8 @@ cpd_status cpd_get_last_mttkrp(cpd_ctx* ctx, int n0, double* host_out) {
   if (n0 < 0 || n0 >= ctx->N || !host_out) return fail(ctx, CPD_ERR_INVALID_ARG, "bad mode");
   if (n0 < ctx->N - 1 && ctx->world > 1) {
     int64_t ro = rows_own(ctx, n0);
-    NC(ncclAllGather(ctx->Mlast[n0] + own_off(ctx, n0) * ctx->R, ctx->Mlast[n0], ro * ctx->R, ncclDouble,
-                     ctx->comm, ctx->st));
+    CM(cpd::comm_all_gather(ctx->cm, ctx->Mlast[n0] + own_off(ctx, n0) * ctx->R, ctx->Mlast[n0], ro * ctx->R,
+                            &m_));
   }
   return gather_rows(ctx, n0, ctx->Mlast[n0], host_out);
 }

@@ -22,7 +22,7 @@ class CPDecomposition:
     """
 
     def __init__(self, T, shape, R, A0, *, device=0, rank=0, world=1, nccl_id=None, stream=None,
-                 pp_eps=0.1, reuse_root_in_pp_init=True, profile_phases=False):
+                 pp_eps=0.1, reuse_root_in_pp_init=True, profile_phases=False, local_group=None):
         lib = load_library()
         self.N = len(shape)
         self.shape = tuple(int(s) for s in shape)
@@ -40,6 +40,7 @@ class CPDecomposition:
         o.pp_eps = float(pp_eps)
         o.reuse_root_in_pp_init = int(bool(reuse_root_in_pp_init))
         o.profile_phases = int(bool(profile_phases))
+        o.local_group = local_group.value if local_group is not None else None
         A0 = [np.ascontiguousarray(a, dtype=np.float64) for a in A0]
         shp = (C.c_int64 * self.N)(*self.shape)
         ctx = C.c_void_p()

@@ -1,0 +1,110 @@
+"""The 1-D-grid multi-rank path (Alg. 3 / Alg. 4: slab-local contractions, reduce-scatter
+of the partial MTTKRP, all-gather of factor rows, all-reduce of the last mode's Gram, dS and
+scalars) run on ONE GPU with P ranks of an in-process cpd_local_group, each rank driven by
+its own host thread, compared with P = 1 and with the oracle (-m gpu)."""
+import threading
+
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def cpd():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2010_12056_b200 as pkg
+    from paper_2010_12056_b200 import build
+    build.build()
+    pkg.load_library()
+    return pkg
+
+
+def slab(cpd, cfg, rank, world):
+    lo, hi = synth.slab_range(cfg.s, rank, world)
+    T = torch.empty([cfg.s] * (cfg.N - 1) + [hi - lo], dtype=torch.float64, device="cuda")
+    cpd.cpd_gen_tensor(T, cfg.shape, lo, hi, 0, synth.true_factors(cfg), np.sqrt(cfg.noise_var), cfg.seed_noise)
+    torch.cuda.synchronize()
+    return T
+
+
+def schedule(m, N):
+    """3 MSDT sweeps, PP init + 2 PP sweeps, 1 MSDT sweep, 1 DT sweep; record everything."""
+    rec = {"f": [], "M": [], "A": []}
+    for _ in range(3):
+        rec["f"].append(m.msdt_sweep())
+        rec["M"].append([m.get_last_mttkrp(n) for n in range(N)])
+    rec["A"].append([m.get_factor(n) for n in range(N)])
+    m.pp_init()
+    for _ in range(2):
+        rec["f"].append(m.pp_approx_sweep()[0])
+        rec["M"].append([m.get_last_mttkrp(n) for n in range(N)])
+    rec["f"].append(m.msdt_sweep())
+    rec["f"].append(m.dt_sweep())
+    rec["A"].append([m.get_factor(n) for n in range(N)])
+    return rec
+
+
+def run_group(cpd, cfg, P):
+    group = cpd.cpd_local_group_create(P)
+    Ts = [slab(cpd, cfg, r, P) for r in range(P)]
+    out, errs = [None] * P, []
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(0)
+            m = cpd.cp_als_init(Ts[r], cfg.shape, cfg.R, synth.init_factors(cfg), rank=r, world=P,
+                                local_group=group, stream=torch.cuda.Stream())
+            out[r] = schedule(m, cfg.N)
+            m.close()
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append((r, repr(e)))
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(300)
+    cpd.cpd_local_group_destroy(group)
+    assert not errs, errs
+    assert all(not t.is_alive() for t in th)
+    return out
+
+
+@pytest.mark.parametrize("cfg,P", [(synth.config(1), 2), (synth.config(1), 4), (synth.custom(4, 8, 3, noise_var=1e-3, seed=31), 2),
+                                   (synth.custom(3, 16, 5, noise_var=1e-4, seed=32), 8)])
+def test_local_group_equals_single_rank_and_oracle(cpd, cfg, P):
+    ref = run_group(cpd, cfg, 1)[0]
+    got = run_group(cpd, cfg, P)
+    for r in range(P):  # every rank returns the same gathered results
+        for a, b in zip(got[r]["f"], ref["f"]):
+            assert abs(a - b) <= TOL * abs(b)
+        for Ms, Mr in zip(got[r]["M"], ref["M"]):
+            for a, b in zip(Ms, Mr):
+                assert np.linalg.norm(a - b) <= TOL * np.linalg.norm(b)
+        for As, Ar in zip(got[r]["A"], ref["A"]):
+            for a, b in zip(As, Ar):
+                assert np.linalg.norm(a - b) <= TOL * np.linalg.norm(b)
+    # and the first three sweeps against the oracle directly
+    T = O.make_tensor(cfg)
+    A = synth.init_factors(cfg)
+    for k in range(3):
+        o = O.als_sweep(T, A)
+        A = o["A"]
+        assert abs(got[0]["f"][k] - o["f"]) <= TOL * abs(o["f"])
+
+
+def test_local_group_rejects_bad_world(cpd):
+    g = cpd.cpd_local_group_create(2)
+    cfg = synth.custom(3, 8, 2, seed=33)
+    T = slab(cpd, cfg, 0, 4)
+    with pytest.raises(cpd.CPDError) as e:
+        cpd.cp_als_init(T, cfg.shape, cfg.R, synth.init_factors(cfg), rank=0, world=4, local_group=g)
+    assert e.value.status == 1
+    cpd.cpd_local_group_destroy(g)
