@@ -21,9 +21,7 @@ namespace cpd {
 namespace {
 
 constexpr int BM = 128;
-constexpr int BK = 16;
 constexpr int THREADS = 256;
-constexpr int LDA_KC = BK + 4;   // [BM][BK+4]  : (g*20 + t) mod 16 distinct for g,t < 4
 constexpr int LDA_MC = BM + 4;   // [BK][BM+4]  : (t*132 + g) mod 16 distinct
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -50,10 +48,13 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 
 template <int NF>
 struct Smem {
-  // NF <= 8 (R <= 64 per tile, <= 128 registers): 3 stages so two CTAs (16 warps) fit
-  // per SM; wider tiles keep 4 stages at one CTA per SM.
-  static constexpr int STAGES = NF <= 8 ? 3 : 4;
+  // NF <= 8 (R <= 64 per tile, <= 128 registers): BK = 32, 2 stages, two CTAs (16 warps)
+  // per SM (fewer barriers per flop); wider tiles (one CTA per SM by registers): BK = 16,
+  // 4 stages.  Chosen by measurement on the BASELINE shapes (tools/bench_ttm.cu).
+  static constexpr int BK = NF <= 8 ? 32 : 16;
+  static constexpr int STAGES = NF <= 8 ? 2 : 4;
   static constexpr int MIN_BLOCKS = NF <= 8 ? 2 : 1;
+  static constexpr int LDA_KC = BK + 4;  // [BM][BK+4]: (g*LDA + t) mod 16 distinct for g,t < 4
   static constexpr int BN = 8 * NF;
   static constexpr int LDB = ((BN + 15) / 16) * 16 + 4;
   static constexpr int A_ELEMS = (BM * LDA_KC > BK * LDA_MC) ? BM * LDA_KC : BK * LDA_MC;
@@ -72,6 +73,8 @@ __global__ void __launch_bounds__(THREADS, Smem<NF>::MIN_BLOCKS)
   using S = Smem<NF>;
   constexpr int BN = S::BN;
   constexpr int STAGES = S::STAGES;
+  constexpr int BK = S::BK;
+  constexpr int LDA_KC = S::LDA_KC;
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -85,15 +88,17 @@ __global__ void __launch_bounds__(THREADS, Smem<NF>::MIN_BLOCKS)
   const int64_t nk = (K + BK - 1) / BK;
 
   // ---- per-thread constant parts of the T addresses ----
-  // KC: VEC2 -> chunk c = tid%8 (k pair), rows tid/8 + 32q (q<4);  scalar -> col tid%16, rows tid/16 + 16q (q<8)
-  // MC: VEC2 -> row pair 2*(tid%64), k-rows tid/64 + 4q (q<4);    scalar -> row tid%128, k-rows tid/128 + 2q (q<8)
-  constexpr int NQ = VEC2 ? 4 : 8;
+  // KC: CPR chunks (k pairs, or single k) per row; thread: chunk tid%CPR, rows tid/CPR + RSTEP*q
+  // MC: row pair 2*(tid%64) (or row tid%128), k-rows tid/64 + 4q (or tid/128 + 2q)
+  constexpr int CPR = VEC2 ? BK / 2 : BK;
+  constexpr int RSTEP = THREADS / CPR;
+  constexpr int NQ = MC ? (VEC2 ? BK / 4 : BK / 2) : BM / RSTEP;
   int64_t abase[MC ? 1 : NQ];
   bool arow_ok[MC ? 1 : NQ];
   if constexpr (!MC) {
 #pragma unroll
     for (int q = 0; q < NQ; q++) {
-      int r = VEC2 ? (tid / 8 + 32 * q) : (tid / 16 + 16 * q);
+      int r = tid / CPR + RSTEP * q;
       int64_t i = i0 + r;
       arow_ok[q] = i < Mrows;
       abase[q] = (arow_ok[q] ? i : 0) * K;
@@ -115,12 +120,12 @@ __global__ void __launch_bounds__(THREADS, Smem<NF>::MIN_BLOCKS)
 #pragma unroll
       for (int q = 0; q < NQ; q++) {
         if constexpr (VEC2) {
-          int r = tid / 8 + 32 * q, c = tid % 8;
+          int r = tid / CPR + RSTEP * q, c = tid % CPR;
           int64_t k = k0 + 2 * c;
           bool ok = arow_ok[q] && k < K;
           cp16(As + r * LDA_KC + 2 * c, X + abase[q] + (ok ? k : 0), ok);
         } else {
-          int r = tid / 16 + 16 * q, c = tid % 16;
+          int r = tid / CPR + RSTEP * q, c = tid % CPR;
           int64_t k = k0 + c;
           bool ok = arow_ok[q] && k < K;
           cp8(As + r * LDA_KC + c, X + abase[q] + (ok ? k : 0), ok);
@@ -144,9 +149,9 @@ __global__ void __launch_bounds__(THREADS, Smem<NF>::MIN_BLOCKS)
     }
     // B tile: BK x BN from B[k0.., n0..]
     if constexpr (BVEC2) {
-      constexpr int CPR = BN / 2;  // chunks per k-row
-      for (int e = tid; e < BK * CPR; e += THREADS) {
-        int y = e / CPR, c = e % CPR;
+      constexpr int BCPR = BN / 2;  // chunks per k-row
+      for (int e = tid; e < BK * BCPR; e += THREADS) {
+        int y = e / BCPR, c = e % BCPR;
         int64_t k = k0 + y;
         int n = n0 + 2 * c;
         bool ok = k < K && n < ncols;
