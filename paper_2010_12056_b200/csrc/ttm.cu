@@ -20,9 +20,6 @@
 namespace cpd {
 namespace {
 
-constexpr int BM = 128;
-constexpr int THREADS = 256;
-constexpr int LDA_MC = BM + 4;   // [BK][BM+4]  : (t*132 + g) mod 16 distinct
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -48,12 +45,16 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 
 template <int NF>
 struct Smem {
-  // NF <= 8 (R <= 64 per tile, <= 128 registers): BK = 32, 2 stages, two CTAs (16 warps)
-  // per SM (fewer barriers per flop); wider tiles (one CTA per SM by registers): BK = 16,
-  // 4 stages.  Chosen by measurement on the BASELINE shapes (tools/bench_ttm.cu).
+  // Tile shapes per accumulator width (measured on the BASELINE shapes, tools/bench_ttm.cu):
+  //   NF <= 4 : BM  64, BK 32, 2 stages, 4 CTAs/SM  (short K, e.g. C4 K = 64: CTAs overlap)
+  //   NF <= 8 : BM 128, BK 32, 2 stages, 2 CTAs/SM  (C2: 89 % of the DMMA peak)
+  //   NF > 8  : BM  64, BK 16, 4 stages, 2 CTAs/SM  (> 128 registers per thread)
   static constexpr int BK = NF <= 8 ? 32 : 16;
   static constexpr int STAGES = NF <= 8 ? 2 : 4;
-  static constexpr int MIN_BLOCKS = NF <= 8 ? 2 : 1;
+  static constexpr int BM = (NF <= 4 || NF > 8) ? 64 : 128;
+  static constexpr int THREADS = 2 * BM;  // 16 rows per warp
+  static constexpr int MIN_BLOCKS = NF <= 4 ? 4 : 2;
+  static constexpr int LDA_MC = BM + 4;  // [BK][BM+4]: (t*LDA + g) mod 16 distinct
   static constexpr int LDA_KC = BK + 4;  // [BM][BK+4]: (g*LDA + t) mod 16 distinct for g,t < 4
   static constexpr int BN = 8 * NF;
   static constexpr int LDB = ((BN + 15) / 16) * 16 + 4;
@@ -66,7 +67,7 @@ struct Smem {
 // MC: post > 1 (M-contiguous rows); VEC2: 16-byte chunks (requires post even for MC,
 // K even for KC, ncols even for B).
 template <int NF, bool MC, bool VEC2, bool BVEC2>
-__global__ void __launch_bounds__(THREADS, Smem<NF>::MIN_BLOCKS)
+__global__ void __launch_bounds__(Smem<NF>::THREADS, Smem<NF>::MIN_BLOCKS)
     ttm_dmma_kernel(const double* __restrict__ X, int64_t pre, int64_t K, int64_t post,
                     const double* __restrict__ B, int ncols, int ntiles_n,
                     double* __restrict__ out, int beta) {
@@ -75,6 +76,10 @@ __global__ void __launch_bounds__(THREADS, Smem<NF>::MIN_BLOCKS)
   constexpr int STAGES = S::STAGES;
   constexpr int BK = S::BK;
   constexpr int LDA_KC = S::LDA_KC;
+  constexpr int LDA_MC = S::LDA_MC;
+  constexpr int BM = S::BM;
+  constexpr int THREADS = S::THREADS;
+  constexpr int HB = BM / 2;  // MC 16-byte chunks per k-row
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -92,7 +97,7 @@ __global__ void __launch_bounds__(THREADS, Smem<NF>::MIN_BLOCKS)
   // MC: row pair 2*(tid%64) (or row tid%128), k-rows tid/64 + 4q (or tid/128 + 2q)
   constexpr int CPR = VEC2 ? BK / 2 : BK;
   constexpr int RSTEP = THREADS / CPR;
-  constexpr int NQ = MC ? (VEC2 ? BK / 4 : BK / 2) : BM / RSTEP;
+  constexpr int NQ = MC ? (VEC2 ? BK / (THREADS / HB) : BK / (THREADS / BM)) : BM / RSTEP;
   int64_t abase[MC ? 1 : NQ];
   bool arow_ok[MC ? 1 : NQ];
   if constexpr (!MC) {
@@ -104,7 +109,7 @@ __global__ void __launch_bounds__(THREADS, Smem<NF>::MIN_BLOCKS)
       abase[q] = (arow_ok[q] ? i : 0) * K;
     }
   } else {
-    int r = VEC2 ? 2 * (tid % 64) : (tid % 128);
+    int r = VEC2 ? 2 * (tid % HB) : (tid % BM);
     int64_t i = i0 + r;
     arow_ok[0] = i < Mrows;
     int64_t ii = arow_ok[0] ? i : 0;
@@ -135,12 +140,12 @@ __global__ void __launch_bounds__(THREADS, Smem<NF>::MIN_BLOCKS)
 #pragma unroll
       for (int q = 0; q < NQ; q++) {
         if constexpr (VEC2) {
-          int y = tid / 64 + 4 * q, c = tid % 64;
+          int y = tid / HB + (THREADS / HB) * q, c = tid % HB;
           int64_t k = k0 + y;
           bool ok = arow_ok[0] && k < K;
           cp16(As + y * LDA_MC + 2 * c, X + abase[0] + (ok ? k * post : 0), ok);
         } else {
-          int y = tid / 128 + 2 * q, c = tid % 128;
+          int y = tid / BM + (THREADS / BM) * q, c = tid % BM;
           int64_t k = k0 + y;
           bool ok = arow_ok[0] && k < K;
           cp8(As + y * LDA_MC + c, X + abase[0] + (ok ? k * post : 0), ok);
@@ -250,11 +255,12 @@ cudaError_t launch_nf(const double* X, int64_t pre, int64_t K, int64_t post, con
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
+  constexpr int BM = Smem<NF>::BM;
   int64_t mt = (pre * post + BM - 1) / BM;
   int64_t grid = mt * ntiles_n;
   if (grid > 0x7fffffff) return cudaErrorInvalidConfiguration;
   g_launches++;
-  kern<<<(unsigned)grid, THREADS, smem, st>>>(X, pre, K, post, B, ncols, ntiles_n, out, beta);
+  kern<<<(unsigned)grid, Smem<NF>::THREADS, smem, st>>>(X, pre, K, post, B, ncols, ntiles_n, out, beta);
   return cudaGetLastError();
 }
 
@@ -285,8 +291,11 @@ cudaError_t launch_ttm(const double* X, int64_t pre, int64_t K, int64_t post, co
                        int ncols, double* out, int beta, cudaStream_t st) {
   if (pre <= 0 || post <= 0 || ncols <= 0) return cudaSuccess;
   if (K <= 0) return cudaErrorInvalidValue;
+#ifndef CPD_TTM_MAXNF
+#define CPD_TTM_MAXNF 16
+#endif
   int nf_total = (ncols + 7) / 8;
-  int ntiles = (nf_total + 15) / 16;
+  int ntiles = (nf_total + CPD_TTM_MAXNF - 1) / CPD_TTM_MAXNF;
   int nf = (nf_total + ntiles - 1) / ntiles;
   switch (nf) {
     case 1: return dispatch_layout<1>(X, pre, K, post, B, ncols, ntiles, out, beta, st);
