@@ -66,7 +66,9 @@ typedef struct {
   void* stream;               /* cudaStream_t to run on, or NULL (library creates one) */
   double pp_eps;              /* ε in (0,1) for still_valid / cpd_pp_condition (Alg. 2 line 5) */
   int reuse_root_in_pp_init;  /* P:384 footnote: reuse a still-valid MSDT root in pp_init (default 1) */
-  int profile_phases;         /* 1: CUDA-event timers per phase (TTM, mTTV, solve, hadamard, other) */
+  int profile_phases;         /* CUDA-event timers: 0 off; 1 TTM and mTTV launches only (the roofline
+                                 kernels, low overhead); 2 every phase (TTM, mTTV, solve, hadamard,
+                                 other; the P:748 breakdown) */
   void* local_group;          /* NULL: NCCL (one process per GPU).  Else a cpd_local_group of `world`
                                  ranks in ONE process on ONE device, each rank's calls made from its own
                                  host thread (verification of the 1-D partition on a single GPU) */
@@ -149,6 +151,9 @@ cpd_status cpd_get_phase_ms(cpd_ctx* ctx, double out[5]);
  * out[3]=mTTV/PP-stream launches, out[4]=first-level TTMs (roots) built,
  * out[5]=kernels launched by libcpd.so in this process (all kernels, monotone; not reset). */
 cpd_status cpd_get_counters(cpd_ctx* ctx, double out[6]);
+
+/* Change the timer level of opts.profile_phases (0, 1, 2) between calls. */
+cpd_status cpd_set_profile_level(cpd_ctx* ctx, int level);
 
 /* Zero the phase timers and counters. */
 cpd_status cpd_reset_counters(cpd_ctx* ctx);

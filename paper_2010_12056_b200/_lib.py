@@ -20,7 +20,7 @@ EXPORTED_SYMBOLS = [
     "pp_approx_sweep", "fitness", "cpd_pp_condition", "cpd_get_factor", "cpd_get_last_mttkrp",
     "cpd_set_factors", "cpd_get_phase_ms", "cpd_get_counters", "cpd_reset_counters",
     "cpd_debug_get_pp_operator", "cpd_last_error", "cpd_destroy", "cpd_gen_tensor", "cpd_ttm",
-    "cpd_mttv", "cpd_local_group_create", "cpd_local_group_destroy",
+    "cpd_mttv", "cpd_local_group_create", "cpd_local_group_destroy", "cpd_set_profile_level",
 ]
 
 
@@ -66,6 +66,7 @@ def load_library():
         "cpd_get_phase_ms": (C.c_int, [_P, _D]),
         "cpd_get_counters": (C.c_int, [_P, _D]),
         "cpd_reset_counters": (C.c_int, [_P]),
+        "cpd_set_profile_level": (C.c_int, [_P, C.c_int]),
         "cpd_debug_get_pp_operator": (C.c_int, [_P, C.c_int, C.c_int, _D]),
         "cpd_last_error": (C.c_char_p, [_P]),
         "cpd_destroy": (C.c_int, [_P]),

@@ -76,7 +76,7 @@ struct cpd_ctx {
   int64_t T_elems = 0;
   cpd_opts opts{};
   // factors: mode N-1 holds only the local slab rows
-  std::vector<double*> A, Aold, dA, Mlast, Ap, Mp;
+  std::vector<double*> A, Aold, dA, Mlast, Ap, Mp, Mt;
   double* S_all = nullptr;   // N x R x R
   double* dS_all = nullptr;  // N x R x R
   double* Lp[2] = {nullptr, nullptr};  // packed Cholesky factors (double-buffered)
@@ -185,7 +185,10 @@ struct PhaseScope {
   cpd_ctx* c;
   PhaseRec rec;
   bool on;
-  PhaseScope(cpd_ctx* ctx, int phase) : c(ctx), on(ctx->opts.profile_phases != 0) {
+  // profile level 1: only the two roofline kernels (TTM, mTTV) are bracketed, so the timers
+  // add ~4 event records per mode update; level 2: every phase (P:748 breakdown)
+  PhaseScope(cpd_ctx* ctx, int phase)
+      : c(ctx), on(ctx->opts.profile_phases >= 2 || (ctx->opts.profile_phases == 1 && phase <= PH_MTTV)) {
     if (on) {
       rec.a = get_event(c);
       rec.b = get_event(c);
@@ -507,6 +510,7 @@ void free_pp(cpd_ctx* c) {
   for (auto& kv : c->ops) dfree(c, kv.second);
   c->ops.clear();
   for (auto& p : c->Mp) dfree(c, p);
+  for (auto& p : c->Mt) dfree(c, p);
   c->pp_valid = false;
 }
 
@@ -660,7 +664,7 @@ cpd_status cpd_destroy(cpd_ctx* c) {
   cudaSetDevice(c->dev);
   clear_subtree(c);
   free_pp(c);
-  for (auto* v : {&c->A, &c->Aold, &c->dA, &c->Mlast, &c->Ap, &c->Mp})
+  for (auto* v : {&c->A, &c->Aold, &c->dA, &c->Mlast, &c->Ap, &c->Mp, &c->Mt})
     for (auto& p : *v) dfree(c, p);
   dfree(c, c->S_all);
   dfree(c, c->dS_all);
@@ -796,6 +800,7 @@ cpd_status cp_als_init(cpd_ctx** out, int N, const int64_t* shape, int R, const 
   ctx->Mlast.assign(N, nullptr);
   ctx->Ap.assign(N, nullptr);
   ctx->Mp.assign(N, nullptr);
+  ctx->Mt.assign(N, nullptr);
   for (int n = 0; n < N; n++) {
     int64_t e = ext(ctx, n) * R;
     ITRY(dalloc(ctx, &ctx->A[n], e));
@@ -962,6 +967,7 @@ cpd_status pp_init(cpd_ctx* ctx) {
     int o = n == 0 ? 1 : 0;
     int a = std::min(n, o), b = std::max(n, o);
     TRY(dalloc(ctx, &ctx->Mp[n], ext(ctx, n) * ctx->R));
+    TRY(dalloc(ctx, &ctx->Mt[n], ext(ctx, n) * ctx->R));
     TRY(mttv(ctx, ctx->ops[{a, b}], {a, b}, o, ctx->Ap[o], ctx->Mp[n], 0));
   }
   CU(cudaStreamSynchronize(ctx->st));
@@ -978,22 +984,31 @@ cpd_status pp_approx_sweep(cpd_ctx* ctx, double* fitness_out, int* still_valid) 
   if (!ctx->pp_valid || !ctx->pp_regime) return fail(ctx, CPD_ERR_STATE, "pp_approx_sweep needs a valid pp_init");
   const int N = ctx->N;
   for (int n = 0; n < N; n++) {
-    double* Mt = nullptr;
-    TRY(dalloc(ctx, &Mt, ext(ctx, n) * ctx->R));
-    {
-      PhaseScope ps(ctx, PH_OTHER);
-      CU(cudaMemcpyAsync(Mt, ctx->Mp[n], sizeof(double) * ext(ctx, n) * ctx->R, cudaMemcpyDeviceToDevice,
-                         ctx->st));
-    }
+    // M~_loc^(n) = M_p^(n) + Σ_{i≠n} U^(n,i) (Eqs. 5-6): the N-1 operator streams of this mode
+    // in one launch, summed with M_p^(n) in a fixed order
+    cpd::MttvSpec sp[CPD_MAX_ORDER];
+    int J = 0;
+    double bytes = 0.0;
     for (int i = 0; i < N; i++) {
       if (i == n) continue;
-      int a = std::min(n, i), b = std::max(n, i);
-      // U^(n,i) (Eq. 6): contract the operator's axis of mode i with dA^(i)
-      TRY(mttv(ctx, ctx->ops[{a, b}], {a, b}, i, ctx->dA[i], Mt, 1));
+      const int a = std::min(n, i), b = std::max(n, i);
+      // operator [s_a, s_b, R]: contract the axis of mode i
+      sp[J].X = ctx->ops[{a, b}];
+      sp[J].v = ctx->dA[i];
+      sp[J].K = ext(ctx, i);
+      sp[J].pre = n < i ? ext(ctx, n) : 1;
+      sp[J].post = n < i ? 1 : ext(ctx, n);
+      bytes += 8.0 * ((double)ext(ctx, a) * ext(ctx, b) * ctx->R + (double)ext(ctx, i) * ctx->R);
+      J++;
     }
-    cpd_status s = update_mode(ctx, n, Mt, true);
-    dfree(ctx, Mt);
-    if (s != CPD_OK) return s;
+    double* Mt = ctx->Mt[n];
+    {
+      PhaseScope ps(ctx, PH_MTTV);
+      CU(cpd::launch_mttv_multi(sp, J, ctx->R, ctx->Mp[n], Mt, 0, ctx->ws_mttv, kMttvWs, ctx->st));
+    }
+    ctx->counters[2] += bytes + 8.0 * 2 * ext(ctx, n) * ctx->R;
+    ctx->counters[3] += 1;
+    TRY(update_mode(ctx, n, Mt, true));
   }
   TRY(finish_sweep(ctx, fitness_out));
   if (still_valid) *still_valid = pp_cond(ctx) ? 1 : 0;
@@ -1062,6 +1077,14 @@ cpd_status cpd_get_counters(cpd_ctx* ctx, double out[6]) {
   if (!ctx || !out) return CPD_ERR_INVALID_ARG;
   for (int i = 0; i < 5; i++) out[i] = ctx->counters[i];
   out[5] = (double)cpd::g_launches.load();
+  return CPD_OK;
+}
+
+cpd_status cpd_set_profile_level(cpd_ctx* ctx, int level) {
+  if (!ctx || level < 0 || level > 2) return CPD_ERR_INVALID_ARG;
+  cudaStreamSynchronize(ctx->st);
+  drain_timers(ctx);
+  ctx->opts.profile_phases = level;
   return CPD_OK;
 }
 

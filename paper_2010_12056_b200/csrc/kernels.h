@@ -24,6 +24,17 @@ cudaError_t launch_mttv(const double* X, int64_t pre, int64_t K, int64_t post, i
                         const double* v, double* out, int beta, double* ws, int64_t ws_elems,
                         cudaStream_t st);
 
+// Several contractions with the same output shape summed into one output (the N-1
+// U-streams of a PP mode, Eq. 6): out = base + Σ_jobs contraction_j (base may be null:
+// then out = beta*out + Σ).  One launch plus one fixed-order reduce.
+struct MttvSpec {
+  const double* X;
+  const double* v;
+  int64_t pre, K, post;
+};
+cudaError_t launch_mttv_multi(const MttvSpec* specs, int J, int R, const double* base, double* out, int beta,
+                              double* ws, int64_t ws_elems, cudaStream_t st);
+
 // ---- synthetic tensor (synth/__init__.py recipe) ------------------------------------
 // T[q, z] += std*normal(seed, g) (kind 0) or T = uniform(seed, g) (kind 1) with
 // g = q*sN + lo + z the global index, T viewed as [Q, w] (w = hi - lo).

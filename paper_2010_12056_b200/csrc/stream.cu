@@ -20,28 +20,46 @@ namespace {
 constexpr int MT_THREADS = 256;
 constexpr int MT_COLS = 64;  // columns per CTA (32 lanes x double2)
 
-// One CTA = one work item (p, 64-column chunk, K-split); 8 warps interleave the rows of
-// the split, 4 rows in flight per warp; fixed-order shared-memory reduction.  With
-// ks > 1 the partial sums go to ws[split][p*C + c] and mttv_reduce_kernel adds them in
-// split order (deterministic).
+// One CTA = one work item (job, p, 64-column chunk, K-split); 8 warps interleave the rows
+// of the split, 4 rows in flight per warp; fixed-order shared-memory reduction.  A launch
+// may carry several jobs with the same output shape (the N-1 U-streams of one PP mode,
+// Eq. 6): their partial sums go to ws[slot][p*C + c] and mttv_reduce_kernel adds base
+// (M_p^(n)) and the slots in job/split order (deterministic).  A single job with no
+// K-split writes out directly (out = beta*out + sum).
+struct MttvJob {
+  const double* X;
+  const double* v;
+  int64_t pre, K, C, rps, item0, slot0;
+  int nchunks, ks;
+};
+struct MttvJobs {
+  MttvJob j[8];
+  int J;
+  int64_t E;  // output elements (pre*C, same for every job)
+};
+
 template <bool VEC2, bool VV>
 __global__ void __launch_bounds__(MT_THREADS)
-    mttv_kernel(const double* __restrict__ X, int64_t pre, int64_t K, int64_t C, int R,
-                const double* __restrict__ v, double* __restrict__ out, int beta, int nchunks, int ks,
-                int64_t rps, double* __restrict__ ws) {
+    mttv_kernel(MttvJobs jobs, int R, double* __restrict__ out, int beta, double* __restrict__ ws) {
   __shared__ double red[8][MT_COLS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int split = blockIdx.x % ks;
-  const int64_t rest = blockIdx.x / ks;
-  const int64_t p = rest / nchunks;
-  const int chunk = (int)(rest % nchunks);
-  const int64_t k0 = split * rps;
-  const int64_t k1 = min(K, k0 + rps);
+  int jj = 0;
+  while (jj + 1 < jobs.J && (int64_t)blockIdx.x >= jobs.j[jj + 1].item0) jj++;
+  const MttvJob& jb = jobs.j[jj];
+  const int64_t local = (int64_t)blockIdx.x - jb.item0;
+  const int split = (int)(local % jb.ks);
+  const int64_t rest = local / jb.ks;
+  const int64_t p = rest / jb.nchunks;
+  const int chunk = (int)(rest % jb.nchunks);
+  const int64_t K = jb.K, C = jb.C;
+  const double* __restrict__ v = jb.v;
+  const int64_t k0 = split * jb.rps;
+  const int64_t k1 = min(K, k0 + jb.rps);
   const int64_t cA = (int64_t)chunk * MT_COLS + (VEC2 ? 2 * lane : lane);
   const int64_t cB = VEC2 ? cA + 1 : cA + 32;
   const bool okA = cA < C, okB = cB < C;
   const int rA = okA ? (int)(cA % R) : 0, rB = okB ? (int)(cB % R) : 0;
-  const double* Xp = X + p * K * C;
+  const double* Xp = jb.X + p * K * C;
   double sA = 0.0, sB = 0.0;
   if (okA) {
     int64_t y = k0 + warp;
@@ -100,22 +118,23 @@ __global__ void __launch_bounds__(MT_THREADS)
       double s = red[0][threadIdx.x];
 #pragma unroll
       for (int w = 1; w < 8; w++) s += red[w][threadIdx.x];
-      if (ks == 1) {
+      if (ws == nullptr) {
         double* o = out + p * C + c;
         *o = beta ? *o + s : s;
       } else {
-        ws[split * pre * C + p * C + c] = s;
+        ws[(jb.slot0 + split) * jobs.E + p * C + c] = s;
       }
     }
   }
 }
 
-__global__ void mttv_reduce_kernel(const double* __restrict__ ws, int ks, int64_t n, double* __restrict__ out,
-                                   int beta) {
+// out[e] = (base ? base[e] : beta*out[e]) + Σ_slot ws[slot*n + e]   (slot order fixed)
+__global__ void mttv_reduce_kernel(const double* __restrict__ ws, int slots, int64_t n, const double* __restrict__ base,
+                                   double* __restrict__ out, int beta) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    double s = ws[e];
-    for (int k = 1; k < ks; k++) s += ws[k * n + e];
-    out[e] = beta ? out[e] + s : s;
+    double s = base ? base[e] : (beta ? out[e] : 0.0);
+    for (int k = 0; k < slots; k++) s += ws[k * n + e];
+    out[e] = s;
   }
 }
 
@@ -219,44 +238,90 @@ __global__ void sub_kernel(const double* __restrict__ x, const double* __restric
 
 }  // namespace
 
-cudaError_t launch_mttv(const double* X, int64_t pre, int64_t K, int64_t post, int R,
-                        const double* v, double* out, int beta, double* ws, int64_t ws_elems, cudaStream_t st) {
-  const int64_t C = post * R;
-  if (pre <= 0 || C <= 0) return cudaSuccess;
-  if (K <= 0) return cudaErrorInvalidValue;
-  const bool vec2 = (C % 2) == 0 && ((uintptr_t)X % 16) == 0;
-  const bool vv = vec2 && (R % 2) == 0 && ((uintptr_t)v % 16) == 0;
-  const int nchunks = (int)((C + MT_COLS - 1) / MT_COLS);
-  const int64_t items0 = pre * nchunks;
-  // split K so that the grid is >= ~8 waves of 4 resident CTAs per SM (tail <= 1/8 wave)
-  int64_t ks = (148 * 4 * 8 + items0 - 1) / items0;
-  int64_t max_by_rows = K / 64;
-  if (ks > max_by_rows) ks = max_by_rows;
-  if (ks > 16) ks = 16;
-  if (ws == nullptr || ks * pre * C > ws_elems) ks = 1;
-  if (ks < 1) ks = 1;
-  const int64_t rps = (K + ks - 1) / ks;
-  int64_t grid = items0 * ks;
-  if (grid > 0x7fffffff) return cudaErrorInvalidConfiguration;
+cudaError_t launch_mttv_multi(const MttvSpec* specs, int J, int R, const double* base, double* out, int beta,
+                              double* ws, int64_t ws_elems, cudaStream_t st) {
+  if (J < 1 || J > 8) return cudaErrorInvalidValue;
+  MttvJobs jobs{};
+  jobs.J = J;
+  jobs.E = specs[0].pre * specs[0].post * R;
+  bool vec2 = true, vv = (R % 2) == 0;
+  int64_t items = 0, slots = 0;
+  for (int q = 0; q < J; q++) {
+    const MttvSpec& sp = specs[q];
+    MttvJob& jb = jobs.j[q];
+    jb.X = sp.X;
+    jb.v = sp.v;
+    jb.pre = sp.pre;
+    jb.K = sp.K;
+    jb.C = sp.post * R;
+    if (jb.pre * jb.C != jobs.E || jb.K <= 0) return cudaErrorInvalidValue;
+    jb.nchunks = (int)((jb.C + MT_COLS - 1) / MT_COLS);
+    vec2 = vec2 && (jb.C % 2) == 0 && ((uintptr_t)sp.X % 16) == 0;
+    vv = vv && ((uintptr_t)sp.v % 16) == 0;
+    const int64_t items0 = jb.pre * jb.nchunks;
+    // split K so the whole grid is >= ~8 waves of 4 resident CTAs per SM (tail <= 1/8 wave)
+    int64_t ks = (148 * 4 * 8 / J + items0 - 1) / items0;
+    if (ks > jb.K / 64) ks = jb.K / 64;
+    if (ks > 16) ks = 16;
+    if (ks < 1) ks = 1;
+    jb.ks = (int)ks;
+    jb.rps = (jb.K + ks - 1) / ks;
+    jb.item0 = items;
+    jb.slot0 = slots;
+    items += items0 * ks;
+    slots += ks;
+  }
+  const bool direct = (J == 1 && slots == 1 && base == nullptr);
+  if (!direct && (ws == nullptr || slots * jobs.E > ws_elems)) {
+    // not enough workspace: fall back to one direct launch per job, no K-split
+    if (base) {
+      cudaError_t e = cudaMemcpyAsync(out, base, sizeof(double) * jobs.E, cudaMemcpyDeviceToDevice, st);
+      if (e != cudaSuccess) return e;
+      beta = 1;
+    }
+    for (int q = 0; q < J; q++) {
+      MttvJobs one{};
+      one.J = 1;
+      one.E = jobs.E;
+      one.j[0] = jobs.j[q];
+      one.j[0].ks = 1;
+      one.j[0].rps = one.j[0].K;
+      one.j[0].item0 = 0;
+      one.j[0].slot0 = 0;
+      int64_t grid = one.j[0].pre * one.j[0].nchunks;
+      g_launches++;
+      if (vec2 && vv)
+        mttv_kernel<true, true><<<(unsigned)grid, MT_THREADS, 0, st>>>(one, R, out, q > 0 ? 1 : beta, nullptr);
+      else if (vec2)
+        mttv_kernel<true, false><<<(unsigned)grid, MT_THREADS, 0, st>>>(one, R, out, q > 0 ? 1 : beta, nullptr);
+      else
+        mttv_kernel<false, false><<<(unsigned)grid, MT_THREADS, 0, st>>>(one, R, out, q > 0 ? 1 : beta, nullptr);
+    }
+    return cudaGetLastError();
+  }
+  if (items > 0x7fffffff) return cudaErrorInvalidConfiguration;
+  double* w = direct ? nullptr : ws;
   g_launches++;
-#define CPD_MTTV(V2, VV_)                                                                              \
-  mttv_kernel<V2, VV_><<<(unsigned)grid, MT_THREADS, 0, st>>>(X, pre, K, C, R, v, out, beta, nchunks, (int)ks, \
-                                                              rps, ws)
   if (vec2 && vv)
-    CPD_MTTV(true, true);
+    mttv_kernel<true, true><<<(unsigned)items, MT_THREADS, 0, st>>>(jobs, R, out, beta, w);
   else if (vec2)
-    CPD_MTTV(true, false);
+    mttv_kernel<true, false><<<(unsigned)items, MT_THREADS, 0, st>>>(jobs, R, out, beta, w);
   else
-    CPD_MTTV(false, false);
-#undef CPD_MTTV
-  if (ks > 1) {
+    mttv_kernel<false, false><<<(unsigned)items, MT_THREADS, 0, st>>>(jobs, R, out, beta, w);
+  if (!direct) {
     g_launches++;
-    int64_t n = pre * C;
-    int64_t blocks = (n + 255) / 256;
+    int64_t blocks = (jobs.E + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
-    mttv_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(ws, (int)ks, n, out, beta);
+    mttv_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(ws, (int)slots, jobs.E, base, out, beta);
   }
   return cudaGetLastError();
+}
+
+cudaError_t launch_mttv(const double* X, int64_t pre, int64_t K, int64_t post, int R,
+                        const double* v, double* out, int beta, double* ws, int64_t ws_elems, cudaStream_t st) {
+  if (pre <= 0 || post * R <= 0) return cudaSuccess;
+  MttvSpec sp{X, v, pre, K, post};
+  return launch_mttv_multi(&sp, 1, R, nullptr, out, beta, ws, ws_elems, st);
 }
 
 cudaError_t launch_noise(double* T, int64_t Q, int64_t w, int64_t sN, int64_t lo, int kind,

@@ -39,7 +39,7 @@ class CPDecomposition:
         o.stream = _lib._stream_ptr(stream)
         o.pp_eps = float(pp_eps)
         o.reuse_root_in_pp_init = int(bool(reuse_root_in_pp_init))
-        o.profile_phases = int(bool(profile_phases))
+        o.profile_phases = int(profile_phases)
         o.local_group = local_group.value if local_group is not None else None
         A0 = [np.ascontiguousarray(a, dtype=np.float64) for a in A0]
         shp = (C.c_int64 * self.N)(*self.shape)
@@ -104,6 +104,9 @@ class CPDecomposition:
         return dict(zip(["ttm_flops", "ttm_launches", "stream_bytes", "stream_launches", "roots",
                          "kernel_launches"],
                         out.tolist()))
+
+    def set_profile_level(self, level):
+        check(self._lib.cpd_set_profile_level(self._ctx, int(level)), self._ctx)
 
     def reset_counters(self):
         check(self._lib.cpd_reset_counters(self._ctx), self._ctx)
