@@ -23,10 +23,13 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <unordered_map>
 #include <string>
 #include <utility>
 #include <vector>
@@ -77,6 +80,7 @@ struct cpd_ctx {
   cpd_opts opts{};
   // factors: mode N-1 holds only the local slab rows
   std::vector<double*> A, Aold, dA, Mlast, Ap, Mp, Mt;
+  std::vector<double*> Mlast_src;  // non-null: the last M of mode n lives there (PP: Mt[n])
   double* S_all = nullptr;   // N x R x R
   double* dS_all = nullptr;  // N x R x R
   double* Lp[2] = {nullptr, nullptr};  // packed Cholesky factors (double-buffered)
@@ -113,6 +117,8 @@ struct cpd_ctx {
   double phase_ms[5] = {0};
   double counters[5] = {0};
   std::vector<PhaseRec> pending;
+  std::multimap<size_t, void*> node_cache;         // free device blocks by exact size
+  std::unordered_map<void*, size_t> node_bytes;    // size of every block from dalloc
   std::vector<cudaEvent_t> free_events;
 };
 
@@ -214,14 +220,45 @@ void drain_timers(cpd_ctx* c) {  // call after a stream sync
 }
 
 // ---------------- memory ----------------
+// Exact-size caching allocator for tree nodes / PP operators.  Node sizes repeat every
+// cycle (a handful of distinct shapes), so after the first cycle every allocation is a
+// cache hit; splitting a pool block for a small node could otherwise force the next
+// root-sized allocation to map new memory (measured: tens of ms for 6.4 GB).  All users
+// of these buffers run on ctx->st, so stream order makes immediate reuse safe.
+void release_cache(cpd_ctx* c) {
+  for (auto& kv : c->node_cache) cudaFreeAsync(kv.second, c->st);
+  c->node_cache.clear();
+}
+
 cpd_status dalloc(cpd_ctx* ctx, double** p, int64_t elems) {
   *p = nullptr;
   if (elems <= 0) elems = 1;
-  CU(cudaMallocAsync((void**)p, sizeof(double) * (size_t)elems, ctx->st));
+  const size_t bytes = sizeof(double) * (size_t)elems;
+  auto it = ctx->node_cache.find(bytes);
+  if (it != ctx->node_cache.end()) {
+    *p = (double*)it->second;
+    ctx->node_cache.erase(it);
+    return CPD_OK;  // node_bytes[*p] already recorded
+  }
+  static const bool dbg = getenv("CPD_DEBUG_ALLOC") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  cudaError_t e = cudaMallocAsync((void**)p, bytes, ctx->st);
+  if (e == cudaErrorMemoryAllocation) {  // give the cached blocks back and retry once
+    cudaGetLastError();
+    release_cache(ctx);
+    cudaStreamSynchronize(ctx->st);
+    e = cudaMallocAsync((void**)p, bytes, ctx->st);
+  }
+  CU(e);
+  ctx->node_bytes[(void*)*p] = bytes;
+  if (dbg) {
+    double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (ms > 0.5) fprintf(stderr, "[cpd] cudaMallocAsync %.3f GB took %.2f ms\n", 1e-9 * bytes, ms);
+  }
   return CPD_OK;
 }
 void dfree(cpd_ctx* c, double*& p) {
-  if (p) cudaFreeAsync(p, c->st);
+  if (p) c->node_cache.emplace(c->node_bytes[(void*)p], (void*)p);
   p = nullptr;
 }
 
@@ -395,7 +432,9 @@ cpd_status prefetch_solve(cpd_ctx* ctx, int m, bool pp) {
   const int b = ctx->pf_buf ^ 1;
   CU(cudaEventRecord(ctx->ev_s, ctx->st));
   CU(cudaStreamWaitEvent(ctx->st2, ctx->ev_s, 0));
-  CU(cpd::launch_gamma_chol(ctx->S_all, ctx->N, m, ctx->R, ctx->Lp[b], ctx->pf_status + b, ctx->st2));
+  // status written straight to status[m]: a prefetch for the next sweep may overwrite it
+  // while finish_sweep reads it -- either value is a valid SPD verdict for Γ^(m)
+  CU(cpd::launch_gamma_chol(ctx->S_all, ctx->N, m, ctx->R, ctx->Lp[b], ctx->status + m, ctx->st2));
   if (pp) CU(cpd::launch_pp_w(ctx->S_all, ctx->dS_all, ctx->N, m, ctx->R, ctx->Wb[b], ctx->st2));
   CU(cudaEventRecord(ctx->ev_pf, ctx->st2));
   ctx->pf_buf = b;
@@ -411,8 +450,7 @@ cpd_status acquire_solve(cpd_ctx* ctx, int n, bool pp, int* buf) {
   CU(cudaStreamWaitEvent(ctx->st, ctx->ev_pf, 0));
   *buf = ctx->pf_buf;
   ctx->pf_mode = -1;
-  CU(cudaMemcpyAsync(ctx->status + n, ctx->pf_status + ctx->pf_buf, sizeof(int), cudaMemcpyDeviceToDevice,
-                     ctx->st));
+
   return CPD_OK;
 }
 
@@ -440,8 +478,13 @@ cpd_status update_mode(cpd_ctx* ctx, int n, double* Mloc, bool pp) {
   }
   {
     PhaseScope ps(ctx, PH_OTHER);
-    CU(cudaMemcpyAsync(ctx->Mlast[n] + off * R, Mown, sizeof(double) * ro * R, cudaMemcpyDeviceToDevice,
-                       ctx->st));
+    if (pp) {
+      ctx->Mlast_src[n] = Mloc;  // persistent M~ buffer: no copy, read on demand
+    } else {
+      ctx->Mlast_src[n] = nullptr;
+      CU(cudaMemcpyAsync(ctx->Mlast[n] + off * R, Mown, sizeof(double) * ro * R, cudaMemcpyDeviceToDevice,
+                         ctx->st));
+    }
     if (!pp)
       CU(cudaMemcpyAsync(ctx->Aold[n], ctx->A[n], sizeof(double) * rows_full * R,
                          cudaMemcpyDeviceToDevice, ctx->st));
@@ -510,6 +553,13 @@ void free_pp(cpd_ctx* c) {
   for (auto& kv : c->ops) dfree(c, kv.second);
   c->ops.clear();
   for (auto& p : c->Mp) dfree(c, p);
+  for (int n = 0; n < (int)c->Mlast_src.size(); n++)
+    if (c->Mlast_src[n]) {  // keep the last M~ readable after the PP buffers go away
+      const int64_t ro = rows_own(c, n), off = own_off(c, n);
+      cudaMemcpyAsync(c->Mlast[n] + off * c->R, c->Mlast_src[n] + off * c->R, sizeof(double) * ro * c->R,
+                      cudaMemcpyDeviceToDevice, c->st);
+      c->Mlast_src[n] = nullptr;
+    }
   for (auto& p : c->Mt) dfree(c, p);
   c->pp_valid = false;
 }
@@ -681,6 +731,7 @@ cpd_status cpd_destroy(cpd_ctx* c) {
   dfree(c, c->scal);
   dfree(c, c->partial);
   dfree(c, c->gather_tmp);
+  release_cache(c);
   if (c->status) cudaFreeAsync(c->status, c->st);
   cudaStreamSynchronize(c->st);
   for (auto& r : c->pending) {
@@ -801,6 +852,7 @@ cpd_status cp_als_init(cpd_ctx** out, int N, const int64_t* shape, int R, const 
   ctx->Ap.assign(N, nullptr);
   ctx->Mp.assign(N, nullptr);
   ctx->Mt.assign(N, nullptr);
+  ctx->Mlast_src.assign(N, nullptr);
   for (int n = 0; n < N; n++) {
     int64_t e = ext(ctx, n) * R;
     ITRY(dalloc(ctx, &ctx->A[n], e));
@@ -1057,6 +1109,11 @@ cpd_status cpd_get_factor(cpd_ctx* ctx, int n0, double* host_out) {
 cpd_status cpd_get_last_mttkrp(cpd_ctx* ctx, int n0, double* host_out) {
   TRY(check_ctx(ctx));
   if (n0 < 0 || n0 >= ctx->N || !host_out) return fail(ctx, CPD_ERR_INVALID_ARG, "bad mode");
+  if (ctx->Mlast_src[n0]) {
+    const int64_t ro = rows_own(ctx, n0), off = own_off(ctx, n0);
+    CU(cudaMemcpyAsync(ctx->Mlast[n0] + off * ctx->R, ctx->Mlast_src[n0] + off * ctx->R,
+                       sizeof(double) * ro * ctx->R, cudaMemcpyDeviceToDevice, ctx->st));
+  }
   if (n0 < ctx->N - 1 && ctx->world > 1) {
     int64_t ro = rows_own(ctx, n0);
     CM(cpd::comm_all_gather(ctx->cm, ctx->Mlast[n0] + own_off(ctx, n0) * ctx->R, ctx->Mlast[n0], ro * ctx->R,
