@@ -194,6 +194,9 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+TTM_IMPL = {"dmma": 0, "int8": 1}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -205,6 +208,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--oracle-slab", type=int, default=16)
+    ap.add_argument("--ttm-impl", default="dmma", choices=["dmma", "int8"],
+                    help="first-level TTM engine: FP64 DMMA or FP64-via-int8-digits on tcgen05")
     args = ap.parse_args()
     world, rank, local = dist_setup(args)
     if args.impl == "reference":
@@ -235,7 +240,8 @@ def main():
     torch.cuda.synchronize()
     A0 = synth.init_factors(cfg)
     m = cpd.cp_als_init(T, cfg.shape, cfg.R, A0, device=local, rank=rank, world=world, nccl_id=nccl_id,
-                        stream=stream, pp_eps=0.2 if args.config == 4 else 0.1, profile_phases=1)
+                        stream=stream, pp_eps=0.2 if args.config == 4 else 0.1, profile_phases=1,
+                        ttm_impl=TTM_IMPL[args.ttm_impl])
     # untimed: converge until the PP entry condition holds (Alg. 2 line 5), so the forced
     # PP sweeps of each step run in their regime of validity
     pre = 0
@@ -330,6 +336,26 @@ def main():
                "sample": f"oracle als_sweep on a {'x'.join([str(cfg.s)] * (N - 1))}x{args.oracle_slab} slab "
                          f"(best of 2), x{cfg.s // args.oracle_slab} slabs of the 1-D partition (linear extrapolation)"}
 
+    if args.ttm_impl == "dmma":
+        ttm_roof = {"kernel": "ttm_dmma (first-level TTM, DMMA.8x8x4)", "bound": "tensor", "achieved": ttm_tf,
+                    "peak": fp64, "peak_source": fp64_src, "unit": "TFLOP/s",
+                    "frac": (ttm_tf / fp64) if ttm_tf else None,
+                    "traffic": ncu_traffic("ttm_dmma"), "flops_per_launch": ttm_launch_flops,
+                    "avg_launch_ms": ttm_ms, "launches": int(ctr["ttm_launches"])}
+    else:
+        # int8-digit TTM: one pass over T per launch (R <= 64), so the bound is HBM; algorithmic
+        # bytes = T slab + output + factor, per launch (equidimensional: K = s)
+        t_el = ttm_launch_flops / (2 * cfg.R)
+        k = cfg.s
+        ttm_bytes = 8.0 * (t_el + t_el / k * cfg.R + k * cfg.R)
+        ttm_gbs = ttm_bytes / (ttm_ms * 1e-3) / 1e9 if ttm_ms > 0 else None
+        ttm_roof = {"kernel": "ttm_i8 (first-level TTM, FP64 operands as int8 digits, tcgen05 kind::i8)",
+                    "bound": "hbm", "achieved": ttm_gbs, "peak": peaks.get("hbm_gbs"),
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)", "unit": "GB/s",
+                    "frac": (ttm_gbs / peaks["hbm_gbs"]) if ttm_gbs and peaks.get("hbm_gbs") else None,
+                    "traffic": ncu_traffic("ttm_i8"), "bytes_per_launch": ttm_bytes,
+                    "fp64_equiv_tflops": ttm_tf, "fp64_equiv_frac_of_dmma_peak": (ttm_tf / fp64) if ttm_tf else None,
+                    "avg_launch_ms": ttm_ms, "launches": int(ctr["ttm_launches"])}
     if rank == 0:
         line = {
             "metric": METRIC, "value": msdt_ms, "unit": "ms/sweep (MSDT)", "n_gpus": world, "steps": args.steps,
@@ -340,15 +366,11 @@ def main():
                        else "i.i.d. U(0,1)", "parallelism": f"1-D split of mode N over {world} GPU(s)",
                        "step": f"{N - 1} msdt_sweep + pp_init + {N - 1} pp_approx_sweep + 1 dt_sweep",
                        "l2": "inputs larger than L2 (no flush)", "presweeps": pre, "pp_condition_held": pp_ok,
-                       "fitness_before_steps": f},
+                       "fitness_before_steps": f, "ttm_impl": args.ttm_impl},
             "sweeps_ms": {"msdt": msdt_ms, "pp_approx": ppapprox_ms, "pp_init": ppinit_ms, "dt": dt_ms,
                           "dt_over_msdt": dt_ms / msdt_ms, "dt_over_pp_approx": dt_ms / ppapprox_ms},
             "phase_ms_per_step": {k: v / 2 for k, v in ph_all.items()},
-            "roofline": {"kernel": "ttm_dmma (first-level TTM, DMMA.8x8x4)", "bound": "tensor", "achieved": ttm_tf,
-                         "peak": fp64, "peak_source": fp64_src, "unit": "TFLOP/s",
-                         "frac": (ttm_tf / fp64) if ttm_tf else None,
-                         "traffic": ncu_traffic("ttm_dmma"), "flops_per_launch": ttm_launch_flops,
-                         "avg_launch_ms": ttm_ms, "launches": int(ctr["ttm_launches"])},
+            "roofline": ttm_roof,
             "roofline_stream": {"kernel": "mttv (mTTV levels + PP U-stream)", "bound": "hbm", "achieved": st_gbs,
                                 "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
                                 "frac": (st_gbs / peaks["hbm_gbs"]) if st_gbs and peaks.get("hbm_gbs") else None,
@@ -374,7 +396,8 @@ def run_e2e(args, cpd, torch, cfg, T, m, rank, world, local, nccl_id, stream):
     T_dev = torch.empty_like(T)
     T_dev.copy_(T)
     m2 = cpd.cp_als_init(T_dev, cfg.shape, cfg.R, A_host, device=local, rank=rank, world=world,
-                         nccl_id=nccl_id if world == 1 else _new_id(cpd, dist, rank), stream=stream)
+                         nccl_id=nccl_id if world == 1 else _new_id(cpd, dist, rank), stream=stream,
+                         ttm_impl=TTM_IMPL[args.ttm_impl])
     outs = [np.empty((cfg.s, cfg.R)) for _ in range(N)]
     pinned_A = [torch.from_numpy(a).pin_memory().numpy() for a in A_host]
     ts = []

@@ -72,7 +72,14 @@ typedef struct {
   void* local_group;          /* NULL: NCCL (one process per GPU).  Else a cpd_local_group of `world`
                                  ranks in ONE process on ONE device, each rank's calls made from its own
                                  host thread (verification of the 1-D partition on a single GPU) */
+  int ttm_impl;               /* first-level TTM engine: CPD_TTM_DMMA (0, default) = FP64 tensor cores
+                                 (mma.sync .f64); CPD_TTM_INT8 (1) = FP64 operands sliced into int8
+                                 digits on the tcgen05 INT8 tensor cores (cpd_ttm_i8; modes with
+                                 s_j > 16384 use DMMA) */
 } cpd_opts;
+
+#define CPD_TTM_DMMA 0
+#define CPD_TTM_INT8 1
 
 typedef struct cpd_local_group cpd_local_group;
 /* In-process group for `world` (1..8) ranks sharing one device (see cpd_opts.local_group):
@@ -184,6 +191,15 @@ cpd_status cpd_gen_tensor(double* T_dev, int N, const int64_t* shape, int64_t lo
  * [pre, K, post]; out is [pre*post, R] row-major.  All device pointers; synchronous. */
 cpd_status cpd_ttm(const double* T_dev, int64_t pre, int64_t K, int64_t post,
                    const double* A_dev, int R, double* out_dev, void* stream);
+
+/* The same first-level TTM on the INT8 tensor cores (tcgen05.mma kind::i8): both FP64 operands
+ * are converted to 54-bit fixed point (one exponent for T = ceil(log2 max|T|), one per column of
+ * A) and split into 7 signed 8-bit digits; the 28 most significant digit-pair products are
+ * exact int32 tensor-core sums, recombined in FP64 (DESIGN.md §6 K2i).  Norm-wise error of
+ * the order of FP64 rounding relative to max|T|·|A|.  K <= 16384, 1 <= R <= 256; otherwise
+ * CPD_ERR_INVALID_ARG.  Synchronous; allocates its workspace on `stream`. */
+cpd_status cpd_ttm_i8(const double* T_dev, int64_t pre, int64_t K, int64_t post,
+                      const double* A_dev, int R, double* out_dev, void* stream);
 
 /* Batched TTV: out[p, c] = beta*out[p, c] + Σ_y X[p, y, c] v[y, c % R],
  * X viewed as [pre, K, C] with C = post*R; beta in {0, 1}.  Synchronous. */

@@ -19,7 +19,7 @@ EXPORTED_SYMBOLS = [
     "cpd_opts_default", "cpd_nccl_unique_id", "cp_als_init", "msdt_sweep", "dt_sweep", "pp_init",
     "pp_approx_sweep", "fitness", "cpd_pp_condition", "cpd_get_factor", "cpd_get_last_mttkrp",
     "cpd_set_factors", "cpd_get_phase_ms", "cpd_get_counters", "cpd_reset_counters",
-    "cpd_debug_get_pp_operator", "cpd_last_error", "cpd_destroy", "cpd_gen_tensor", "cpd_ttm",
+    "cpd_debug_get_pp_operator", "cpd_last_error", "cpd_destroy", "cpd_gen_tensor", "cpd_ttm", "cpd_ttm_i8",
     "cpd_mttv", "cpd_local_group_create", "cpd_local_group_destroy", "cpd_set_profile_level",
 ]
 
@@ -33,7 +33,8 @@ class CPDError(RuntimeError):
 class cpd_opts(C.Structure):
     _fields_ = [("struct_size", C.c_uint32), ("device", C.c_int), ("rank", C.c_int), ("world", C.c_int),
                 ("nccl_unique_id", C.c_void_p), ("stream", C.c_void_p), ("pp_eps", C.c_double),
-                ("reuse_root_in_pp_init", C.c_int), ("profile_phases", C.c_int), ("local_group", C.c_void_p)]
+                ("reuse_root_in_pp_init", C.c_int), ("profile_phases", C.c_int), ("local_group", C.c_void_p),
+                ("ttm_impl", C.c_int)]
 
 
 _lib = None
@@ -73,6 +74,7 @@ def load_library():
         "cpd_gen_tensor": (C.c_int, [_P, C.c_int, C.POINTER(C.c_int64), C.c_int64, C.c_int64, C.c_int,
                                      C.POINTER(_D), C.c_int, C.c_double, C.c_uint64, _P]),
         "cpd_ttm": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, _P, C.c_int, _P, _P]),
+        "cpd_ttm_i8": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, _P, C.c_int, _P, _P]),
         "cpd_mttv": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, C.c_int, _P, _P, C.c_int, _P]),
         "cpd_local_group_create": (C.c_int, [C.c_int, C.POINTER(_P)]),
         "cpd_local_group_destroy": (C.c_int, [_P]),
@@ -128,6 +130,11 @@ def cpd_gen_tensor(T, shape, lo, hi, kind, At, noise_std, seed, stream=None):
 def cpd_ttm(T, pre, K, post, A, R, out, stream=None):
     check(load_library().cpd_ttm(C.c_void_p(T.data_ptr()), pre, K, post, C.c_void_p(A.data_ptr()), R,
                                  C.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+
+
+def cpd_ttm_i8(T, pre, K, post, A, R, out, stream=None):
+    check(load_library().cpd_ttm_i8(C.c_void_p(T.data_ptr()), pre, K, post, C.c_void_p(A.data_ptr()), R,
+                                    C.c_void_p(out.data_ptr()), _stream_ptr(stream)))
 
 
 def cpd_mttv(X, pre, K, post, R, v, out, beta=0, stream=None):

@@ -120,6 +120,10 @@ struct cpd_ctx {
   std::multimap<size_t, void*> node_cache;         // free device blocks by exact size
   std::unordered_map<void*, size_t> node_bytes;    // size of every block from dalloc
   std::vector<cudaEvent_t> free_events;
+  // INT8 tensor-core TTM (opts.ttm_impl == CPD_TTM_INT8)
+  int* texp = nullptr;       // device: 2^texp > max|T| over all ranks' slabs
+  void* ws_i8 = nullptr;     // sliced factor digits + exponents
+  size_t ws_i8_bytes = 0;
 };
 
 // scalar slots
@@ -269,7 +273,12 @@ cpd_status ttm(cpd_ctx* ctx, int j, double* out) {
   for (int m = 0; m < j; m++) pre *= ext(ctx, m);
   for (int m = j + 1; m < ctx->N; m++) post *= ext(ctx, m);
   PhaseScope ps(ctx, PH_TTM);
-  CU(cpd::launch_ttm(ctx->T, pre, ext(ctx, j), post, ctx->A[j], ctx->R, out, 0, ctx->st));
+  if (ctx->opts.ttm_impl == CPD_TTM_INT8 && ext(ctx, j) <= cpd::kMaxKI8) {
+    CU(cpd::launch_ttm_i8(ctx->T, pre, ext(ctx, j), post, ctx->A[j], ctx->R, out, 0, ctx->texp, ctx->ws_i8,
+                          ctx->ws_i8_bytes, ctx->st));
+  } else {
+    CU(cpd::launch_ttm(ctx->T, pre, ext(ctx, j), post, ctx->A[j], ctx->R, out, 0, ctx->st));
+  }
   ctx->counters[0] += 2.0 * (double)pre * post * ext(ctx, j) * ctx->R;
   ctx->counters[1] += 1;
   ctx->counters[4] += 1;
@@ -680,6 +689,7 @@ cpd_status cpd_opts_default(cpd_opts* o) {
   o->reuse_root_in_pp_init = 1;
   o->profile_phases = 0;
   o->local_group = nullptr;
+  o->ttm_impl = CPD_TTM_DMMA;
   return CPD_OK;
 }
 
@@ -733,6 +743,8 @@ cpd_status cpd_destroy(cpd_ctx* c) {
   dfree(c, c->gather_tmp);
   release_cache(c);
   if (c->status) cudaFreeAsync(c->status, c->st);
+  if (c->texp) cudaFreeAsync(c->texp, c->st);
+  if (c->ws_i8) cudaFreeAsync(c->ws_i8, c->st);
   cudaStreamSynchronize(c->st);
   for (auto& r : c->pending) {
     cudaEventDestroy(r.a);
@@ -765,6 +777,7 @@ cpd_status cp_als_init(cpd_ctx** out, int N, const int64_t* shape, int R, const 
   }
   if (!(o.pp_eps > 0.0 && o.pp_eps < 1.0)) return fail(ctx, CPD_ERR_INVALID_ARG, "pp_eps must be in (0,1)");
   if (o.world < 1 || o.rank < 0 || o.rank >= o.world) return fail(ctx, CPD_ERR_INVALID_ARG, "bad rank/world");
+  if (o.ttm_impl != CPD_TTM_DMMA && o.ttm_impl != CPD_TTM_INT8) return fail(ctx, CPD_ERR_INVALID_ARG, "bad ttm_impl");
   if (o.world > 1 && !o.nccl_unique_id && !o.local_group)
     return fail(ctx, CPD_ERR_INVALID_ARG, "world > 1 needs nccl_unique_id or local_group");
   if (o.local_group && cpd::local_group_world((cpd::LocalGroup*)o.local_group) != o.world)
@@ -896,6 +909,16 @@ cpd_status cp_als_init(cpd_ctx** out, int N, const int64_t* shape, int R, const 
       fail(ctx, r_ == 5 ? CPD_ERR_NCCL : CPD_ERR_CUDA, m_);
       return bail(r_ == 5 ? CPD_ERR_NCCL : CPD_ERR_CUDA);
     }
+  }
+  if (o.ttm_impl == CPD_TTM_INT8) {
+    // one exponent for this rank's slab (T is read-only, so once per ctx); ranks may differ,
+    // which changes results only at the rounding level
+    ICU(cudaMallocAsync((void**)&ctx->texp, sizeof(int), ctx->st));
+    ICU(cpd::launch_absmax_exp(ctx->T, ctx->T_elems, ctx->partial, ctx->texp, ctx->st));
+    int64_t kmax = 1;
+    for (int n = 0; n < N; n++) kmax = std::max(kmax, ext(ctx, n));
+    ctx->ws_i8_bytes = cpd::ttm_i8_workspace_bytes(std::min(kmax, cpd::kMaxKI8), R);
+    ICU(cudaMallocAsync(&ctx->ws_i8, ctx->ws_i8_bytes, ctx->st));
   }
   cpd_status s = cpd_set_factors(ctx, A0_host);
   if (s != CPD_OK) {
@@ -1220,6 +1243,33 @@ cpd_status cpd_ttm(const double* T_dev, int64_t pre, int64_t K, int64_t post, co
                    double* out_dev, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cpd::launch_ttm(T_dev, pre, K, post, A_dev, R, out_dev, 0, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    g_init_error = cudaGetErrorString(e);
+    return CPD_ERR_CUDA;
+  }
+  return CPD_OK;
+}
+
+cpd_status cpd_ttm_i8(const double* T_dev, int64_t pre, int64_t K, int64_t post, const double* A_dev, int R,
+                      double* out_dev, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (K > cpd::kMaxKI8 || R < 1 || R > 256) {
+    g_init_error = "cpd_ttm_i8: K or R out of range";
+    return CPD_ERR_INVALID_ARG;
+  }
+  const size_t wsb = cpd::ttm_i8_workspace_bytes(K, R);
+  void* ws = nullptr;
+  double* part = nullptr;
+  int* ex = nullptr;
+  cudaError_t e = cudaMallocAsync(&ws, wsb, st);
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&part, sizeof(double) * cpd::kNormBlocks, st);
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&ex, sizeof(int), st);
+  if (e == cudaSuccess) e = cpd::launch_absmax_exp(T_dev, pre * K * post, part, ex, st);
+  if (e == cudaSuccess) e = cpd::launch_ttm_i8(T_dev, pre, K, post, A_dev, R, out_dev, 0, ex, ws, wsb, st);
+  if (ws) cudaFreeAsync(ws, st);
+  if (part) cudaFreeAsync(part, st);
+  if (ex) cudaFreeAsync(ex, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) {
     g_init_error = cudaGetErrorString(e);

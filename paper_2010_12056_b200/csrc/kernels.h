@@ -17,6 +17,17 @@ extern std::atomic<long long> g_launches;
 cudaError_t launch_ttm(const double* X, int64_t pre, int64_t K, int64_t post, const double* B,
                        int ncols, double* out, int beta, cudaStream_t st);
 
+// ---- the same first-level TTM on the INT8 tensor cores (tcgen05 kind::i8, exact integer
+// slicing of both FP64 operands; ttm_i8.cu).  Xexp: device int with 2^Xexp > max|X|
+// (launch_absmax_exp); ws: ttm_i8_workspace_bytes(K, ncols) bytes (sliced B + exponents).
+// K <= kMaxKI8 (int32 accumulators), ncols <= 256.
+constexpr int64_t kMaxKI8 = 16384;
+size_t ttm_i8_workspace_bytes(int64_t K, int ncols);
+cudaError_t launch_ttm_i8(const double* X, int64_t pre, int64_t K, int64_t post, const double* B, int ncols,
+                          double* out, int beta, const int* Xexp, void* ws, size_t ws_bytes, cudaStream_t st);
+// *e_out = e with 2^e > max|x_i| (0 if x == 0); partial: kNormBlocks doubles
+cudaError_t launch_absmax_exp(const double* x, int64_t n, double* partial, int* e_out, cudaStream_t st);
+
 // ---- batched TTV (mTTV) stream, P:320-322 ----------------------------------------------
 // out[p, c] = beta*out[p, c] + Σ_y X[(p*K + y)*C + c] * v[y*R + c % R],  C = post*R
 // ws (ws_elems doubles, may be null): K-split partials when the (p, chunk) grid is too small

@@ -22,7 +22,8 @@ class CPDecomposition:
     """
 
     def __init__(self, T, shape, R, A0, *, device=0, rank=0, world=1, nccl_id=None, stream=None,
-                 pp_eps=0.1, reuse_root_in_pp_init=True, profile_phases=False, local_group=None):
+                 pp_eps=0.1, reuse_root_in_pp_init=True, profile_phases=False, local_group=None,
+                 ttm_impl=0):
         lib = load_library()
         self.N = len(shape)
         self.shape = tuple(int(s) for s in shape)
@@ -41,6 +42,7 @@ class CPDecomposition:
         o.reuse_root_in_pp_init = int(bool(reuse_root_in_pp_init))
         o.profile_phases = int(profile_phases)
         o.local_group = local_group.value if local_group is not None else None
+        o.ttm_impl = int(ttm_impl)
         A0 = [np.ascontiguousarray(a, dtype=np.float64) for a in A0]
         shp = (C.c_int64 * self.N)(*self.shape)
         ctx = C.c_void_p()

@@ -107,14 +107,16 @@ def _model(cpd, cfg, T, A0=None, **kw):
     return cpd.cp_als_init(T, cfg.shape, cfg.R, synth.init_factors(cfg) if A0 is None else A0, **kw)
 
 
-def test_c1_full_trajectory(cpd):
+@pytest.mark.parametrize("ttm_impl", [0, 1])
+def test_c1_full_trajectory(cpd, ttm_impl):
     """C1: 10 msdt_sweep, then pp_init + 5 forced pp_approx_sweep (reading Q14); every
-    M^(n) and every fitness compared with the oracle (full-trajectory parity)."""
+    M^(n) and every fitness compared with the oracle (full-trajectory parity); with the
+    DMMA and with the INT8 tensor-core TTM."""
     cfg = synth.config(1)
     T = dev_tensor(cpd, cfg)
     To = O.make_tensor(cfg)
     nt2 = O.norm2(To)
-    m = _model(cpd, cfg, T)
+    m = _model(cpd, cfg, T, ttm_impl=ttm_impl)
     A = synth.init_factors(cfg)
     for sweep in range(10):
         f = m.msdt_sweep()
@@ -167,14 +169,15 @@ def test_c1_early_pp_exercises_second_order(cpd, early):
     m.close()
 
 
+@pytest.mark.parametrize("ttm_impl", [0, 1])
 @pytest.mark.parametrize("N,s,R", [(4, 12, 5), (5, 6, 3), (3, 40, 24), (6, 4, 2)])
-def test_msdt_and_dt_sweeps_order_N(cpd, N, s, R):
+def test_msdt_and_dt_sweeps_order_N(cpd, N, s, R, ttm_impl):
     cfg = synth.custom(N, s, R, noise_var=1e-4, seed=N * 10 + s)
     T = dev_tensor(cpd, cfg)
     To = O.make_tensor(cfg)
     nt2 = O.norm2(To)
     for kind in ("msdt", "dt"):
-        m = _model(cpd, cfg, T)
+        m = _model(cpd, cfg, T, ttm_impl=ttm_impl)
         A = synth.init_factors(cfg)
         for sweep in range(2 * (N - 1)):
             f = m.msdt_sweep() if kind == "msdt" else m.dt_sweep()
@@ -293,8 +296,9 @@ def test_set_factors_restarts_cycle(cpd):
 
 # ------------------------------- full-size sampled checks --------------------------------
 
+@pytest.mark.parametrize("ttm_impl", [0, 1])
 @pytest.mark.parametrize("c", [2, 3, 4, 5])
-def test_full_size_sampled_rows(cpd, c):
+def test_full_size_sampled_rows(cpd, c, ttm_impl):
     """BASELINE configs at full size: one msdt_sweep; sampled rows of every M^(n) against
     the oracle's slice-by-slice explicit-KRP rows with the GPU's input factors."""
     cfg = synth.config(c)
@@ -302,7 +306,7 @@ def test_full_size_sampled_rows(cpd, c):
     if free < 1.5 * 8 * cfg.numel + 16e9:
         pytest.skip("not enough device memory")
     T = dev_tensor(cpd, cfg)
-    m = _model(cpd, cfg, T)
+    m = _model(cpd, cfg, T, ttm_impl=ttm_impl)
     A0 = synth.init_factors(cfg)
     m.msdt_sweep()
     A1 = [m.get_factor(n) for n in range(cfg.N)]
@@ -316,3 +320,43 @@ def test_full_size_sampled_rows(cpd, c):
     m.close()
     del T
     torch.cuda.empty_cache()
+
+
+# ------------------------------- INT8 tensor-core TTM -----------------------------------
+
+@pytest.mark.parametrize("shape,R", [((37, 29, 41), 8), ((16, 130, 12), 64), ((33, 20, 17), 13), ((9, 10, 11, 12), 100),
+                                     ((11, 7, 13), 200), ((6, 5, 3), 1), ((200, 3, 130), 33), ((5, 300, 4), 17),
+                                     ((64, 64, 64), 64), ((40, 33, 257), 32)])
+def test_ttm_i8_all_positions(cpd, shape, R):
+    """cpd_ttm_i8 (int8 digit slicing on tcgen05) against the oracle's T x_j A at every
+    contraction position: ragged M tiles, K tails (odd K, K % 32 != 0), 1-4 N tiles."""
+    rng = np.random.default_rng(sum(shape) + R + 1)
+    Tn = rng.standard_normal(shape)
+    T = torch.from_numpy(Tn).cuda()
+    for j in range(len(shape)):
+        A = rng.standard_normal((shape[j], R))
+        pre = int(np.prod(shape[:j])) if j else 1
+        post = int(np.prod(shape[j + 1:])) if j < len(shape) - 1 else 1
+        out = torch.empty((pre * post, R), dtype=torch.float64, device="cuda")
+        cpd.cpd_ttm_i8(T, pre, shape[j], post, torch.from_numpy(A).cuda(), R, out)
+        ref = O.ttm(Tn, A, j).reshape(pre * post, R)
+        assert rel(out.cpu().numpy(), ref) <= 1e-13, (j, rel(out.cpu().numpy(), ref))
+
+
+def test_ttm_i8_wide_dynamic_range(cpd):
+    """Entries spread over 12 orders of magnitude and column scales over 6: the error is
+    relative to max|T| (one tensor exponent), so the norm-wise bound still holds."""
+    rng = np.random.default_rng(7)
+    shape = (48, 40, 36)
+    Tn = rng.standard_normal(shape) * 10.0 ** rng.uniform(-12, 0, shape)
+    T = torch.from_numpy(Tn).cuda()
+    for j in range(3):
+        A = rng.standard_normal((shape[j], 24)) * 10.0 ** rng.uniform(-3, 3, (1, 24))
+        pre = int(np.prod(shape[:j])) if j else 1
+        post = int(np.prod(shape[j + 1:])) if j < 2 else 1
+        out = torch.empty((pre * post, 24), dtype=torch.float64, device="cuda")
+        cpd.cpd_ttm_i8(T, pre, shape[j], post, torch.from_numpy(A).cuda(), 24, out)
+        ref = O.ttm(Tn, A, j).reshape(pre * post, 24)
+        got = out.cpu().numpy()
+        for c in range(24):  # per column (columns have different scales)
+            assert rel(got[:, c], ref[:, c]) <= 1e-12, (j, c, rel(got[:, c], ref[:, c]))
