@@ -197,9 +197,11 @@ cpd_status cpd_ttm(const double* T_dev, int64_t pre, int64_t K, int64_t post,
  * A) and split into 7 signed 8-bit digits; the 28 most significant digit-pair products are
  * exact int32 tensor-core sums, recombined in FP64 (DESIGN.md §6 K2i).  Norm-wise error of
  * the order of FP64 rounding relative to max|T|·|A|.  K <= 16384, 1 <= R <= 256; otherwise
- * CPD_ERR_INVALID_ARG.  Synchronous; allocates its workspace on `stream`. */
+ * CPD_ERR_INVALID_ARG.  use_digits != 0: T's digit planes are sliced first (7 bytes per
+ * element, as cp_als_init does once) and streamed by TMA where the layout allows it; 0: T is
+ * converted inside the TTM.  Synchronous; allocates its workspace on `stream`. */
 cpd_status cpd_ttm_i8(const double* T_dev, int64_t pre, int64_t K, int64_t post,
-                      const double* A_dev, int R, double* out_dev, void* stream);
+                      const double* A_dev, int R, double* out_dev, int use_digits, void* stream);
 
 /* Batched TTV: out[p, c] = beta*out[p, c] + Σ_y X[p, y, c] v[y, c % R],
  * X viewed as [pre, K, C] with C = post*R; beta in {0, 1}.  Synchronous. */

@@ -74,7 +74,7 @@ def load_library():
         "cpd_gen_tensor": (C.c_int, [_P, C.c_int, C.POINTER(C.c_int64), C.c_int64, C.c_int64, C.c_int,
                                      C.POINTER(_D), C.c_int, C.c_double, C.c_uint64, _P]),
         "cpd_ttm": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, _P, C.c_int, _P, _P]),
-        "cpd_ttm_i8": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, _P, C.c_int, _P, _P]),
+        "cpd_ttm_i8": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, _P, C.c_int, _P, C.c_int, _P]),
         "cpd_mttv": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, C.c_int, _P, _P, C.c_int, _P]),
         "cpd_local_group_create": (C.c_int, [C.c_int, C.POINTER(_P)]),
         "cpd_local_group_destroy": (C.c_int, [_P]),
@@ -132,9 +132,9 @@ def cpd_ttm(T, pre, K, post, A, R, out, stream=None):
                                  C.c_void_p(out.data_ptr()), _stream_ptr(stream)))
 
 
-def cpd_ttm_i8(T, pre, K, post, A, R, out, stream=None):
+def cpd_ttm_i8(T, pre, K, post, A, R, out, use_digits=True, stream=None):
     check(load_library().cpd_ttm_i8(C.c_void_p(T.data_ptr()), pre, K, post, C.c_void_p(A.data_ptr()), R,
-                                    C.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+                                    C.c_void_p(out.data_ptr()), int(bool(use_digits)), _stream_ptr(stream)))
 
 
 def cpd_mttv(X, pre, K, post, R, v, out, beta=0, stream=None):

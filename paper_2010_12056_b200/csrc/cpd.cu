@@ -123,6 +123,7 @@ struct cpd_ctx {
   // INT8 tensor-core TTM (opts.ttm_impl == CPD_TTM_INT8)
   int* texp = nullptr;       // device: 2^texp > max|T| over all ranks' slabs
   void* ws_i8 = nullptr;     // sliced factor digits + exponents
+  uint8_t* Td = nullptr;     // T's 7 int8 digit planes (computed once; null -> convert T per TTM)
   size_t ws_i8_bytes = 0;
 };
 
@@ -275,7 +276,7 @@ cpd_status ttm(cpd_ctx* ctx, int j, double* out) {
   PhaseScope ps(ctx, PH_TTM);
   if (ctx->opts.ttm_impl == CPD_TTM_INT8 && ext(ctx, j) <= cpd::kMaxKI8) {
     CU(cpd::launch_ttm_i8(ctx->T, pre, ext(ctx, j), post, ctx->A[j], ctx->R, out, 0, ctx->texp, ctx->ws_i8,
-                          ctx->ws_i8_bytes, ctx->st));
+                          ctx->ws_i8_bytes, ctx->st, ctx->Td));
   } else {
     CU(cpd::launch_ttm(ctx->T, pre, ext(ctx, j), post, ctx->A[j], ctx->R, out, 0, ctx->st));
   }
@@ -745,6 +746,7 @@ cpd_status cpd_destroy(cpd_ctx* c) {
   if (c->status) cudaFreeAsync(c->status, c->st);
   if (c->texp) cudaFreeAsync(c->texp, c->st);
   if (c->ws_i8) cudaFreeAsync(c->ws_i8, c->st);
+  if (c->Td) cudaFreeAsync(c->Td, c->st);
   cudaStreamSynchronize(c->st);
   for (auto& r : c->pending) {
     cudaEventDestroy(r.a);
@@ -919,6 +921,14 @@ cpd_status cp_als_init(cpd_ctx** out, int N, const int64_t* shape, int R, const 
     for (int n = 0; n < N; n++) kmax = std::max(kmax, ext(ctx, n));
     ctx->ws_i8_bytes = cpd::ttm_i8_workspace_bytes(std::min(kmax, cpd::kMaxKI8), R);
     ICU(cudaMallocAsync(&ctx->ws_i8, ctx->ws_i8_bytes, ctx->st));
+    // T's digit planes once (7 bytes per element): every first-level TTM then streams them
+    // instead of converting T; without the memory the TTM converts T on the fly
+    if (cudaMallocAsync((void**)&ctx->Td, (size_t)7 * cpd::digit_plane_stride(ctx->T_elems), ctx->st) == cudaSuccess) {
+      ICU(cpd::launch_slice_digits(ctx->T, ctx->T_elems, ctx->texp, ctx->Td, ctx->st));
+    } else {
+      cudaGetLastError();
+      ctx->Td = nullptr;
+    }
   }
   cpd_status s = cpd_set_factors(ctx, A0_host);
   if (s != CPD_OK) {
@@ -1252,7 +1262,7 @@ cpd_status cpd_ttm(const double* T_dev, int64_t pre, int64_t K, int64_t post, co
 }
 
 cpd_status cpd_ttm_i8(const double* T_dev, int64_t pre, int64_t K, int64_t post, const double* A_dev, int R,
-                      double* out_dev, void* stream) {
+                      double* out_dev, int use_digits, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (K > cpd::kMaxKI8 || R < 1 || R > 256) {
     g_init_error = "cpd_ttm_i8: K or R out of range";
@@ -1266,7 +1276,13 @@ cpd_status cpd_ttm_i8(const double* T_dev, int64_t pre, int64_t K, int64_t post,
   if (e == cudaSuccess) e = cudaMallocAsync((void**)&part, sizeof(double) * cpd::kNormBlocks, st);
   if (e == cudaSuccess) e = cudaMallocAsync((void**)&ex, sizeof(int), st);
   if (e == cudaSuccess) e = cpd::launch_absmax_exp(T_dev, pre * K * post, part, ex, st);
-  if (e == cudaSuccess) e = cpd::launch_ttm_i8(T_dev, pre, K, post, A_dev, R, out_dev, 0, ex, ws, wsb, st);
+  uint8_t* Td = nullptr;
+  if (e == cudaSuccess && use_digits) {
+    e = cudaMallocAsync((void**)&Td, (size_t)7 * cpd::digit_plane_stride(pre * K * post), st);
+    if (e == cudaSuccess) e = cpd::launch_slice_digits(T_dev, pre * K * post, ex, Td, st);
+  }
+  if (e == cudaSuccess) e = cpd::launch_ttm_i8(T_dev, pre, K, post, A_dev, R, out_dev, 0, ex, ws, wsb, st, Td);
+  if (Td) cudaFreeAsync(Td, st);
   if (ws) cudaFreeAsync(ws, st);
   if (part) cudaFreeAsync(part, st);
   if (ex) cudaFreeAsync(ex, st);

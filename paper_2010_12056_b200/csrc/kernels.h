@@ -23,8 +23,15 @@ cudaError_t launch_ttm(const double* X, int64_t pre, int64_t K, int64_t post, co
 // K <= kMaxKI8 (int32 accumulators), ncols <= 256.
 constexpr int64_t kMaxKI8 = 16384;
 size_t ttm_i8_workspace_bytes(int64_t K, int ncols);
+// Xd (may be null): X's 7 int8 digit planes (launch_slice_digits, 7 bytes per element, plane-major);
+// when given and ttm_i8_digits_ok(pre, K, post), the TTM streams them instead of converting X.
 cudaError_t launch_ttm_i8(const double* X, int64_t pre, int64_t K, int64_t post, const double* B, int ncols,
-                          double* out, int beta, const int* Xexp, void* ws, size_t ws_bytes, cudaStream_t st);
+                          double* out, int beta, const int* Xexp, void* ws, size_t ws_bytes, cudaStream_t st,
+                          const uint8_t* Xd = nullptr);
+bool ttm_i8_digits_ok(int64_t pre, int64_t K, int64_t post);
+// bytes between digit planes for n elements (the planes buffer holds 7 * digit_plane_stride(n) bytes)
+inline int64_t digit_plane_stride(int64_t n) { return (n + 63) / 64 * 64; }
+cudaError_t launch_slice_digits(const double* X, int64_t n, const int* Xexp, uint8_t* planes, cudaStream_t st);
 // *e_out = e with 2^e > max|x_i| (0 if x == 0); partial: kNormBlocks doubles
 cudaError_t launch_absmax_exp(const double* x, int64_t n, double* partial, int* e_out, cudaStream_t st);
 

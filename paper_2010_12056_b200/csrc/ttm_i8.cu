@@ -28,6 +28,12 @@
 //   warps 9-12 epilogue: tcgen05.ld of the 7 diagonals, exact int64 partial recombination,
 //              FP64 scale, 32-byte vector stores.
 #include <algorithm>
+#include <cstdlib>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstring>
 
 #include "kernels.h"
 
@@ -36,18 +42,30 @@ namespace {
 
 constexpr int kBM = 128;
 constexpr int kND = 7;
-constexpr int kDS = 3;                       // digit-plane stages
-constexpr int kFS = 3;                       // FP64 staging stages
-constexpr int kConv = 256;                   // converter threads
-constexpr int kThreads = kConv + 32 + 128;
 constexpr int kRpMax = 64;
 constexpr int kAPlane = kBM * 32;            // bytes of one digit plane per K32 step
 constexpr int kAStage = kND * kAPlane;       // 28672
 constexpr int kBStage = kND * kRpMax * 32;   // 14336 (max)
-constexpr int kDStage = kAStage + kBStage;
-constexpr int kFStage = kConv * 16 * 8;      // 32768: 16 doubles per converter thread
-constexpr int kSmemData = kDS * kDStage + kFS * kFStage;
-constexpr int kSmem = kSmemData + 128;
+constexpr int kDStage = kAStage + kBStage;   // 43008
+constexpr int kFStage = kBM * 32 * 8;        // 32768: one 128 x 32 FP64 tile
+// loader variants: register loads (generic shapes) or TMA tiles into an FP64 smem ring
+enum { L_KC = 0, L_MC = 2, L_KC_TMA = 3, L_MC_TMA = 4 };
+template <int L>
+struct Cfg {
+  static constexpr bool MC = (L == L_MC || L == L_MC_TMA);
+  static constexpr bool TMA = L >= L_KC_TMA;
+  static constexpr int NCW = TMA ? 16 : 8;           // converter warps
+  static constexpr int NDS = TMA ? 3 : 5;            // digit stages
+  static constexpr int NFS = TMA ? 3 : 0;            // FP64 stages
+  static constexpr int THREADS = NCW * 32 + 128;     // + 4 epilogue warps (the first also issues MMAs)
+  static constexpr int FOFF = NDS * kDStage;         // FP64 ring offset (1024-aligned)
+  static constexpr int DATA = FOFF + NFS * kFStage;
+  static constexpr int SMEM = DATA + 256;
+  static constexpr int MAXREG = TMA ? 96 : 168;      // 5 resp. 3 warps per SMSP register file
+};
+static_assert(Cfg<L_KC_TMA>::FOFF % 1024 == 0, "swizzled TMA boxes need 1024-byte alignment");
+static_assert(Cfg<L_KC_TMA>::SMEM <= 232448, "smem");
+static_assert(Cfg<L_KC>::SMEM <= 232448, "smem");
 constexpr uint64_t kBias = 0x0080808080808080ull;
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -59,9 +77,12 @@ __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
-__device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
@@ -71,16 +92,14 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void cp16(uint32_t dst, const void* src, bool valid) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0));
-}
-__device__ __forceinline__ void cp8(uint32_t dst, const void* src, bool valid) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 8 : 0));
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+// blocking form: the thread is suspended until the phase completes (or the time hint passes)
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@P1 bra DONE_%=;\nbra WAIT_%=;\nDONE_%=:\n}\n" ::"r"(bar),
+      "r"(parity), "r"(1000000)
+      : "memory");
 }
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   uint32_t r;
@@ -126,30 +145,45 @@ struct Geo {
   int nkc;                  // K32 steps
 };
 
-template <bool MC, bool VEC>
-__global__ void __launch_bounds__(kThreads, 1)
+// 128-byte swizzle of the TMA KC boxes: 16-byte chunk c of row r is stored at c ^ (r % 8)
+__device__ __forceinline__ int swz(int row, int c) { return row * 128 + ((c ^ (row & 7)) << 4); }
+
+template <int L, int RP>
+__global__ void __maxnreg__(Cfg<L>::MAXREG)
     ttm_i8_kernel(const double* __restrict__ X, Geo g, const uint8_t* __restrict__ Bimg,
-                  const int* __restrict__ Fexp, const int* __restrict__ Xexp, double* __restrict__ out, int beta) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  uint8_t* dring = smem;                               // kDS digit stages
-  uint8_t* fring = smem + kDS * kDStage;               // kFS FP64 stages
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemData);
-  const uint32_t full0 = su32(bars), empty0 = su32(bars + kDS);
-  const uint32_t tfull = su32(bars + 2 * kDS), tempty = su32(bars + 2 * kDS + 1);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * kDS + 2);
+                  const int* __restrict__ Fexp, const int* __restrict__ Xexp, double* __restrict__ out, int beta,
+                  int dbg, const __grid_constant__ CUtensorMap tmap) {
+  using C = Cfg<L>;
+  constexpr bool MC = C::MC;
+  constexpr int NDS = C::NDS, NFS = C::NFS;
+  constexpr int Rp = RP;  // padded columns per N tile (16, 32, 48 or 64): MMA shapes are compile-time
+  constexpr int Bbytes = kND * Rp * 32;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* dring = smem;                               // NDS digit stages
+  uint8_t* fring = smem + C::FOFF;                     // NFS FP64 stages (TMA variants)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::DATA);
+  const uint32_t full0 = su32(bars), empty0 = su32(bars + NDS);
+  const uint32_t tfull = su32(bars + 2 * NDS), tempty = su32(bars + 2 * NDS + 1);
+  const uint32_t ffull0 = su32(bars + 2 * NDS + 2), fempty0 = su32(bars + 2 * NDS + 2 + NFS);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * NDS + 2 + 2 * NFS);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int Bbytes = kND * g.Rp * 32;
+  constexpr int MMAW = C::NCW;  // TMEM allocator, MMA issuer (lane 0), epilogue quarter 0
 
   if (tid == 0) {
-    for (int s = 0; s < kDS; s++) {
-      mbar_init(full0 + 8 * s, kConv);
+    for (int s = 0; s < NDS; s++) {
+      mbar_init(full0 + 8 * s, C::NCW);   // one arrival per converter warp
       mbar_init(empty0 + 8 * s, 1);
+    }
+    for (int f = 0; f < NFS; f++) {
+      mbar_init(ffull0 + 8 * f, 1);
+      mbar_init(fempty0 + 8 * f, C::NCW);
     }
     mbar_init(tfull, 1);
     mbar_init(tempty, 128);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if constexpr (C::TMA) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
   }
-  if (warp == 8) {
+  if (warp == MMAW) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(tslot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -160,151 +194,244 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int64_t my_tiles = g.ntiles > blockIdx.x ? (g.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t iters = my_tiles * g.nkc;
 
-  if (warp < 8) {
+  if (warp < C::NCW) {
     // ===================== converters =====================
-    const int row = MC ? (tid & 127) : (tid >> 1);
-    const int h = MC ? (tid >> 7) : (tid & 1);
     const double scale = pow2(54 - *Xexp);
-    auto issue = [&](int64_t it) {
-      const int fs = (int)(it % kFS);
-      const uint32_t fb = su32(fring + fs * kFStage) + tid * 16;
-      if (it < iters) {
-        const int64_t tile = blockIdx.x + (it / g.nkc) * gridDim.x;
-        const int kc = (int)(it % g.nkc);
-        const int64_t mt = tile / g.ntn;
-        const int64_t i = mt * kBM + row;
-        const bool rok = i < g.Mrows;
-        const int64_t k0 = (int64_t)kc * 32 + 16 * h;
-        if constexpr (!MC) {
-          const double* src = X + (rok ? i : 0) * g.K;
-#pragma unroll
-          for (int q = 0; q < 8; q++) {
-            const int64_t k = k0 + 2 * q;
-            if constexpr (VEC) {
-              const bool ok = rok && k < g.K;  // K even: pairs never straddle the end
-              cp16(fb + q * (kConv * 16), src + (ok ? k : 0), ok);
-            } else {
-              cp8(fb + q * (kConv * 16), src + (rok && k < g.K ? k : 0), rok && k < g.K);
-              cp8(fb + q * (kConv * 16) + 8, src + (rok && k + 1 < g.K ? k + 1 : 0), rok && k + 1 < g.K);
-            }
-          }
-        } else {
-          const int64_t ii = rok ? i : 0;
-          const int64_t p = ii / g.post, m = ii - p * g.post;
-          const double* src = X + p * g.K * g.post + m;
-#pragma unroll
-          for (int q = 0; q < 16; q++) {
-            const int64_t k = k0 + q;
-            const bool ok = rok && k < g.K;
-            cp8(fb + (q >> 1) * (kConv * 16) + (q & 1) * 8, src + (ok ? k * g.post : 0), ok);
-          }
-        }
-      }
-      cp_commit();
-    };
-#pragma unroll 1
-    for (int q = 0; q < kFS - 1; q++) issue(q);
-#pragma unroll 1
-    for (int64_t it = 0; it < iters; it++) {
-      issue(it + kFS - 1);
-      cp_wait<kFS - 1>();
-      const int fs = (int)(it % kFS);
-      const double2* fp = reinterpret_cast<const double2*>(fring + fs * kFStage) + tid;
-      uint32_t lo[16], hi[16];
-#pragma unroll
-      for (int q = 0; q < 8; q++) {
-        const double2 v = fp[q * kConv];
-        const long long a0 = __double2ll_rn(v.x * scale) + (long long)kBias;
-        const long long a1 = __double2ll_rn(v.y * scale) + (long long)kBias;
-        lo[2 * q] = (uint32_t)a0;
-        hi[2 * q] = (uint32_t)((unsigned long long)a0 >> 32);
-        lo[2 * q + 1] = (uint32_t)a1;
-        hi[2 * q + 1] = (uint32_t)((unsigned long long)a1 >> 32);
-      }
-      const int s = (int)(it % kDS);
-      const uint32_t round = (uint32_t)(it / kDS);
-      mbar_wait(empty0 + 8 * s, (round & 1) ^ 1);
+    int64_t tile = blockIdx.x;
+    int kc = 0, s = 0;
+    uint32_t dpar = 1;  // parity of the digit-stage round we wait for (first round passes)
+    // x: this thread's NV consecutive-k values of one row -> digits, stores, arrive
+    auto emit = [&](const double* x, int NV, int row, int kb0) {
+      if (dbg & 16) mbar_wait_sleep(empty0 + 8 * s, dpar); else mbar_wait(empty0 + 8 * s, dpar);
       uint8_t* st = dring + s * kDStage;
-      // plane a, this thread's 16 k-bytes of row `row`, K half h
-      const int off = (row >> 3) * 256 + h * 128 + (row & 7) * 16;
-      uint32_t pl[8][4];
-#pragma unroll
-      for (int w = 0; w < 4; w++) {
-        uint32_t o[4];
-        transpose4(lo[4 * w], lo[4 * w + 1], lo[4 * w + 2], lo[4 * w + 3], o);
-#pragma unroll
-        for (int b = 0; b < 4; b++) pl[b][w] = o[b] ^ 0x80808080u;
-        transpose4(hi[4 * w], hi[4 * w + 1], hi[4 * w + 2], hi[4 * w + 3], o);
-#pragma unroll
-        for (int b = 0; b < 4; b++) pl[4 + b][w] = o[b] ^ 0x80808080u;
-      }
-#pragma unroll
-      for (int a = 0; a < kND; a++)
-        *reinterpret_cast<uint4*>(st + a * kAPlane + off) = make_uint4(pl[a][0], pl[a][1], pl[a][2], pl[a][3]);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      if (tid == 0) {
-        const int64_t tile = blockIdx.x + (it / g.nkc) * gridDim.x;
+      if (tid == 0 && !(dbg & 8)) {  // the factor digits of this K step: bulk copy, overlapping the conversion
         const int nt = (int)(tile % g.ntn);
-        const int kc = (int)(it % g.nkc);
         const uint8_t* src = Bimg + ((int64_t)nt * g.nkc + kc) * Bbytes;
-        mbar_arrive_tx(full0 + 8 * s, Bbytes);
+        mbar_expect_tx(full0 + 8 * s, Bbytes);  // tx only: thread 0 arrives after its own stores
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                 su32(st + kAStage)),
             "l"(src), "r"(Bbytes), "r"(full0 + 8 * s)
             : "memory");
-      } else {
-        mbar_arrive(full0 + 8 * s);
       }
-    }
-    cp_wait<0>();
-  } else if (warp == 8) {
-    // ===================== MMA issuer =====================
-    if (lane == 0) {
-      int64_t it = 0;
-      for (int64_t tt = 0; tt < my_tiles; tt++) {
-        mbar_wait(tempty, ((uint32_t)tt & 1) ^ 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        for (int kc = 0; kc < g.nkc; kc++, it++) {
-          const int s = (int)(it % kDS);
-          mbar_wait(full0 + 8 * s, (uint32_t)(it / kDS) & 1);
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t abase = su32(dring + s * kDStage), bbase = abase + kAStage;
-#pragma unroll 1
-          for (int a = kND - 1; a >= 0; a--) {
-            const uint32_t acc = (kc > 0 || a < kND - 1) ? 1u : 0u;
-            const uint64_t ad = sdesc(abase + a * kAPlane, 128, 256);
-            const int b0 = kND - 1 - a;  // first B plane: diagonal 0
-            const int n = (a + 1) * g.Rp;
-            const uint32_t bstart = bbase + b0 * g.Rp * 32;
-            const int n1 = n > 256 ? 256 : n;
-            mma_i8(tmem, ad, sdesc(bstart, 128, 256), idesc(n1), acc);
-            if (n > 256) mma_i8(tmem + 256, ad, sdesc(bstart + 256 * 32, 128, 256), idesc(n - 256), acc);
-          }
-          mma_commit(empty0 + 8 * s);
+      // plane a of row `row`, bytes kb0.. of the K32 step (UMMA K-major canonical, no swizzle)
+      const int off = (row >> 3) * 256 + (kb0 >> 4) * 128 + (row & 7) * 16 + (kb0 & 15);
+      // groups of 8 values: int64 fixed point + bias, byte transpose, 7 x 8-byte stores
+      for (int hf = 0; hf < NV / 8; hf++) {
+        if (dbg & 4) break;
+        uint32_t lo[8], hi[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+          const long long a = __double2ll_rn(x[8 * hf + q] * scale) + (long long)kBias;
+          lo[q] = (uint32_t)a;
+          hi[q] = (uint32_t)((unsigned long long)a >> 32);
         }
-        mma_commit(tfull);
+        uint32_t pl[7][2];
+#pragma unroll
+        for (int w = 0; w < 2; w++) {
+          uint32_t o[4];
+          transpose4(lo[4 * w], lo[4 * w + 1], lo[4 * w + 2], lo[4 * w + 3], o);
+#pragma unroll
+          for (int b = 0; b < 4; b++) pl[b][w] = o[b] ^ 0x80808080u;
+          transpose4(hi[4 * w], hi[4 * w + 1], hi[4 * w + 2], hi[4 * w + 3], o);
+#pragma unroll
+          for (int b = 0; b < 3; b++) pl[4 + b][w] = o[b] ^ 0x80808080u;
+        }
+#pragma unroll
+        for (int a = 0; a < kND; a++)
+          *reinterpret_cast<uint2*>(st + a * kAPlane + off + 8 * hf) = make_uint2(pl[a][0], pl[a][1]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // own stores -> async proxy
+      __syncwarp();
+      if (lane == 0) mbar_arrive(full0 + 8 * s);
+      if (++s == NDS) {
+        s = 0;
+        dpar ^= 1;
+      }
+      if (++kc == g.nkc) {
+        kc = 0;
+        tile += gridDim.x;
+      }
+    };
+
+    if constexpr (C::TMA) {
+      // ---- TMA loader (thread 0 issues K steps NFS-1 ahead) + 16 converter warps ----
+      const int row = tid & 127, part = tid >> 7;  // 8 consecutive k of one row per K step
+      int64_t l_tile = blockIdx.x, l_it = 0;
+      int l_kc = 0, l_f = 0;
+      uint32_t l_par = 1;
+      auto issue = [&]() {  // thread 0: next FP64 tile into the ring
+        if (l_it >= iters) return;
+        if (dbg & 16) mbar_wait_sleep(fempty0 + 8 * l_f, l_par); else mbar_wait(fempty0 + 8 * l_f, l_par);
+        const uint32_t dst = su32(fring + l_f * kFStage), bar = ffull0 + 8 * l_f;
+        if (!(dbg & 2)) {
+          mbar_arrive_expect_tx(bar, kFStage);
+          const int64_t i0 = (l_tile / g.ntn) * kBM;
+          const int k0 = l_kc * 32;
+          if constexpr (!MC) {
+            for (int hb = 0; hb < 2; hb++)
+              asm volatile(
+                  "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+                  "[%4];" ::"r"(dst + hb * (kFStage / 2)),
+                  "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(k0 + 16 * hb), "r"((int)i0), "r"(bar)
+                  : "memory");
+          } else {
+            const int64_t p = i0 / g.post, m0 = i0 - p * g.post;
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+                "[%5];" ::"r"(dst),
+                "l"(reinterpret_cast<uint64_t>(&tmap)), "r"((int)m0), "r"(k0), "r"((int)p), "r"(bar)
+                : "memory");
+          }
+        } else {
+          mbar_arrive(bar);
+        }
+        l_it++;
+        if (++l_f == NFS) {
+          l_f = 0;
+          l_par ^= 1;
+        }
+        if (++l_kc == g.nkc) {
+          l_kc = 0;
+          l_tile += gridDim.x;
+        }
+      };
+      if (tid == 0)
+        for (int q = 0; q < NFS - 1; q++) issue();
+      int f = 0;
+      uint32_t fpar = 0;
+#pragma unroll 1
+      for (int64_t it = 0; it < iters; it++) {
+        if (tid == 0) issue();
+        if (dbg & 16) mbar_wait_sleep(ffull0 + 8 * f, fpar); else mbar_wait(ffull0 + 8 * f, fpar);
+        const uint8_t* fb = fring + f * kFStage;
+        double x[8];
+        if constexpr (!MC) {
+          // box part>>1 holds k 16*(part>>1).., row-major 128-byte rows, 128B-swizzled
+          const uint8_t* box = fb + (part >> 1) * (kFStage / 2);
+#pragma unroll
+          for (int c = 0; c < 4; c++) {
+            const double2 v = *reinterpret_cast<const double2*>(box + swz(row, (part & 1) * 4 + c));
+            x[2 * c] = v.x;
+            x[2 * c + 1] = v.y;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; q++) x[q] = reinterpret_cast<const double*>(fb)[(8 * part + q) * kBM + row];
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(fempty0 + 8 * f);
+        if (++f == NFS) {
+          f = 0;
+          fpar ^= 1;
+        }
+        emit(x, 8, row, 8 * part);
+      }
+    } else {
+      // ---- register loader: 16 values per thread, two K steps ahead (three named buffers) ----
+      const int row = MC ? (tid & 127) : (tid >> 1);
+      const int h = MC ? (tid >> 7) : (tid & 1);
+      int64_t l_tile = blockIdx.x, l_it = 0;
+      int l_kc = 0;
+      const double* l_src = X;
+      bool l_rok = false;
+      auto new_tile = [&]() {  // base of this thread's row in tile l_tile
+        const int64_t mt = l_tile / g.ntn;
+        const int64_t i = mt * kBM + row;
+        l_rok = i < g.Mrows;
+        const int64_t ii = l_rok ? i : 0;
+        if constexpr (!MC) {
+          l_src = X + ii * g.K;
+        } else {
+          const int64_t p = ii / g.post, m = ii - p * g.post;
+          l_src = X + p * g.K * g.post + m;
+        }
+      };
+      if (iters > 0) new_tile();
+      auto load = [&](double (&x)[16]) {
+        if (l_it < iters) {
+          const int64_t k0 = (int64_t)l_kc * 32 + 16 * h;
+          if constexpr (!MC) {
+#pragma unroll
+            for (int q = 0; q < 16; q++) x[q] = (l_rok && k0 + q < g.K) ? __ldg(l_src + k0 + q) : 0.0;
+          } else {
+            const double* src = l_src + k0 * g.post;
+#pragma unroll
+            for (int q = 0; q < 16; q++) x[q] = (l_rok && k0 + q < g.K) ? __ldg(src + q * g.post) : 0.0;
+          }
+          l_it++;
+          if (++l_kc == g.nkc) {
+            l_kc = 0;
+            l_tile += gridDim.x;
+            if (l_it < iters) new_tile();
+          }
+        }
+      };
+      double xa[16], xb[16], xc[16];
+      load(xa);
+      load(xb);
+#pragma unroll 1
+      for (int64_t it = 0; it < iters; it += 3) {
+        load(xc);
+        emit(xa, 16, row, 16 * h);
+        if (it + 1 >= iters) break;
+        load(xa);
+        emit(xb, 16, row, 16 * h);
+        if (it + 2 >= iters) break;
+        load(xb);
+        emit(xc, 16, row, 16 * h);
       }
     }
-    __syncwarp();
   } else {
-    // ===================== epilogue =====================
+    // ===================== epilogue (4 warps; the first also issues the MMAs) =====================
     const int q = warp & 3;  // TMEM lane quarter of this warp
     const int r = q * 32 + lane;
     const int ex = *Xexp;
+    int s = 0;  // MMA issuer: digit stage and its parity
+    uint32_t fpar = 0;
     for (int64_t tt = 0; tt < my_tiles; tt++) {
       const int64_t tile = blockIdx.x + tt * gridDim.x;
       const int64_t mt = tile / g.ntn;
       const int nt = (int)(tile % g.ntn);
       const int64_t i = mt * kBM + r;
       const int n0 = nt * g.Rn;
-      mbar_wait(tfull, (uint32_t)tt & 1);
+      if (warp == MMAW) {
+        if (lane == 0) {
+          mbar_wait_sleep(tempty, ((uint32_t)tt & 1) ^ 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          for (int kc = 0; kc < g.nkc; kc++) {
+            mbar_wait(full0 + 8 * s, fpar);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t abase = su32(dring + s * kDStage);
+            const uint64_t ad0 = sdesc(abase, 128, 256), bd0 = sdesc(abase + kAStage, 128, 256);
+            if (!(dbg & 1)) {
+#pragma unroll
+              for (int a = kND - 1; a >= 0; a--) {
+                const uint32_t acc = (kc > 0 || a < kND - 1) ? 1u : 0u;
+                const int n = (a + 1) * Rp;                                  // diagonals 0..a
+                const uint64_t ad = ad0 + (uint64_t)((a * kAPlane) >> 4);
+                const uint64_t bd = bd0 + (uint64_t)(((kND - 1 - a) * Rp * 32) >> 4);  // B planes 6-a..6
+                mma_i8(tmem, ad, bd, idesc(n > 256 ? 256 : n), acc);
+                if (n > 256) mma_i8(tmem + 256, ad, bd + ((256 * 32) >> 4), idesc(n - 256), acc);
+              }
+            }
+            mma_commit(empty0 + 8 * s);
+            if (++s == NDS) {
+              s = 0;
+              fpar ^= 1;
+            }
+          }
+          mma_commit(tfull);
+        }
+        __syncwarp();
+      }
+      mbar_wait_sleep(tfull, (uint32_t)tt & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      for (int c0 = 0; c0 < g.Rp; c0 += 8) {
+      for (int c0 = 0; c0 < Rp; c0 += 8) {
         uint32_t D[kND][8];
 #pragma unroll
         for (int d = 0; d < kND; d++) {
-          const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + d * g.Rp + c0;
+          const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + d * Rp + c0;
           asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                        : "=r"(D[d][0]), "=r"(D[d][1]), "=r"(D[d][2]), "=r"(D[d][3]), "=r"(D[d][4]),
                          "=r"(D[d][5]), "=r"(D[d][6]), "=r"(D[d][7])
@@ -344,7 +471,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  if (warp == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  if (warp == MMAW) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 // ---- operand preparation ----
@@ -446,16 +573,343 @@ Geo make_geo(int64_t pre, int64_t K, int64_t post, int ncols) {
   return g;
 }
 
-template <bool MC, bool VEC>
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// TMA descriptor of T for the loader variant: KC = 2-D [Mrows][K] in 16 x 128 boxes with
+// the 128-byte swizzle; MC = 3-D [pre][K][post] in 128 x 32 x 1 boxes (post % 128 == 0)
+bool make_tmap(int L, const double* X, const Geo& g, CUtensorMap* tm) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  CUresult r;
+  if (L == L_KC_TMA) {
+    cuuint64_t dims[2] = {(cuuint64_t)g.K, (cuuint64_t)g.Mrows};
+    cuuint64_t strides[1] = {(cuuint64_t)g.K * 8};
+    cuuint32_t box[2] = {16, (cuuint32_t)kBM}, es[2] = {1, 1};
+    r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(X), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    cuuint64_t dims[3] = {(cuuint64_t)g.post, (cuuint64_t)g.K, (cuuint64_t)g.pre};
+    cuuint64_t strides[2] = {(cuuint64_t)g.post * 8, (cuuint64_t)g.K * g.post * 8};
+    cuuint32_t box[3] = {(cuuint32_t)kBM, 32, 1}, es[3] = {1, 1, 1};
+    r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(X), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  return r == CUDA_SUCCESS;
+}
+
+template <int L, int RP>
 cudaError_t run_i8(int grid, const double* X, const Geo& g, const uint8_t* Bimg, const int* F, const int* Xexp,
-                   double* out, int beta, cudaStream_t st) {
+                   double* out, int beta, const CUtensorMap& tm, cudaStream_t st) {
+  static const int dbg = getenv("CPD_I8_DBG") ? atoi(getenv("CPD_I8_DBG")) : 0;  // profiling switches
   static bool attr = false;  // per instantiation
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(ttm_i8_kernel<MC, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaError_t e = cudaFuncSetAttribute(ttm_i8_kernel<L, RP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg<L>::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  ttm_i8_kernel<MC, VEC><<<grid, kThreads, kSmem, st>>>(X, g, Bimg, F, Xexp, out, beta);
+  ttm_i8_kernel<L, RP><<<grid, Cfg<L>::THREADS, Cfg<L>::SMEM, st>>>(X, g, Bimg, F, Xexp, out, beta, dbg, tm);
+  return cudaGetLastError();
+}
+
+template <int RP>
+cudaError_t dispatch_i8(int L, int grid, const double* X, const Geo& g, const uint8_t* Bimg, const int* F,
+                        const int* Xexp, double* out, int beta, const CUtensorMap& tm, cudaStream_t st) {
+  switch (L) {
+    case L_KC: return run_i8<L_KC, RP>(grid, X, g, Bimg, F, Xexp, out, beta, tm, st);
+    case L_MC: return run_i8<L_MC, RP>(grid, X, g, Bimg, F, Xexp, out, beta, tm, st);
+    case L_KC_TMA: return run_i8<L_KC_TMA, RP>(grid, X, g, Bimg, F, Xexp, out, beta, tm, st);
+    case L_MC_TMA: return run_i8<L_MC_TMA, RP>(grid, X, g, Bimg, F, Xexp, out, beta, tm, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// ============================================================================================
+// Digit-plane variant: T's 7 int8 digit planes are computed ONCE (T is read-only for the
+// whole decomposition, like the paper's stored transposed copies of T) and the
+// TTM streams them with TMA straight into the UMMA operand layout -- no per-sweep conversion.
+// Planes are stored plane-major, each with T's row-major layout (7 bytes per element).
+//   KC (contract the last kept mode, K contiguous): 3-D map {K, Mrows, 7}, box {32, 128, 7},
+//      128 rows x 32 bytes per plane, 32-byte swizzle = UMMA K-major SWIZZLE_32B;
+//   MC (post % 128 == 0): 4-D map {post, K, pre, 7}, box {128, 32, 1, 7}: 32 k-rows x 128 m
+//      bytes per plane, 128-byte swizzle = UMMA MN-major SWIZZLE_128B.
+// Warps: 0 TMA producer, 1 TMEM allocator + MMA issuer, 2-9 epilogue (two per lane quarter).
+// ============================================================================================
+enum { D_KC = 0, D_MC = 1 };
+constexpr int kStagesD = 5;
+constexpr int kThreadsD = 32 * 10;
+constexpr int kSmemD = kStagesD * kDStage + 256;
+static_assert(kSmemD <= 232448, "smem");
+
+// UMMA descriptor with a swizzle layout type (2 = 128B, 6 = 32B), base offset 0
+__device__ __forceinline__ uint64_t sdesc_sw(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  return sdesc(addr, lbo, sbo) | ((uint64_t)layout << 61);
+}
+
+template <int L, int RP>
+__global__ void __launch_bounds__(kThreadsD, 1)
+    ttm_i8d_kernel(Geo g, const uint8_t* __restrict__ Bimg, const int* __restrict__ Fexp,
+                   const int* __restrict__ Xexp, double* __restrict__ out, int beta,
+                   const __grid_constant__ CUtensorMap tmap) {
+  constexpr int Rp = RP;
+  constexpr int Bbytes = kND * Rp * 32;
+  constexpr int NDS = kStagesD;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NDS * kDStage);
+  const uint32_t full0 = su32(bars), empty0 = su32(bars + NDS);
+  const uint32_t tfull = su32(bars + 2 * NDS), tempty = su32(bars + 2 * NDS + 1);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * NDS + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < NDS; s++) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 256);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+  const int64_t my_tiles = g.ntiles > blockIdx.x ? (g.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      int s = 0;
+      uint32_t par = 1;
+      for (int64_t tt = 0; tt < my_tiles; tt++) {
+        const int64_t tile = blockIdx.x + tt * gridDim.x;
+        const int64_t i0 = (tile / g.ntn) * kBM;
+        const int nt = (int)(tile % g.ntn);
+        int p = 0, m0 = 0;
+        if constexpr (L == D_MC) {
+          p = (int)(i0 / g.post);
+          m0 = (int)(i0 - (int64_t)p * g.post);
+        }
+        for (int kc = 0; kc < g.nkc; kc++) {
+          mbar_wait(empty0 + 8 * s, par);
+          const uint32_t st = su32(smem + s * kDStage), bar = full0 + 8 * s;
+          mbar_arrive_expect_tx(bar, kAStage + Bbytes);
+          if constexpr (L == D_KC) {
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+                "%4}], [%5];" ::"r"(st),
+                "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(kc * 32), "r"((int)i0), "r"(0), "r"(bar)
+                : "memory");
+          } else {
+            asm volatile(
+                "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+                "%4, %5}], [%6];" ::"r"(st),
+                "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(m0), "r"(kc * 32), "r"(p), "r"(0), "r"(bar)
+                : "memory");
+          }
+          const uint8_t* bsrc = Bimg + ((int64_t)nt * g.nkc + kc) * Bbytes;
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  st + kAStage),
+              "l"(bsrc), "r"(Bbytes), "r"(bar)
+              : "memory");
+          if (++s == NDS) {
+            s = 0;
+            par ^= 1;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
+      int s = 0;
+      uint32_t par = 0;
+      // A: KC K-major SW32 (8-row groups of 256 B); MC MN-major SW128 (8-k-row groups of 1 KB)
+      constexpr uint32_t A_LBO = L == D_KC ? 16 : 16, A_SBO = L == D_KC ? 256 : 1024;
+      constexpr uint32_t A_LAYOUT = L == D_KC ? 6 : 2;
+      constexpr uint32_t AMAJ = L == D_KC ? 0u : (1u << 15);
+      for (int64_t tt = 0; tt < my_tiles; tt++) {
+        mbar_wait_sleep(tempty, ((uint32_t)tt & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        for (int kc = 0; kc < g.nkc; kc++) {
+          mbar_wait(full0 + 8 * s, par);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t abase = su32(smem + s * kDStage);
+          const uint64_t ad0 = sdesc_sw(abase, A_LBO, A_SBO, A_LAYOUT), bd0 = sdesc(abase + kAStage, 128, 256);
+#pragma unroll
+          for (int a = kND - 1; a >= 0; a--) {
+            const uint32_t acc = (kc > 0 || a < kND - 1) ? 1u : 0u;
+            const int n = (a + 1) * Rp;  // diagonals 0..a
+            const uint64_t ad = ad0 + (uint64_t)((a * kAPlane) >> 4);
+            const uint64_t bd = bd0 + (uint64_t)(((kND - 1 - a) * Rp * 32) >> 4);  // B planes 6-a..6
+            mma_i8(tmem, ad, bd, idesc(n > 256 ? 256 : n) | AMAJ, acc);
+            if (n > 256) mma_i8(tmem + 256, ad, bd + ((256 * 32) >> 4), idesc(n - 256) | AMAJ, acc);
+          }
+          mma_commit(empty0 + 8 * s);
+          if (++s == NDS) {
+            s = 0;
+            par ^= 1;
+          }
+        }
+        mma_commit(tfull);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===================== epilogue: warps 2-9, lane quarter warp % 4, column half =====================
+    const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int r = q * 32 + lane;
+    const int ex = *Xexp;
+    constexpr int CH = Rp / 2;  // columns per half (8, 16, 24, 32)
+    for (int64_t tt = 0; tt < my_tiles; tt++) {
+      const int64_t tile = blockIdx.x + tt * gridDim.x;
+      const int64_t i = (tile / g.ntn) * kBM + r;
+      const int nt = (int)(tile % g.ntn);
+      const int n0 = nt * g.Rn;
+      mbar_wait_sleep(tfull, (uint32_t)tt & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll 1
+      for (int c0 = half * CH; c0 < (half + 1) * CH; c0 += 8) {
+        uint32_t D[kND][8];
+#pragma unroll
+        for (int d = 0; d < kND; d++) {
+          const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + d * Rp + c0;
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                       : "=r"(D[d][0]), "=r"(D[d][1]), "=r"(D[d][2]), "=r"(D[d][3]), "=r"(D[d][4]),
+                         "=r"(D[d][5]), "=r"(D[d][6]), "=r"(D[d][7])
+                       : "r"(ta));
+        }
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const int cmax = min(8, min(g.Rn - c0, g.ncols - n0 - c0));
+        if (i < g.Mrows && cmax > 0) {
+          double v[8];
+#pragma unroll
+          for (int j = 0; j < 8; j++) {
+            const long long l0 = (long long)(int)D[0][j] + ((long long)(int)D[1][j] << 8) +
+                                 ((long long)(int)D[2][j] << 16);
+            const long long l1 = (long long)(int)D[3][j] + ((long long)(int)D[4][j] << 8) +
+                                 ((long long)(int)D[5][j] << 16);
+            const double t = fma((double)(int)D[6][j], 281474976710656.0 /* 2^48 */, (double)l1 * 16777216.0);
+            v[j] = (t + (double)l0) * pow2(ex + Fexp[n0 + c0 + min(j, cmax - 1)] - 60);
+          }
+          double* orow = out + i * g.ncols + n0 + c0;
+          if (cmax == 8 && !beta && ((reinterpret_cast<uintptr_t>(orow) & 31) == 0)) {
+            asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(orow), "d"(v[0]), "d"(v[1]), "d"(v[2]),
+                         "d"(v[3]) : "memory");
+            asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(orow + 4), "d"(v[4]), "d"(v[5]), "d"(v[6]),
+                         "d"(v[7]) : "memory");
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; j++)
+              if (j < cmax) orow[j] = beta ? orow[j] + v[j] : v[j];
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(tempty);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// digit planes of X: plane a, element e = byte a of (rint(X[e] 2^(54-eX)) + bias) xor 0x80,
+// stored at planes[a * ps + e] (ps = digit_plane_stride(n), a multiple of 64)
+__global__ void slice_digits_kernel(const double* __restrict__ X, int64_t n, int64_t ps, const int* __restrict__ Xexp,
+                                    uint8_t* __restrict__ planes) {
+  const double scale = pow2(54 - *Xexp);
+  const int64_t n16 = n / 16;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n16; b += (int64_t)gridDim.x * blockDim.x) {
+    const double2* src = reinterpret_cast<const double2*>(X + 16 * b);
+    uint32_t w[7][4];
+#pragma unroll
+    for (int g4 = 0; g4 < 4; g4++) {
+      uint32_t lo[4], hi[4];
+#pragma unroll
+      for (int q = 0; q < 2; q++) {
+        const double2 v = __ldg(src + 2 * g4 + q);
+        const long long a0 = __double2ll_rn(v.x * scale) + (long long)kBias;
+        const long long a1 = __double2ll_rn(v.y * scale) + (long long)kBias;
+        lo[2 * q] = (uint32_t)a0;
+        hi[2 * q] = (uint32_t)((unsigned long long)a0 >> 32);
+        lo[2 * q + 1] = (uint32_t)a1;
+        hi[2 * q + 1] = (uint32_t)((unsigned long long)a1 >> 32);
+      }
+      uint32_t o[4];
+      transpose4(lo[0], lo[1], lo[2], lo[3], o);
+#pragma unroll
+      for (int a = 0; a < 4; a++) w[a][g4] = o[a] ^ 0x80808080u;
+      transpose4(hi[0], hi[1], hi[2], hi[3], o);
+#pragma unroll
+      for (int a = 0; a < 3; a++) w[4 + a][g4] = o[a] ^ 0x80808080u;
+    }
+#pragma unroll
+    for (int a = 0; a < kND; a++)
+      *reinterpret_cast<uint4*>(planes + a * ps + 16 * b) = make_uint4(w[a][0], w[a][1], w[a][2], w[a][3]);
+  }
+  if (blockIdx.x == 0) {
+    for (int64_t e = 16 * n16 + threadIdx.x; e < n; e += blockDim.x) {
+      const unsigned long long u = (unsigned long long)(__double2ll_rn(X[e] * scale) + (long long)kBias);
+#pragma unroll
+      for (int a = 0; a < kND; a++) planes[a * ps + e] = (uint8_t)(((u >> (8 * a)) & 0xFF) ^ 0x80);
+    }
+  }
+}
+
+bool make_tmap_digits(int L, const uint8_t* Xd, const Geo& g, CUtensorMap* tm) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  const cuuint64_t numel = (cuuint64_t)digit_plane_stride(g.Mrows * g.K);  // plane stride
+  CUresult r;
+  if (L == D_KC) {
+    cuuint64_t dims[3] = {(cuuint64_t)g.K, (cuuint64_t)g.Mrows, (cuuint64_t)kND};
+    cuuint64_t strides[2] = {(cuuint64_t)g.K, numel};
+    cuuint32_t box[3] = {32, (cuuint32_t)kBM, (cuuint32_t)kND}, es[3] = {1, 1, 1};
+    r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(Xd), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    cuuint64_t dims[4] = {(cuuint64_t)g.post, (cuuint64_t)g.K, (cuuint64_t)g.pre, (cuuint64_t)kND};
+    cuuint64_t strides[3] = {(cuuint64_t)g.post, (cuuint64_t)g.K * g.post, numel};
+    cuuint32_t box[4] = {(cuuint32_t)kBM, 32, 1, (cuuint32_t)kND}, es[4] = {1, 1, 1, 1};
+    r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(Xd), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  return r == CUDA_SUCCESS;
+}
+
+template <int L, int RP>
+cudaError_t run_i8d(int grid, const Geo& g, const uint8_t* Bimg, const int* F, const int* Xexp, double* out,
+                    int beta, const CUtensorMap& tm, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(ttm_i8d_kernel<L, RP>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemD);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  ttm_i8d_kernel<L, RP><<<grid, kThreadsD, kSmemD, st>>>(g, Bimg, F, Xexp, out, beta, tm);
   return cudaGetLastError();
 }
 
@@ -473,8 +927,20 @@ cudaError_t launch_absmax_exp(const double* x, int64_t n, double* partial, int* 
   return cudaGetLastError();
 }
 
+cudaError_t launch_slice_digits(const double* X, int64_t n, const int* Xexp, uint8_t* planes, cudaStream_t st) {
+  g_launches++;
+  if (((uintptr_t)X % 16) != 0) return cudaErrorInvalidValue;
+  slice_digits_kernel<<<148 * 8, 256, 0, st>>>(X, n, digit_plane_stride(n), Xexp, planes);
+  return cudaGetLastError();
+}
+
+bool ttm_i8_digits_ok(int64_t pre, int64_t K, int64_t post) {
+  return post > 1 ? (post % kBM) == 0 : (K % 16) == 0;
+}
+
 cudaError_t launch_ttm_i8(const double* X, int64_t pre, int64_t K, int64_t post, const double* B, int ncols,
-                          double* out, int beta, const int* Xexp, void* ws, size_t ws_bytes, cudaStream_t st) {
+                          double* out, int beta, const int* Xexp, void* ws, size_t ws_bytes, cudaStream_t st,
+                          const uint8_t* Xd) {
   if (pre <= 0 || post <= 0 || ncols <= 0) return cudaSuccess;
   if (K <= 0 || K > kMaxKI8 || ncols > 256) return cudaErrorInvalidValue;
   Geo g = make_geo(pre, K, post, ncols);
@@ -489,12 +955,45 @@ cudaError_t launch_ttm_i8(const double* X, int64_t pre, int64_t K, int64_t post,
     int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
     b_image_kernel<<<blocks, 256, 0, st>>>(B, K, g, F, Bimg);
   }
+  const int grid0 = (int)std::min<int64_t>(g.ntiles, sm_count());
+  static const bool no_digits = getenv("CPD_I8_NO_DIGITS") != nullptr;
+  if (Xd && !no_digits && ttm_i8_digits_ok(pre, K, post) && ((uintptr_t)Xd % 16) == 0) {
+    const int Ld = post > 1 ? D_MC : D_KC;
+    CUtensorMap tmd;
+    if (make_tmap_digits(Ld, Xd, g, &tmd)) {
+      switch (g.Rp) {
+#define CPD_I8D_CASE(RP_) \
+  case RP_:               \
+    return Ld == D_KC ? run_i8d<D_KC, RP_>(grid0, g, Bimg, F, Xexp, out, beta, tmd, st) \
+                      : run_i8d<D_MC, RP_>(grid0, g, Bimg, F, Xexp, out, beta, tmd, st);
+        CPD_I8D_CASE(16)
+        CPD_I8D_CASE(32)
+        CPD_I8D_CASE(48)
+        CPD_I8D_CASE(64)
+#undef CPD_I8D_CASE
+      }
+    }
+  }
+  // loader: TMA when the layout allows it (16-byte aligned strides; MC tiles must not straddle
+  // the prefix index, i.e. post % 128 == 0), else register loads
+  static const bool no_tma = getenv("CPD_I8_NO_TMA") != nullptr;
   const bool mc = post > 1;
-  const bool vec = !mc && (K % 2) == 0 && ((uintptr_t)X % 16) == 0;
+  const bool aligned = ((uintptr_t)X % 16) == 0;
+  int L = mc ? L_MC : L_KC;
+  CUtensorMap tm;
+  std::memset(&tm, 0, sizeof(tm));
+  if (!no_tma && aligned && (mc ? (post % kBM) == 0 : (K % 2) == 0)) {
+    const int Lt = mc ? L_MC_TMA : L_KC_TMA;
+    if (make_tmap(Lt, X, g, &tm)) L = Lt;
+  }
   const int grid = (int)std::min<int64_t>(g.ntiles, sm_count());
-  if (mc) return run_i8<true, false>(grid, X, g, Bimg, F, Xexp, out, beta, st);
-  if (vec) return run_i8<false, true>(grid, X, g, Bimg, F, Xexp, out, beta, st);
-  return run_i8<false, false>(grid, X, g, Bimg, F, Xexp, out, beta, st);
+  switch (g.Rp) {
+    case 16: return dispatch_i8<16>(L, grid, X, g, Bimg, F, Xexp, out, beta, tm, st);
+    case 32: return dispatch_i8<32>(L, grid, X, g, Bimg, F, Xexp, out, beta, tm, st);
+    case 48: return dispatch_i8<48>(L, grid, X, g, Bimg, F, Xexp, out, beta, tm, st);
+    case 64: return dispatch_i8<64>(L, grid, X, g, Bimg, F, Xexp, out, beta, tm, st);
+  }
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace cpd

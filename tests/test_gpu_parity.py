@@ -324,10 +324,11 @@ def test_full_size_sampled_rows(cpd, c, ttm_impl):
 
 # ------------------------------- INT8 tensor-core TTM -----------------------------------
 
+@pytest.mark.parametrize("digits", [True, False])
 @pytest.mark.parametrize("shape,R", [((37, 29, 41), 8), ((16, 130, 12), 64), ((33, 20, 17), 13), ((9, 10, 11, 12), 100),
                                      ((11, 7, 13), 200), ((6, 5, 3), 1), ((200, 3, 130), 33), ((5, 300, 4), 17),
-                                     ((64, 64, 64), 64), ((40, 33, 257), 32)])
-def test_ttm_i8_all_positions(cpd, shape, R):
+                                     ((64, 64, 64), 64), ((40, 33, 257), 32), ((3, 256, 128), 48), ((130, 48, 256), 64)])
+def test_ttm_i8_all_positions(cpd, shape, R, digits):
     """cpd_ttm_i8 (int8 digit slicing on tcgen05) against the oracle's T x_j A at every
     contraction position: ragged M tiles, K tails (odd K, K % 32 != 0), 1-4 N tiles."""
     rng = np.random.default_rng(sum(shape) + R + 1)
@@ -338,7 +339,7 @@ def test_ttm_i8_all_positions(cpd, shape, R):
         pre = int(np.prod(shape[:j])) if j else 1
         post = int(np.prod(shape[j + 1:])) if j < len(shape) - 1 else 1
         out = torch.empty((pre * post, R), dtype=torch.float64, device="cuda")
-        cpd.cpd_ttm_i8(T, pre, shape[j], post, torch.from_numpy(A).cuda(), R, out)
+        cpd.cpd_ttm_i8(T, pre, shape[j], post, torch.from_numpy(A).cuda(), R, out, use_digits=digits)
         ref = O.ttm(Tn, A, j).reshape(pre * post, R)
         assert rel(out.cpu().numpy(), ref) <= 1e-13, (j, rel(out.cpu().numpy(), ref))
 
