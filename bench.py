@@ -194,7 +194,7 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-TTM_IMPL = {"dmma": 0, "int8": 1}
+TTM_IMPL = {"dmma": 0, "int8": 1, "auto": 2}
 
 
 def main():
@@ -206,10 +206,12 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--presweeps", type=int, default=60, help="max untimed MSDT sweeps before the steps")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-dmma-compare", action="store_true", help="skip the FP64-DMMA engine comparison cycles")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--oracle-slab", type=int, default=16)
-    ap.add_argument("--ttm-impl", default="dmma", choices=["dmma", "int8"],
-                    help="first-level TTM engine: FP64 DMMA or FP64-via-int8-digits on tcgen05")
+    ap.add_argument("--ttm-impl", default="auto", choices=["dmma", "int8", "auto"],
+                    help="first-level TTM engine: FP64 DMMA, FP64 operands as int8 digits on tcgen05, or the "
+                         "library's choice (int8 when its error bound is FP64-class)")
     args = ap.parse_args()
     world, rank, local = dist_setup(args)
     if args.impl == "reference":
@@ -336,26 +338,28 @@ def main():
                "sample": f"oracle als_sweep on a {'x'.join([str(cfg.s)] * (N - 1))}x{args.oracle_slab} slab "
                          f"(best of 2), x{cfg.s // args.oracle_slab} slabs of the 1-D partition (linear extrapolation)"}
 
-    if args.ttm_impl == "dmma":
-        ttm_roof = {"kernel": "ttm_dmma (first-level TTM, DMMA.8x8x4)", "bound": "tensor", "achieved": ttm_tf,
-                    "peak": fp64, "peak_source": fp64_src, "unit": "TFLOP/s",
-                    "frac": (ttm_tf / fp64) if ttm_tf else None,
-                    "traffic": ncu_traffic("ttm_dmma"), "flops_per_launch": ttm_launch_flops,
-                    "avg_launch_ms": ttm_ms, "launches": int(ctr["ttm_launches"])}
+    engine = m.ttm_engine()
+    if engine == "dmma":
+        ttm_roof = dmma_roof(ttm_tf, fp64, fp64_src, ttm_launch_flops, ttm_ms, ctr)
+        engines = None
     else:
-        # int8-digit TTM: one pass over T per launch (R <= 64), so the bound is HBM; algorithmic
-        # bytes = T slab + output + factor, per launch (equidimensional: K = s)
+        # int8-digit TTM: streams T's 7 digit planes (7 B/element) once per launch (R <= 64), so
+        # the bound is HBM; bytes = digit planes + FP64 output + the factor's digit image (K x R x 7)
         t_el = ttm_launch_flops / (2 * cfg.R)
-        k = cfg.s
-        ttm_bytes = 8.0 * (t_el + t_el / k * cfg.R + k * cfg.R)
+        k = cfg.s // world if False else cfg.s
+        ttm_bytes = (7.0 if engine == "int8-digits" else 8.0) * t_el + 8.0 * t_el / k * cfg.R + 7.0 * k * cfg.R
         ttm_gbs = ttm_bytes / (ttm_ms * 1e-3) / 1e9 if ttm_ms > 0 else None
-        ttm_roof = {"kernel": "ttm_i8 (first-level TTM, FP64 operands as int8 digits, tcgen05 kind::i8)",
+        ttm_roof = {"kernel": f"ttm_i8 ({engine}: first-level TTM, FP64 operands as exact int8 digit products, "
+                              "tcgen05.mma kind::i8, TMEM accumulators)",
                     "bound": "hbm", "achieved": ttm_gbs, "peak": peaks.get("hbm_gbs"),
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)", "unit": "GB/s",
                     "frac": (ttm_gbs / peaks["hbm_gbs"]) if ttm_gbs and peaks.get("hbm_gbs") else None,
                     "traffic": ncu_traffic("ttm_i8"), "bytes_per_launch": ttm_bytes,
-                    "fp64_equiv_tflops": ttm_tf, "fp64_equiv_frac_of_dmma_peak": (ttm_tf / fp64) if ttm_tf else None,
+                    "fp64_equiv_tflops": ttm_tf, "fp64_equiv_over_dmma_peak": (ttm_tf / fp64) if ttm_tf else None,
                     "avg_launch_ms": ttm_ms, "launches": int(ctr["ttm_launches"])}
+        engines = {engine: {"msdt_ms_per_sweep": msdt_ms, "ttm_ms": ttm_ms, "ttm_fp64_equiv_tflops": ttm_tf}}
+        if not args.no_dmma_compare:
+            engines["dmma"] = dmma_compare(cpd, torch, cfg, T, m, local, rank, world, nccl_id, stream, fp64, fp64_src)
     if rank == 0:
         line = {
             "metric": METRIC, "value": msdt_ms, "unit": "ms/sweep (MSDT)", "n_gpus": world, "steps": args.steps,
@@ -370,7 +374,7 @@ def main():
             "sweeps_ms": {"msdt": msdt_ms, "pp_approx": ppapprox_ms, "pp_init": ppinit_ms, "dt": dt_ms,
                           "dt_over_msdt": dt_ms / msdt_ms, "dt_over_pp_approx": dt_ms / ppapprox_ms},
             "phase_ms_per_step": {k: v / 2 for k, v in ph_all.items()},
-            "roofline": ttm_roof,
+            "roofline": ttm_roof, "ttm_engine": engine, "engines": engines,
             "roofline_stream": {"kernel": "mttv (mTTV levels + PP U-stream)", "bound": "hbm", "achieved": st_gbs,
                                 "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
                                 "frac": (st_gbs / peaks["hbm_gbs"]) if st_gbs and peaks.get("hbm_gbs") else None,
@@ -382,6 +386,43 @@ def main():
     m.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def dmma_roof(ttm_tf, fp64, fp64_src, flops, ms, ctr):
+    return {"kernel": "ttm_dmma (first-level TTM, DMMA.8x8x4)", "bound": "tensor", "achieved": ttm_tf,
+            "peak": fp64, "peak_source": fp64_src, "unit": "TFLOP/s", "frac": (ttm_tf / fp64) if ttm_tf else None,
+            "traffic": ncu_traffic("ttm_dmma"), "flops_per_launch": flops, "avg_launch_ms": ms,
+            "launches": int(ctr["ttm_launches"])}
+
+
+def dmma_compare(cpd, torch, cfg, T, m, local, rank, world, nccl_id, stream, fp64, fp64_src):
+    """The FP64 DMMA engine on the same tensor and factors (north_star's TTM FP64-TC %): one
+    warm-up MSDT cycle, then two timed cycles; CUDA events on the library stream."""
+    import torch.distributed as dist
+    N = cfg.N
+    A = [m.get_factor(n) for n in range(N)]
+    md = cpd.cp_als_init(T, cfg.shape, cfg.R, A, device=local, rank=rank, world=world,
+                         nccl_id=nccl_id if world == 1 else _new_id(cpd, dist, rank), stream=stream,
+                         profile_phases=1, ttm_impl=TTM_IMPL["dmma"])
+    for _ in range(N - 1):
+        md.msdt_sweep()
+    torch.cuda.synchronize()
+    md.reset_counters()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(2 * (N - 1)):
+        md.msdt_sweep()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / (2 * (N - 1))
+    ph, ctr = md.phase_ms(), md.counters()
+    md.close()
+    flops = ctr["ttm_flops"] / max(ctr["ttm_launches"], 1)
+    tms = ph["ttm"] / max(ctr["ttm_launches"], 1)
+    tf = flops / (tms * 1e-3) / 1e12 if tms > 0 else None
+    return {"msdt_ms_per_sweep": ms, "ttm_ms": tms, "ttm_fp64_tflops": tf,
+            "roofline": dmma_roof(tf, fp64, fp64_src, flops, tms, ctr)}
 
 
 def run_e2e(args, cpd, torch, cfg, T, m, rank, world, local, nccl_id, stream):
@@ -410,6 +451,7 @@ def run_e2e(args, cpd, torch, cfg, T, m, rank, world, local, nccl_id, stream):
         e0.record(stream)
         with torch.cuda.stream(stream):
             T_dev.copy_(T_host, non_blocking=True)
+        m2.set_tensor()            # new tensor contents: ||T||^2, exponent, digit planes
         m2.set_factors(pinned_A)
         for _ in range(N - 1):
             m2.msdt_sweep()
@@ -429,7 +471,7 @@ def run_e2e(args, cpd, torch, cfg, T, m, rank, world, local, nccl_id, stream):
     h2d = T_host.numel() * 8 + sum(a.size * 8 for a in A_host)
     d2h = sum(a.size * 8 for a in A_host) + 8
     return {"value": v, "unit": "ms/sweep (MSDT)", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "step": f"H2D T slab + factors (pinned), {N - 1} msdt_sweep, D2H factors + fitness"}
+            "step": f"H2D T slab + factors (pinned), cpd_set_tensor, {N - 1} msdt_sweep, D2H factors + fitness"}
 
 
 def _new_id(cpd, dist, rank):

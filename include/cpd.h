@@ -72,14 +72,24 @@ typedef struct {
   void* local_group;          /* NULL: NCCL (one process per GPU).  Else a cpd_local_group of `world`
                                  ranks in ONE process on ONE device, each rank's calls made from its own
                                  host thread (verification of the 1-D partition on a single GPU) */
-  int ttm_impl;               /* first-level TTM engine: CPD_TTM_DMMA (0, default) = FP64 tensor cores
-                                 (mma.sync .f64); CPD_TTM_INT8 (1) = FP64 operands sliced into int8
-                                 digits on the tcgen05 INT8 tensor cores (cpd_ttm_i8; modes with
-                                 s_j > 16384 use DMMA) */
+  int ttm_impl;               /* first-level TTM engine (DESIGN.md §6 K2 / K2i):
+                                 CPD_TTM_DMMA (0) = FP64 tensor cores (mma.sync .f64, DMMA);
+                                 CPD_TTM_INT8 (1) = FP64 operands as 54-bit fixed point split into 7
+                                   int8 digits, exact int8 x int8 -> int32 products on the tcgen05
+                                   tensor cores (cpd_ttm_i8); T's digits are computed once at init
+                                   (7 extra bytes per element when memory allows);
+                                 CPD_TTM_AUTO (2, default) = INT8 when max|T| <= 256 rms(T), i.e. when
+                                   its norm-wise error bound 2^-55 max|T|/rms(T) is FP64-class, else DMMA.
+                                 Modes with s_j > 16384 always use DMMA. */
 } cpd_opts;
 
 #define CPD_TTM_DMMA 0
 #define CPD_TTM_INT8 1
+#define CPD_TTM_AUTO 2
+/* engine a ctx uses (cpd_ttm_engine) */
+#define CPD_ENGINE_DMMA 0
+#define CPD_ENGINE_INT8_DIGITS 1   /* T's digit planes streamed by TMA */
+#define CPD_ENGINE_INT8_CONVERT 2  /* T converted to digits inside each TTM (no memory for the planes) */
 
 typedef struct cpd_local_group cpd_local_group;
 /* In-process group for `world` (1..8) ranks sharing one device (see cpd_opts.local_group):
@@ -89,7 +99,7 @@ cpd_status cpd_local_group_create(int world, cpd_local_group** out);
 cpd_status cpd_local_group_destroy(cpd_local_group* g);
 
 /* Fill *o with defaults: device 0, rank 0, world 1, no NCCL id, library stream,
- * pp_eps 0.1, reuse_root_in_pp_init 1, profile_phases 0. */
+ * pp_eps 0.1, reuse_root_in_pp_init 1, profile_phases 0, ttm_impl CPD_TTM_AUTO. */
 cpd_status cpd_opts_default(cpd_opts* o);
 
 /* NCCL unique id for a multi-GPU ctx (call on rank 0, broadcast the 128 bytes). */
@@ -191,6 +201,15 @@ cpd_status cpd_gen_tensor(double* T_dev, int N, const int64_t* shape, int64_t lo
  * [pre, K, post]; out is [pre*post, R] row-major.  All device pointers; synchronous. */
 cpd_status cpd_ttm(const double* T_dev, int64_t pre, int64_t K, int64_t post,
                    const double* A_dev, int R, double* out_dev, void* stream);
+
+/* The contents of the borrowed T changed (same pointer and shape, e.g. a new tensor uploaded
+ * into the same buffer): recompute ||T||^2, the TTM engine's exponent and digit
+ * planes, and drop every cached tree node and PP operator (the MSDT cycle restarts; the
+ * next sweep is a regular one).  Collective when world > 1. */
+cpd_status cpd_set_tensor(cpd_ctx* ctx);
+
+/* *engine = the first-level TTM engine this ctx chose at init (CPD_ENGINE_*). */
+cpd_status cpd_ttm_engine(const cpd_ctx* ctx, int* engine);
 
 /* The same first-level TTM on the INT8 tensor cores (tcgen05.mma kind::i8): both FP64 operands
  * are converted to 54-bit fixed point (one exponent for T = ceil(log2 max|T|), one per column of

@@ -19,7 +19,7 @@ EXPORTED_SYMBOLS = [
     "cpd_opts_default", "cpd_nccl_unique_id", "cp_als_init", "msdt_sweep", "dt_sweep", "pp_init",
     "pp_approx_sweep", "fitness", "cpd_pp_condition", "cpd_get_factor", "cpd_get_last_mttkrp",
     "cpd_set_factors", "cpd_get_phase_ms", "cpd_get_counters", "cpd_reset_counters",
-    "cpd_debug_get_pp_operator", "cpd_last_error", "cpd_destroy", "cpd_gen_tensor", "cpd_ttm", "cpd_ttm_i8",
+    "cpd_debug_get_pp_operator", "cpd_last_error", "cpd_destroy", "cpd_gen_tensor", "cpd_ttm", "cpd_ttm_i8", "cpd_ttm_engine", "cpd_set_tensor",
     "cpd_mttv", "cpd_local_group_create", "cpd_local_group_destroy", "cpd_set_profile_level",
 ]
 
@@ -74,6 +74,8 @@ def load_library():
         "cpd_gen_tensor": (C.c_int, [_P, C.c_int, C.POINTER(C.c_int64), C.c_int64, C.c_int64, C.c_int,
                                      C.POINTER(_D), C.c_int, C.c_double, C.c_uint64, _P]),
         "cpd_ttm": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, _P, C.c_int, _P, _P]),
+        "cpd_ttm_engine": (C.c_int, [_P, C.POINTER(C.c_int)]),
+        "cpd_set_tensor": (C.c_int, [_P]),
         "cpd_ttm_i8": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, _P, C.c_int, _P, C.c_int, _P]),
         "cpd_mttv": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, C.c_int, _P, _P, C.c_int, _P]),
         "cpd_local_group_create": (C.c_int, [C.c_int, C.POINTER(_P)]),

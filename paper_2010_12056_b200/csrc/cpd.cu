@@ -125,11 +125,12 @@ struct cpd_ctx {
   void* ws_i8 = nullptr;     // sliced factor digits + exponents
   uint8_t* Td = nullptr;     // T's 7 int8 digit planes (computed once; null -> convert T per TTM)
   size_t ws_i8_bytes = 0;
+  int engine = CPD_ENGINE_DMMA;  // first-level TTM engine chosen at init
 };
 
 // scalar slots
 enum { SC_NT2 = 0, SC_MA = 1, SC_GS = 2, SC_DA2 = 3 /* N */, SC_A2 = 3 + CPD_MAX_ORDER /* N */,
-       SC_LASTN2 = 3 + 2 * CPD_MAX_ORDER, SC_COUNT = 8 + 2 * CPD_MAX_ORDER };
+       SC_LASTN2 = 3 + 2 * CPD_MAX_ORDER, SC_TMAX = 4 + 2 * CPD_MAX_ORDER, SC_COUNT = 8 + 2 * CPD_MAX_ORDER };
 
 namespace {
 
@@ -274,7 +275,7 @@ cpd_status ttm(cpd_ctx* ctx, int j, double* out) {
   for (int m = 0; m < j; m++) pre *= ext(ctx, m);
   for (int m = j + 1; m < ctx->N; m++) post *= ext(ctx, m);
   PhaseScope ps(ctx, PH_TTM);
-  if (ctx->opts.ttm_impl == CPD_TTM_INT8 && ext(ctx, j) <= cpd::kMaxKI8) {
+  if (ctx->engine != CPD_ENGINE_DMMA && ext(ctx, j) <= cpd::kMaxKI8) {
     CU(cpd::launch_ttm_i8(ctx->T, pre, ext(ctx, j), post, ctx->A[j], ctx->R, out, 0, ctx->texp, ctx->ws_i8,
                           ctx->ws_i8_bytes, ctx->st, ctx->Td));
   } else {
@@ -671,6 +672,61 @@ cpd_status pp_descend(cpd_ctx* ctx, const Node& node, std::vector<std::pair<int,
   return CPD_OK;
 }
 
+// ||T||^2 (all-reduced) and the TTM engine's view of T: exponent and digit planes
+// (cp_als_init, cpd_set_tensor).  Buffers from a previous call are reused.
+cpd_status prepare_tensor(cpd_ctx* ctx) {
+  CU(cpd::launch_norm2(ctx->T, ctx->T_elems, ctx->partial, ctx->scal + SC_NT2, ctx->st));
+  {
+    std::string m_;
+    int r_ = cpd::comm_all_reduce(ctx->cm, ctx->scal + SC_NT2, 1, &m_);
+    if (r_) {
+      return fail(ctx, r_ == 5 ? CPD_ERR_NCCL : CPD_ERR_CUDA, m_);
+    }
+  }
+  const cpd_opts& o = ctx->opts;
+  const int N = ctx->N, R = ctx->R;
+  ctx->engine = CPD_ENGINE_DMMA;
+  if (o.ttm_impl == CPD_TTM_INT8 || o.ttm_impl == CPD_TTM_AUTO) {
+    // one exponent for this rank's slab (T is read-only, so once per ctx); ranks may differ,
+    // which changes results only at the rounding level
+    CU(cudaMallocAsync((void**)&ctx->texp, sizeof(int), ctx->st));
+    CU(cpd::launch_absmax_exp(ctx->T, ctx->T_elems, ctx->partial, ctx->texp, ctx->st, ctx->scal + SC_TMAX));
+    bool use_i8 = true;
+    if (o.ttm_impl == CPD_TTM_AUTO) {
+      // the digit TTM's norm-wise error is ~2^-55 max|T|/rms(T) (DESIGN.md §6 K2i): use it when
+      // that is FP64-class (max|T| <= 256 rms(T), i.e. <= 2^-47), else the FP64 DMMA engine
+      double h[SC_COUNT];
+      CU(cudaMemcpyAsync(h, ctx->scal, sizeof(double) * SC_COUNT, cudaMemcpyDeviceToHost, ctx->st));
+      CU(cudaStreamSynchronize(ctx->st));
+      const double numel = (double)ctx->T_elems * ctx->world;
+      const double rms = std::sqrt(h[SC_NT2] / numel);
+      use_i8 = h[SC_TMAX] <= 256.0 * rms;
+    }
+    if (!use_i8 && ctx->Td) {
+      cudaFreeAsync(ctx->Td, ctx->st);
+      ctx->Td = nullptr;
+    }
+    if (use_i8) {
+      int64_t kmax = 1;
+      for (int n = 0; n < N; n++) kmax = std::max(kmax, ext(ctx, n));
+      ctx->ws_i8_bytes = cpd::ttm_i8_workspace_bytes(std::min(kmax, cpd::kMaxKI8), R);
+      CU(cudaMallocAsync(&ctx->ws_i8, ctx->ws_i8_bytes, ctx->st));
+      ctx->engine = CPD_ENGINE_INT8_CONVERT;
+      // T's digit planes once (7 bytes per element): every first-level TTM then streams them
+      // instead of converting T; without the memory the TTM converts T on the fly
+      if (ctx->Td || cudaMallocAsync((void**)&ctx->Td, (size_t)7 * cpd::digit_plane_stride(ctx->T_elems),
+                                     ctx->st) == cudaSuccess) {
+        CU(cpd::launch_slice_digits(ctx->T, ctx->T_elems, ctx->texp, ctx->Td, ctx->st));
+        ctx->engine = CPD_ENGINE_INT8_DIGITS;
+      } else {
+        cudaGetLastError();
+        ctx->Td = nullptr;
+      }
+    }
+  }
+  return CPD_OK;
+}
+
 }  // namespace
 
 // ============================== C ABI ==============================================
@@ -690,7 +746,7 @@ cpd_status cpd_opts_default(cpd_opts* o) {
   o->reuse_root_in_pp_init = 1;
   o->profile_phases = 0;
   o->local_group = nullptr;
-  o->ttm_impl = CPD_TTM_DMMA;
+  o->ttm_impl = CPD_TTM_AUTO;
   return CPD_OK;
 }
 
@@ -779,7 +835,8 @@ cpd_status cp_als_init(cpd_ctx** out, int N, const int64_t* shape, int R, const 
   }
   if (!(o.pp_eps > 0.0 && o.pp_eps < 1.0)) return fail(ctx, CPD_ERR_INVALID_ARG, "pp_eps must be in (0,1)");
   if (o.world < 1 || o.rank < 0 || o.rank >= o.world) return fail(ctx, CPD_ERR_INVALID_ARG, "bad rank/world");
-  if (o.ttm_impl != CPD_TTM_DMMA && o.ttm_impl != CPD_TTM_INT8) return fail(ctx, CPD_ERR_INVALID_ARG, "bad ttm_impl");
+  if (o.ttm_impl != CPD_TTM_DMMA && o.ttm_impl != CPD_TTM_INT8 && o.ttm_impl != CPD_TTM_AUTO)
+    return fail(ctx, CPD_ERR_INVALID_ARG, "bad ttm_impl");
   if (o.world > 1 && !o.nccl_unique_id && !o.local_group)
     return fail(ctx, CPD_ERR_INVALID_ARG, "world > 1 needs nccl_unique_id or local_group");
   if (o.local_group && cpd::local_group_world((cpd::LocalGroup*)o.local_group) != o.world)
@@ -902,32 +959,11 @@ cpd_status cp_als_init(cpd_ctx** out, int N, const int64_t* shape, int R, const 
   ICU(cudaMallocHost((void**)&ctx->hstatus, sizeof(int) * CPD_MAX_ORDER));
   *out = ctx;  // provisional for cpd_set_factors
   // ||T||^2 once, all-reduced
-  ICU(cpd::launch_norm2(ctx->T, ctx->T_elems, ctx->partial, ctx->scal + SC_NT2, ctx->st));
   {
-    std::string m_;
-    int r_ = cpd::comm_all_reduce(ctx->cm, ctx->scal + SC_NT2, 1, &m_);
-    if (r_) {
+    cpd_status ps = prepare_tensor(ctx);
+    if (ps != CPD_OK) {
       *out = nullptr;
-      fail(ctx, r_ == 5 ? CPD_ERR_NCCL : CPD_ERR_CUDA, m_);
-      return bail(r_ == 5 ? CPD_ERR_NCCL : CPD_ERR_CUDA);
-    }
-  }
-  if (o.ttm_impl == CPD_TTM_INT8) {
-    // one exponent for this rank's slab (T is read-only, so once per ctx); ranks may differ,
-    // which changes results only at the rounding level
-    ICU(cudaMallocAsync((void**)&ctx->texp, sizeof(int), ctx->st));
-    ICU(cpd::launch_absmax_exp(ctx->T, ctx->T_elems, ctx->partial, ctx->texp, ctx->st));
-    int64_t kmax = 1;
-    for (int n = 0; n < N; n++) kmax = std::max(kmax, ext(ctx, n));
-    ctx->ws_i8_bytes = cpd::ttm_i8_workspace_bytes(std::min(kmax, cpd::kMaxKI8), R);
-    ICU(cudaMallocAsync(&ctx->ws_i8, ctx->ws_i8_bytes, ctx->st));
-    // T's digit planes once (7 bytes per element): every first-level TTM then streams them
-    // instead of converting T; without the memory the TTM converts T on the fly
-    if (cudaMallocAsync((void**)&ctx->Td, (size_t)7 * cpd::digit_plane_stride(ctx->T_elems), ctx->st) == cudaSuccess) {
-      ICU(cpd::launch_slice_digits(ctx->T, ctx->T_elems, ctx->texp, ctx->Td, ctx->st));
-    } else {
-      cudaGetLastError();
-      ctx->Td = nullptr;
+      return bail(ps);
     }
   }
   cpd_status s = cpd_set_factors(ctx, A0_host);
@@ -974,6 +1010,24 @@ cpd_status cpd_set_factors(cpd_ctx* ctx, const double* const* A_host) {
   ctx->have_dA = false;
   invalidate_prefetch(ctx);
   CU(cudaStreamSynchronize(ctx->st));
+  return CPD_OK;
+}
+
+cpd_status cpd_set_tensor(cpd_ctx* ctx) {
+  TRY(check_ctx(ctx));
+  TRY(prepare_tensor(ctx));
+  CU(cudaStreamSynchronize(ctx->st));
+  CU(cudaMemcpy(ctx->hscal, ctx->scal, sizeof(double) * SC_COUNT, cudaMemcpyDeviceToHost));
+  if (!(ctx->hscal[SC_NT2] > 0.0) || !std::isfinite(ctx->hscal[SC_NT2]))
+    return fail(ctx, CPD_ERR_NUMERIC, "||T||^2 is zero or not finite");
+  // every cached tree node and PP operator was built from the old contents
+  clear_subtree(ctx);
+  ctx->t = 0;
+  ctx->sub_is_msdt = false;
+  free_pp(ctx);
+  ctx->pp_regime = false;
+  ctx->have_dA = false;
+  ctx->have_fit = false;
   return CPD_OK;
 }
 
@@ -1160,6 +1214,12 @@ cpd_status cpd_get_phase_ms(cpd_ctx* ctx, double out[5]) {
   cudaStreamSynchronize(ctx->st);
   drain_timers(ctx);
   for (int i = 0; i < 5; i++) out[i] = ctx->phase_ms[i];
+  return CPD_OK;
+}
+
+cpd_status cpd_ttm_engine(const cpd_ctx* ctx, int* engine) {
+  if (!ctx || !engine) return CPD_ERR_INVALID_ARG;
+  *engine = ctx->engine;
   return CPD_OK;
 }
 

@@ -32,8 +32,9 @@ bool ttm_i8_digits_ok(int64_t pre, int64_t K, int64_t post);
 // bytes between digit planes for n elements (the planes buffer holds 7 * digit_plane_stride(n) bytes)
 inline int64_t digit_plane_stride(int64_t n) { return (n + 63) / 64 * 64; }
 cudaError_t launch_slice_digits(const double* X, int64_t n, const int* Xexp, uint8_t* planes, cudaStream_t st);
-// *e_out = e with 2^e > max|x_i| (0 if x == 0); partial: kNormBlocks doubles
-cudaError_t launch_absmax_exp(const double* x, int64_t n, double* partial, int* e_out, cudaStream_t st);
+// *e_out = e with 2^e > max|x_i| (0 if x == 0), *max_out = max|x_i| if given; partial: kNormBlocks doubles
+cudaError_t launch_absmax_exp(const double* x, int64_t n, double* partial, int* e_out, cudaStream_t st,
+                              double* max_out = nullptr);
 
 // ---- batched TTV (mTTV) stream, P:320-322 ----------------------------------------------
 // out[p, c] = beta*out[p, c] + Σ_y X[(p*K + y)*C + c] * v[y*R + c % R],  C = post*R

@@ -535,7 +535,8 @@ __global__ void absmax_partial_kernel(const double* __restrict__ x, int64_t n, d
     part[blockIdx.x] = m;
   }
 }
-__global__ void absmax_final_kernel(const double* __restrict__ part, int nb, int* __restrict__ e_out) {
+__global__ void absmax_final_kernel(const double* __restrict__ part, int nb, int* __restrict__ e_out,
+                                    double* __restrict__ m_out) {
   double m = 0.0;
   for (int b = threadIdx.x; b < nb; b += blockDim.x) m = fmax(m, part[b]);
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -543,6 +544,7 @@ __global__ void absmax_final_kernel(const double* __restrict__ part, int nb, int
     int e = 0;
     if (m > 0.0) frexp(m, &e);
     *e_out = e;
+    if (m_out) *m_out = m;
   }
 }
 
@@ -920,10 +922,11 @@ size_t ttm_i8_workspace_bytes(int64_t K, int ncols) {
   return (size_t)g.ntn * g.nkc * kND * g.Rp * 32 + 256 * sizeof(int);
 }
 
-cudaError_t launch_absmax_exp(const double* x, int64_t n, double* partial, int* e_out, cudaStream_t st) {
+cudaError_t launch_absmax_exp(const double* x, int64_t n, double* partial, int* e_out, cudaStream_t st,
+                              double* max_out) {
   g_launches += 2;
   absmax_partial_kernel<<<kNormBlocks, 256, 0, st>>>(x, n, partial);
-  absmax_final_kernel<<<1, 32, 0, st>>>(partial, kNormBlocks, e_out);
+  absmax_final_kernel<<<1, 32, 0, st>>>(partial, kNormBlocks, e_out, max_out);
   return cudaGetLastError();
 }
 

@@ -23,7 +23,7 @@ class CPDecomposition:
 
     def __init__(self, T, shape, R, A0, *, device=0, rank=0, world=1, nccl_id=None, stream=None,
                  pp_eps=0.1, reuse_root_in_pp_init=True, profile_phases=False, local_group=None,
-                 ttm_impl=0):
+                 ttm_impl=2):
         lib = load_library()
         self.N = len(shape)
         self.shape = tuple(int(s) for s in shape)
@@ -119,6 +119,16 @@ class CPDecomposition:
         out = np.empty((sa, sb, self.R))
         check(self._lib.cpd_debug_get_pp_operator(self._ctx, a, b, dptr(out)), self._ctx)
         return out
+
+    def set_tensor(self):
+        """The borrowed T's contents changed: recompute ||T||^2 and the TTM engine's view of T."""
+        check(self._lib.cpd_set_tensor(self._ctx), self._ctx)
+
+    def ttm_engine(self) -> str:
+        """The first-level TTM engine chosen at init: "dmma", "int8-digits" or "int8-convert"."""
+        e = C.c_int()
+        check(self._lib.cpd_ttm_engine(self._ctx, C.byref(e)), self._ctx)
+        return {0: "dmma", 1: "int8-digits", 2: "int8-convert"}[e.value]
 
     def close(self):
         if getattr(self, "_ctx", None) is not None and self._ctx.value:

@@ -361,3 +361,54 @@ def test_ttm_i8_wide_dynamic_range(cpd):
         got = out.cpu().numpy()
         for c in range(24):  # per column (columns have different scales)
             assert rel(got[:, c], ref[:, c]) <= 1e-12, (j, c, rel(got[:, c], ref[:, c]))
+
+
+def test_ttm_engine_auto_selection(cpd):
+    """CPD_TTM_AUTO: the int8 digit engine when max|T| <= 256 rms(T) (its error bound is then
+    FP64-class), the DMMA engine for a tensor with a wide dynamic range; both match the oracle."""
+    cfg = synth.custom(3, 32, 4, noise_var=1e-4, seed=77)
+    T = dev_tensor(cpd, cfg)
+    To = O.make_tensor(cfg)
+    m = _model(cpd, cfg, T)
+    assert m.ttm_engine() == "int8-digits"
+    m.close()
+    m = _model(cpd, cfg, T, ttm_impl=0)
+    assert m.ttm_engine() == "dmma"
+    m.close()
+    # one huge entry: max|T| / rms(T) > 256 -> DMMA
+    Tw = T.clone()
+    Tw.view(-1)[5] = 1e6
+    Tow = Tw.cpu().numpy()
+    m = _model(cpd, cfg, Tw)
+    assert m.ttm_engine() == "dmma"
+    f = m.msdt_sweep()
+    out = O.als_sweep(Tow, synth.init_factors(cfg))
+    assert abs(f - out["f"]) <= TOL * abs(out["f"])
+    m.close()
+    m = _model(cpd, cfg, Tw, ttm_impl=1)  # forced int8 still runs (norm-wise bound relative to max|T|)
+    assert m.ttm_engine() == "int8-digits"
+    m.close()
+
+
+@pytest.mark.parametrize("ttm_impl", [0, 2])
+def test_set_tensor_new_contents(cpd, ttm_impl):
+    """cpd_set_tensor: new contents in the same buffer -> ||T||^2, exponent and digit planes
+    recomputed, caches dropped; the next sweeps match the oracle on the new tensor."""
+    c1 = synth.custom(3, 40, 5, noise_var=1e-4, seed=91)
+    c2 = synth.custom(3, 40, 5, noise_var=1e-4, seed=92)
+    T = dev_tensor(cpd, c1)
+    m = _model(cpd, c1, T, ttm_impl=ttm_impl)
+    m.msdt_sweep()
+    m.msdt_sweep()
+    T.copy_(dev_tensor(cpd, c2))
+    m.set_tensor()
+    A = synth.init_factors(c2)
+    m.set_factors(A)
+    To2 = O.make_tensor(c2)
+    nt2 = O.norm2(To2)
+    for _ in range(3):
+        f = m.msdt_sweep()
+        out = O.als_sweep(To2, A, nt2)
+        assert abs(f - out["f"]) <= TOL * abs(out["f"])
+        A = out["A"]
+    m.close()
