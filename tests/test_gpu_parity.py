@@ -366,7 +366,7 @@ def test_ttm_i8_wide_dynamic_range(cpd):
 def test_ttm_engine_auto_selection(cpd):
     """CPD_TTM_AUTO: the int8 digit engine when max|T| <= 256 rms(T) (its error bound is then
     FP64-class), the DMMA engine for a tensor with a wide dynamic range; both match the oracle."""
-    cfg = synth.custom(3, 32, 4, noise_var=1e-4, seed=77)
+    cfg = synth.custom(3, 48, 4, noise_var=1e-4, seed=77)
     T = dev_tensor(cpd, cfg)
     To = O.make_tensor(cfg)
     m = _model(cpd, cfg, T)
@@ -375,7 +375,7 @@ def test_ttm_engine_auto_selection(cpd):
     m = _model(cpd, cfg, T, ttm_impl=0)
     assert m.ttm_engine() == "dmma"
     m.close()
-    # one huge entry: max|T| / rms(T) > 256 -> DMMA
+    # one huge entry: max|T| / rms(T) -> sqrt(48^3) = 333 > 256 -> DMMA
     Tw = T.clone()
     Tw.view(-1)[5] = 1e6
     Tow = Tw.cpu().numpy()
