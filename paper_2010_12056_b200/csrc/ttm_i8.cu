@@ -664,7 +664,7 @@ template <int L, int RP>
 __global__ void __launch_bounds__(kThreadsD, 1)
     ttm_i8d_kernel(Geo g, const uint8_t* __restrict__ Bimg, const int* __restrict__ Fexp,
                    const int* __restrict__ Xexp, double* __restrict__ out, int beta,
-                   const __grid_constant__ CUtensorMap tmap) {
+                   const __grid_constant__ CUtensorMap tmap, int dbg) {
   constexpr int Rp = RP;
   constexpr int Bbytes = kND * Rp * 32;
   constexpr int NDS = kStagesD;
@@ -791,6 +791,7 @@ __global__ void __launch_bounds__(kThreadsD, 1)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll 1
       for (int c0 = half * CH; c0 < (half + 1) * CH; c0 += 8) {
+        if (dbg & 32) break;
         uint32_t D[kND][8];
 #pragma unroll
         for (int d = 0; d < kND; d++) {
@@ -911,7 +912,8 @@ cudaError_t run_i8d(int grid, const Geo& g, const uint8_t* Bimg, const int* F, c
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  ttm_i8d_kernel<L, RP><<<grid, kThreadsD, kSmemD, st>>>(g, Bimg, F, Xexp, out, beta, tm);
+  static const int dbg = getenv("CPD_I8_DBG") ? atoi(getenv("CPD_I8_DBG")) : 0;  // profiling switches
+  ttm_i8d_kernel<L, RP><<<grid, kThreadsD, kSmemD, st>>>(g, Bimg, F, Xexp, out, beta, tm, dbg);
   return cudaGetLastError();
 }
 
