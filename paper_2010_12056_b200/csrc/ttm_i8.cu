@@ -649,13 +649,16 @@ cudaError_t dispatch_i8(int L, int grid, const double* X, const Geo& g, const ui
 //      bytes per plane, 128-byte swizzle = UMMA MN-major SWIZZLE_128B.
 // Warps: 0 TMA producer, 1 TMEM allocator + MMA issuer, 2-9 epilogue (two per lane quarter).
 // ============================================================================================
-enum { D_KC = 0, D_MC = 1 };
+// loader layouts of the digit kernel: KC, or MC with an MN atom of 128 / 64 / 32 bytes
+// (post % 128 == 0, or post == 64 / 32 with 2 / 4 consecutive prefix indices per tile)
+enum { D_KC = 0, D_MC128 = 1, D_MC64 = 2, D_MC32 = 3 };
 constexpr int kStagesD = 5;
-constexpr int kThreadsD = 32 * 10;
-constexpr int kSmemD = kStagesD * kDStage + 256;
+constexpr int kEpiWarps = 16;                        // 4 per TMEM lane quarter
+constexpr int kThreadsD = 32 * (2 + kEpiWarps);
+constexpr int kSmemD = kStagesD * kDStage + 256 + 256 * 8;  // stages, barriers, column scales
 static_assert(kSmemD <= 232448, "smem");
 
-// UMMA descriptor with a swizzle layout type (2 = 128B, 6 = 32B), base offset 0
+// UMMA descriptor with a swizzle layout type (2 = 128B, 4 = 64B, 6 = 32B), base offset 0
 __device__ __forceinline__ uint64_t sdesc_sw(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
   return sdesc(addr, lbo, sbo) | ((uint64_t)layout << 61);
 }
@@ -668,21 +671,31 @@ __global__ void __launch_bounds__(kThreadsD, 1)
   constexpr int Rp = RP;
   constexpr int Bbytes = kND * Rp * 32;
   constexpr int NDS = kStagesD;
+  // TMEM accumulator buffers: 7 diagonals x Rp columns each; two (ping-pong) when they fit
+  constexpr int NACC = (2 * kND * Rp <= 512 && kND * Rp <= 256) ? 2 : 1;
+  constexpr int MCW = L == D_MC128 ? 128 : L == D_MC64 ? 64 : 32;  // MN atom bytes
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NDS * kDStage);
   const uint32_t full0 = su32(bars), empty0 = su32(bars + NDS);
-  const uint32_t tfull = su32(bars + 2 * NDS), tempty = su32(bars + 2 * NDS + 1);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * NDS + 2);
+  const uint32_t tfull0 = su32(bars + 2 * NDS), tempty0 = su32(bars + 2 * NDS + 2);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * NDS + 4);
+  double* colscale = reinterpret_cast<double*>(smem + NDS * kDStage + 256);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < NDS; s++) {
       mbar_init(full0 + 8 * s, 1);
       mbar_init(empty0 + 8 * s, 1);
     }
-    mbar_init(tfull, 1);
-    mbar_init(tempty, 256);
+    for (int b = 0; b < 2; b++) {
+      mbar_init(tfull0 + 8 * b, 1);
+      mbar_init(tempty0 + 8 * b, 32 * kEpiWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+  }
+  {
+    const int ex = *Xexp;  // 2^(e_X + F_c - 60) per output column c
+    for (int c = tid; c < g.ncols; c += blockDim.x) colscale[c] = pow2(ex + Fexp[c] - 60);
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(tslot)));
@@ -704,7 +717,7 @@ __global__ void __launch_bounds__(kThreadsD, 1)
         const int64_t i0 = (tile / g.ntn) * kBM;
         const int nt = (int)(tile % g.ntn);
         int p = 0, m0 = 0;
-        if constexpr (L == D_MC) {
+        if constexpr (L != D_KC) {
           p = (int)(i0 / g.post);
           m0 = (int)(i0 - (int64_t)p * g.post);
         }
@@ -744,13 +757,18 @@ __global__ void __launch_bounds__(kThreadsD, 1)
     if (lane == 0) {
       int s = 0;
       uint32_t par = 0;
-      // A: KC K-major SW32 (8-row groups of 256 B); MC MN-major SW128 (8-k-row groups of 1 KB)
-      constexpr uint32_t A_LBO = L == D_KC ? 16 : 16, A_SBO = L == D_KC ? 256 : 1024;
-      constexpr uint32_t A_LAYOUT = L == D_KC ? 6 : 2;
+      // A: KC K-major SW32 (8-row groups of 256 B); MC MN-major, swizzle = MN atom width:
+      // LBO = stride between the G atoms (one prefix index each), SBO = 8 k-rows of the atom
+      constexpr uint32_t A_LBO = L == D_KC ? 16 : 32 * MCW;
+      constexpr uint32_t A_SBO = L == D_KC ? 256 : 8 * MCW;
+      constexpr uint32_t A_LAYOUT = (L == D_KC || L == D_MC32) ? 6 : L == D_MC64 ? 4 : 2;
       constexpr uint32_t AMAJ = L == D_KC ? 0u : (1u << 15);
       for (int64_t tt = 0; tt < my_tiles; tt++) {
-        mbar_wait_sleep(tempty, ((uint32_t)tt & 1) ^ 1);
+        const int ab = NACC == 2 ? (int)(tt & 1) : 0;
+        const uint32_t use = NACC == 2 ? (uint32_t)(tt >> 1) : (uint32_t)tt;  // uses of this buffer so far
+        mbar_wait_sleep(tempty0 + 8 * ab, (use & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t dcol = tmem + ab * 256;
         for (int kc = 0; kc < g.nkc; kc++) {
           mbar_wait(full0 + 8 * s, par);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -762,8 +780,8 @@ __global__ void __launch_bounds__(kThreadsD, 1)
             const int n = (a + 1) * Rp;  // diagonals 0..a
             const uint64_t ad = ad0 + (uint64_t)((a * kAPlane) >> 4);
             const uint64_t bd = bd0 + (uint64_t)(((kND - 1 - a) * Rp * 32) >> 4);  // B planes 6-a..6
-            mma_i8(tmem, ad, bd, idesc(n > 256 ? 256 : n) | AMAJ, acc);
-            if (n > 256) mma_i8(tmem + 256, ad, bd + ((256 * 32) >> 4), idesc(n - 256) | AMAJ, acc);
+            mma_i8(dcol, ad, bd, idesc(n > 256 ? 256 : n) | AMAJ, acc);
+            if (n > 256) mma_i8(dcol + 256, ad, bd + ((256 * 32) >> 4), idesc(n - 256) | AMAJ, acc);
           }
           mma_commit(empty0 + 8 * s);
           if (++s == NDS) {
@@ -771,35 +789,36 @@ __global__ void __launch_bounds__(kThreadsD, 1)
             par ^= 1;
           }
         }
-        mma_commit(tfull);
+        mma_commit(tfull0 + 8 * ab);
       }
     }
     __syncwarp();
   } else {
-    // ===================== epilogue: warps 2-9, lane quarter warp % 4, column half =====================
+    // ===================== epilogue: 16 warps, lane quarter warp % 4, column quarter =====================
     const int q = warp & 3;
-    const int half = (warp - 2) >> 2;
+    const int cq = (warp - 2) >> 2;  // 0..3
     const int r = q * 32 + lane;
-    const int ex = *Xexp;
-    constexpr int CH = Rp / 2;  // columns per half (8, 16, 24, 32)
+    constexpr int CQ = (Rp / 4 + 7) / 8 * 8;  // columns per epilogue warp, a multiple of 8
     for (int64_t tt = 0; tt < my_tiles; tt++) {
       const int64_t tile = blockIdx.x + tt * gridDim.x;
       const int64_t i = (tile / g.ntn) * kBM + r;
       const int nt = (int)(tile % g.ntn);
       const int n0 = nt * g.Rn;
-      mbar_wait_sleep(tfull, (uint32_t)tt & 1);
+      const int ab = NACC == 2 ? (int)(tt & 1) : 0;
+      const uint32_t use = NACC == 2 ? (uint32_t)(tt >> 1) : (uint32_t)tt;
+      mbar_wait_sleep(tfull0 + 8 * ab, use & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t tbase = tmem + ab * 256 + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
-      for (int c0 = half * CH; c0 < (half + 1) * CH; c0 += 8) {
+      for (int c0 = cq * CQ; c0 < min(Rp, (cq + 1) * CQ); c0 += 8) {
         if (dbg & 32) break;
         uint32_t D[kND][8];
 #pragma unroll
         for (int d = 0; d < kND; d++) {
-          const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + d * Rp + c0;
           asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                        : "=r"(D[d][0]), "=r"(D[d][1]), "=r"(D[d][2]), "=r"(D[d][3]), "=r"(D[d][4]),
                          "=r"(D[d][5]), "=r"(D[d][6]), "=r"(D[d][7])
-                       : "r"(ta));
+                       : "r"(tbase + d * Rp + c0));
         }
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         const int cmax = min(8, min(g.Rn - c0, g.ncols - n0 - c0));
@@ -807,12 +826,13 @@ __global__ void __launch_bounds__(kThreadsD, 1)
           double v[8];
 #pragma unroll
           for (int j = 0; j < 8; j++) {
+            // Σ_d D_d 256^d: exact int64 partial sums of three diagonals, two FP64 roundings
             const long long l0 = (long long)(int)D[0][j] + ((long long)(int)D[1][j] << 8) +
                                  ((long long)(int)D[2][j] << 16);
             const long long l1 = (long long)(int)D[3][j] + ((long long)(int)D[4][j] << 8) +
                                  ((long long)(int)D[5][j] << 16);
             const double t = fma((double)(int)D[6][j], 281474976710656.0 /* 2^48 */, (double)l1 * 16777216.0);
-            v[j] = (t + (double)l0) * pow2(ex + Fexp[n0 + c0 + min(j, cmax - 1)] - 60);
+            v[j] = (t + (double)l0) * colscale[n0 + c0 + min(j, cmax - 1)];
           }
           double* orow = out + i * g.ncols + n0 + c0;
           if (cmax == 8 && !beta && ((reinterpret_cast<uintptr_t>(orow) & 31) == 0)) {
@@ -828,7 +848,7 @@ __global__ void __launch_bounds__(kThreadsD, 1)
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mbar_arrive(tempty);
+      mbar_arrive(tempty0 + 8 * ab);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -893,12 +913,14 @@ bool make_tmap_digits(int L, const uint8_t* Xd, const Geo& g, CUtensorMap* tm) {
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   } else {
+    const int mcw = L == D_MC128 ? 128 : L == D_MC64 ? 64 : 32;
     cuuint64_t dims[4] = {(cuuint64_t)g.post, (cuuint64_t)g.K, (cuuint64_t)g.pre, (cuuint64_t)kND};
     cuuint64_t strides[3] = {(cuuint64_t)g.post, (cuuint64_t)g.K * g.post, numel};
-    cuuint32_t box[4] = {(cuuint32_t)kBM, 32, 1, (cuuint32_t)kND}, es[4] = {1, 1, 1, 1};
+    cuuint32_t box[4] = {(cuuint32_t)mcw, 32, (cuuint32_t)(kBM / mcw), (cuuint32_t)kND}, es[4] = {1, 1, 1, 1};
+    const CUtensorMapSwizzle sw =
+        mcw == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : mcw == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
     r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(Xd), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   }
   return r == CUDA_SUCCESS;
 }
@@ -940,7 +962,9 @@ cudaError_t launch_slice_digits(const double* X, int64_t n, const int* Xexp, uin
 }
 
 bool ttm_i8_digits_ok(int64_t pre, int64_t K, int64_t post) {
-  return post > 1 ? (post % kBM) == 0 : (K % 16) == 0;
+  if (post == 1) return (K % 16) == 0;
+  if ((post % kBM) == 0) return true;
+  return (post == 64 && pre % 2 == 0) || (post == 32 && pre % 4 == 0);
 }
 
 cudaError_t launch_ttm_i8(const double* X, int64_t pre, int64_t K, int64_t post, const double* B, int ncols,
@@ -963,14 +987,18 @@ cudaError_t launch_ttm_i8(const double* X, int64_t pre, int64_t K, int64_t post,
   const int grid0 = (int)std::min<int64_t>(g.ntiles, sm_count());
   static const bool no_digits = getenv("CPD_I8_NO_DIGITS") != nullptr;
   if (Xd && !no_digits && ttm_i8_digits_ok(pre, K, post) && ((uintptr_t)Xd % 16) == 0) {
-    const int Ld = post > 1 ? D_MC : D_KC;
+    const int Ld = post == 1 ? D_KC : (post % kBM) == 0 ? D_MC128 : post == 64 ? D_MC64 : D_MC32;
     CUtensorMap tmd;
     if (make_tmap_digits(Ld, Xd, g, &tmd)) {
       switch (g.Rp) {
-#define CPD_I8D_CASE(RP_) \
-  case RP_:               \
-    return Ld == D_KC ? run_i8d<D_KC, RP_>(grid0, g, Bimg, F, Xexp, out, beta, tmd, st) \
-                      : run_i8d<D_MC, RP_>(grid0, g, Bimg, F, Xexp, out, beta, tmd, st);
+#define CPD_I8D_CASE(RP_)                                                                         \
+  case RP_:                                                                                       \
+    switch (Ld) {                                                                                 \
+      case D_KC: return run_i8d<D_KC, RP_>(grid0, g, Bimg, F, Xexp, out, beta, tmd, st);          \
+      case D_MC128: return run_i8d<D_MC128, RP_>(grid0, g, Bimg, F, Xexp, out, beta, tmd, st);    \
+      case D_MC64: return run_i8d<D_MC64, RP_>(grid0, g, Bimg, F, Xexp, out, beta, tmd, st);      \
+      default: return run_i8d<D_MC32, RP_>(grid0, g, Bimg, F, Xexp, out, beta, tmd, st);         \
+    }
         CPD_I8D_CASE(16)
         CPD_I8D_CASE(32)
         CPD_I8D_CASE(48)
