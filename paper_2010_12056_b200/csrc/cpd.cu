@@ -84,15 +84,19 @@ struct cpd_ctx {
   double* S_all = nullptr;   // N x R x R
   double* dS_all = nullptr;  // N x R x R
   double* Lp[2] = {nullptr, nullptr};  // packed Cholesky factors (double-buffered)
+  double* Gi[2] = {nullptr, nullptr};  // Γ^{-1} (dense, for the fused update) (double-buffered)
   double* Wb[2] = {nullptr, nullptr};  // PP second-order W (double-buffered)
   int* pf_status = nullptr;            // Cholesky status per buffer
   cudaStream_t st2 = nullptr;          // side stream: Γ factorisation / W ahead of their mode
   cudaEvent_t ev_s = nullptr, ev_pf = nullptr;
   int pf_mode = -1, pf_buf = 0;        // mode whose Γ factor (and W if pf_pp) is being prepared
   bool pf_pp = false;
+  bool pf_fused = false;               // the prefetch formed Γ^{-1} (fused update) rather than L
   double* ws_gram = nullptr; // 2 x 16 x R x R Gram partials
   double* ws_mttv = nullptr; // mTTV K-split partials
   double* st_part = nullptr; // update-stats block partials
+  double* upd_part = nullptr;  // fused-update block partials (3 x kUpdMaxBlocks)
+  double* upd_gpart = nullptr; // fused-update per-CTA Gram partials (kUpdMaxBlocks x 2 R^2)
   unsigned int* st_counter = nullptr;
   double* scal = nullptr;    // device scalars (see SC_*)
   double* partial = nullptr;
@@ -434,6 +438,14 @@ __global__ void gamma_dot_kernel(const double* __restrict__ S_all, int N, int R,
   }
 }
 
+// whether mode n's update runs as the single fused cooperative kernel (update.cu)
+bool use_fused(const cpd_ctx* ctx, int n, bool pp) {
+  const int64_t ro = rows_own(ctx, n);
+  const int blocks = cpd::update_fused_blocks(ro);
+  return ctx->Gi[0] && (ctx->world == 1 || n == ctx->N - 1) &&
+         cpd::update_fused_smem(ctx->R, pp, (int)((ro + blocks - 1) / blocks)) <= 225 * 1024;
+}
+
 // Γ^(m) = ∗_{k≠m} S^(k) depends only on the Grams, so its Cholesky factorisation (and the
 // PP Hadamard sum W^(m) of Eq. 7) can run on a side stream as soon as the previous update
 // has produced its S, overlapping the latency-bound single-CTA factorisation with the
@@ -445,19 +457,27 @@ cpd_status prefetch_solve(cpd_ctx* ctx, int m, bool pp) {
   CU(cudaStreamWaitEvent(ctx->st2, ctx->ev_s, 0));
   // status written straight to status[m]: a prefetch for the next sweep may overwrite it
   // while finish_sweep reads it -- either value is a valid SPD verdict for Γ^(m)
-  CU(cpd::launch_gamma_chol(ctx->S_all, ctx->N, m, ctx->R, ctx->Lp[b], ctx->status + m, ctx->st2));
+  const bool fz = use_fused(ctx, m, pp);
+  if (fz) {
+    // the fused update multiplies by Γ^{-1}: form it directly (Gauss-Jordan, SPD check)
+    CU(cpd::launch_gamma_inverse(ctx->S_all, ctx->N, m, ctx->R, ctx->Gi[b], ctx->status + m, ctx->st2));
+  } else {
+    CU(cpd::launch_gamma_chol(ctx->S_all, ctx->N, m, ctx->R, ctx->Lp[b], ctx->status + m, ctx->st2));
+  }
   if (pp) CU(cpd::launch_pp_w(ctx->S_all, ctx->dS_all, ctx->N, m, ctx->R, ctx->Wb[b], ctx->st2));
   CU(cudaEventRecord(ctx->ev_pf, ctx->st2));
   ctx->pf_buf = b;
   ctx->pf_mode = m;
   ctx->pf_pp = pp;
+  ctx->pf_fused = fz;
   return CPD_OK;
 }
 
 void invalidate_prefetch(cpd_ctx* ctx) { ctx->pf_mode = -1; }
 
 cpd_status acquire_solve(cpd_ctx* ctx, int n, bool pp, int* buf) {
-  if (!(ctx->pf_mode == n && (ctx->pf_pp || !pp))) TRY(prefetch_solve(ctx, n, pp));
+  if (!(ctx->pf_mode == n && (ctx->pf_pp || !pp) && ctx->pf_fused == use_fused(ctx, n, pp)))
+    TRY(prefetch_solve(ctx, n, pp));
   CU(cudaStreamWaitEvent(ctx->st, ctx->ev_pf, 0));
   *buf = ctx->pf_buf;
   ctx->pf_mode = -1;
@@ -474,6 +494,40 @@ cpd_status update_mode(cpd_ctx* ctx, int n, double* Mloc, bool pp) {
   const int64_t ro = rows_own(ctx, n), off = own_off(ctx, n);
   const int64_t rows_full = ext(ctx, n);
   double* Mown = Mloc + off * R;
+  const bool last = n == ctx->N - 1;
+  const bool fused = use_fused(ctx, n, pp);
+  if (fused) {
+    // fused: V term, row solve, dA, statistics, S (and dS) in one cooperative launch
+    int b;
+    TRY(acquire_solve(ctx, n, pp, &b));
+    {
+      PhaseScope ps(ctx, PH_OTHER);
+      if (pp) {
+        ctx->Mlast_src[n] = Mloc;  // persistent M~ buffer: no copy, read on demand
+      } else {
+        ctx->Mlast_src[n] = nullptr;
+        CU(cudaMemcpyAsync(ctx->Mlast[n] + off * R, Mown, sizeof(double) * ro * R, cudaMemcpyDeviceToDevice,
+                           ctx->st));
+      }
+    }
+    {
+      PhaseScope ps(ctx, PH_SOLVE);
+      CU(cpd::launch_update_fused(R, ro, ctx->Gi[b], pp ? ctx->Wb[b] : nullptr, Mown, ctx->A[n] + off * R,
+                                  pp ? ctx->Ap[n] + off * R : nullptr, ctx->dA[n] + off * R, ctx->S_all + n * RR,
+                                  pp ? ctx->dS_all + n * RR : nullptr, ctx->upd_part, ctx->upd_gpart,
+                                  ctx->scal + SC_DA2 + n, ctx->scal + SC_A2 + n, last ? ctx->scal + SC_MA : nullptr,
+                                  ctx->st));
+    }
+    if (last) {
+      TRY(allreduce_lastmode(ctx, pp));
+      PhaseScope ps(ctx, PH_OTHER);
+      cpd::g_launches++;
+      gamma_dot_kernel<<<1, 1024, 0, ctx->st>>>(ctx->S_all, ctx->N, R, ctx->scal + SC_GS);
+      CU(cudaGetLastError());
+    }
+    TRY(prefetch_solve(ctx, (n + 1) % ctx->N, pp));
+    return CPD_OK;
+  }
   if (n < ctx->N - 1 && ctx->world > 1) {
     PhaseScope ps(ctx, PH_OTHER);
     CM(cpd::comm_reduce_scatter(ctx->cm, Mloc, Mown, ro * R, &m_));
@@ -512,7 +566,6 @@ cpd_status update_mode(cpd_ctx* ctx, int n, double* Mloc, bool pp) {
     PhaseScope ps(ctx, PH_HAD);
     const double* base = pp ? ctx->Ap[n] : ctx->Aold[n];
     // dA, ||dA||^2, ||A||^2 (and <M^(N), A^(N)> of Eq. 3 for the last mode) in one pass
-    const bool last = n == ctx->N - 1;
     CU(cpd::launch_update_stats(ctx->A[n], base, ctx->dA[n], last ? Mown : nullptr, rows_full * R, ctx->st_part,
                                 ctx->st_counter, ctx->scal + SC_DA2 + n, ctx->scal + SC_A2 + n,
                                 ctx->scal + SC_MA, ctx->st));
@@ -789,11 +842,14 @@ cpd_status cpd_destroy(cpd_ctx* c) {
   for (int b = 0; b < 2; b++) {
     dfree(c, c->Lp[b]);
     dfree(c, c->Wb[b]);
+    dfree(c, c->Gi[b]);
   }
   if (c->pf_status) cudaFreeAsync(c->pf_status, c->st);
   dfree(c, c->ws_gram);
   dfree(c, c->ws_mttv);
   dfree(c, c->st_part);
+  dfree(c, c->upd_part);
+  dfree(c, c->upd_gpart);
   if (c->st_counter) cudaFreeAsync(c->st_counter, c->st);
   dfree(c, c->scal);
   dfree(c, c->partial);
@@ -938,15 +994,23 @@ cpd_status cp_als_init(cpd_ctx** out, int N, const int64_t* shape, int R, const 
   for (int b2 = 0; b2 < 2; b2++) {
     ITRY(dalloc(ctx, &ctx->Lp[b2], RR + R));
     ITRY(dalloc(ctx, &ctx->Wb[b2], RR));
+    if (R <= cpd::kUpdMaxR) ITRY(dalloc(ctx, &ctx->Gi[b2], RR));
   }
   ICU(cudaMallocAsync((void**)&ctx->pf_status, sizeof(int) * 2, ctx->st));
   ICU(cudaMemsetAsync(ctx->pf_status, 0, sizeof(int) * 2, ctx->st));
-  ICU(cudaStreamCreateWithFlags(&ctx->st2, cudaStreamNonBlocking));
+  {
+    // the side stream (Γ factor / inverse, W) must not queue behind the MTTKRP stream's CTAs
+    int lo = 0, hi = 0;
+    ICU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    ICU(cudaStreamCreateWithPriority(&ctx->st2, cudaStreamNonBlocking, hi));
+  }
   ICU(cudaEventCreateWithFlags(&ctx->ev_s, cudaEventDisableTiming));
   ICU(cudaEventCreateWithFlags(&ctx->ev_pf, cudaEventDisableTiming));
   ITRY(dalloc(ctx, &ctx->ws_gram, 32 * RR));
   ITRY(dalloc(ctx, &ctx->ws_mttv, kMttvWs));
   ITRY(dalloc(ctx, &ctx->st_part, 3 * 64));
+  ITRY(dalloc(ctx, &ctx->upd_part, 3 * cpd::kUpdMaxBlocks));
+  if (R <= cpd::kUpdMaxR) ITRY(dalloc(ctx, &ctx->upd_gpart, (int64_t)cpd::kUpdMaxBlocks * 2 * RR));
   ICU(cudaMallocAsync((void**)&ctx->st_counter, sizeof(unsigned int), ctx->st));
   ICU(cudaMemsetAsync(ctx->st_counter, 0, sizeof(unsigned int), ctx->st));
   ITRY(dalloc(ctx, &ctx->scal, SC_COUNT));

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <atomic>
 
 namespace cpd {
@@ -80,6 +81,13 @@ cudaError_t launch_gram(const double* X, const double* Y1, const double* Y2, int
 // Lp (R(R+1)/2, then the R reciprocal diagonal entries).  status[0] = 0 ok, 1 not SPD.
 cudaError_t launch_gamma_chol(const double* S_all, int N, int n, int R, double* Lp, int* status,
                               cudaStream_t st);
+// Γ^(n) (Eq. 1) and Ginv = Γ^{-1} (dense R x R) by Gauss-Jordan without pivoting (SPD);
+// status[0] = 1 if a pivot is not positive (Γ not SPD).  One CTA, R^2 doubles of shared memory.
+cudaError_t launch_gamma_inverse(const double* S_all, int N, int n, int R, double* Ginv, int* status,
+                                 cudaStream_t st);
+// Ginv = Γ^{-1} = L^{-T} L^{-1} (dense R x R, exactly symmetric) from the packed factor; one CTA,
+// R(R+1)/2 + R + R^2 doubles of shared memory (R <= kUpdMaxR)
+cudaError_t launch_chol_inverse(const double* Lp, int R, double* Ginv, cudaStream_t st);
 // X[i,:] = M[i,:] Γ^{-1} via L (forward + backward substitution per row), rows x R.
 cudaError_t launch_trisolve(const double* Lp, const double* M, int64_t rows, int R, double* X,
                             cudaStream_t st);
@@ -93,5 +101,21 @@ cudaError_t launch_sub(const double* x, const double* y, double* z, int64_t n, c
 cudaError_t launch_update_stats(const double* A, const double* base, double* dA, const double* M, int64_t n,
                                 double* part, unsigned int* counter, double* o_dA2, double* o_A2, double* o_MA,
                                 cudaStream_t st);
+
+// ---- fused factor update (update.cu): V term (PP), row solve, dA, statistics, S and dS ----
+// Cooperative launch (grid sync between the row solves and the Gram reduction); the solve is
+// x = y Ginv with Ginv = Γ^{-1} from launch_chol_inverse ("A = M Γ†").  A holds the
+// old rows on entry (read as a_old for V and, if base == nullptr, as the dA base) and the new
+// rows on exit.  W (PP) may be null (else M += A_old W is written back); dS may be null;
+// S == nullptr skips the Gram phase.
+// R <= kUpdMaxR.
+constexpr int kUpdMaxR = 128;  // Γ^{-1} + the packed factor fit one CTA's shared memory
+constexpr int kUpdMaxBlocks = 64;
+// part: 3 * kUpdMaxBlocks doubles; gpart: kUpdMaxBlocks * 2 * R * R doubles (per-CTA Gram partials)
+size_t update_fused_smem(int R, bool pp, int RB);
+int update_fused_blocks(int64_t rows);
+cudaError_t launch_update_fused(int R, int64_t rows, const double* Ginv, const double* W, double* M, double* A,
+                                const double* base, double* dA, double* S, double* dS, double* part, double* gpart,
+                                double* o_dA2, double* o_A2, double* o_MA, cudaStream_t st);
 
 }  // namespace cpd

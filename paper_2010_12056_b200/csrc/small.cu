@@ -361,6 +361,121 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// --------- Γ^{-1} = L^{-T} L^{-1} from the packed factor (Alg. 1 line 7 "M Γ†") ---------
+// L^{-1} column by column (thread per column: Linv(i,j) = -Σ_{k=j}^{i-1} L(i,k) Linv(k,j) / L(i,i)),
+// then Ginv(a,b) = Σ_{k >= max(a,b)} Linv(k,a) Linv(k,b) in ascending k (exactly symmetric).
+__global__ void __launch_bounds__(256)
+    chol_inverse_kernel(const double* __restrict__ Lp, int R, double* __restrict__ Ginv) {
+  extern __shared__ double sm[];
+  const int total = R * (R + 1) / 2;
+  double* L = sm;                // packed factor
+  const double* iv = sm + total; // reciprocal diagonal
+  double* Li = sm + total + R;   // R x R dense, Linv(i, j) at Li[i * R + j]
+  for (int e = threadIdx.x; e < total + R; e += blockDim.x) L[e] = Lp[e];
+  __syncthreads();
+  for (int j = threadIdx.x; j < R; j += blockDim.x) {
+    for (int i = 0; i < j; i++) Li[i * R + j] = 0.0;
+    Li[j * R + j] = iv[j];
+    for (int i = j + 1; i < R; i++) {
+      double s = 0.0;
+      for (int k = j; k < i; k++) s = fma(L[pk(i, k, R)], Li[k * R + j], s);
+      Li[i * R + j] = -s * iv[i];
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int a = e / R, b = e - a * R;
+    double s = 0.0;
+    for (int k = max(a, b); k < R; k++) s = fma(Li[k * R + a], Li[k * R + b], s);
+    Ginv[e] = s;
+  }
+}
+
+// --------- Γ^{(n)} = ∗_{k≠n} S^(k) (Eq. 1) and Γ^{-1} by in-place Gauss-Jordan (SPD: no pivoting;
+// every pivot is a Schur complement diagonal, > 0 iff Γ is SPD -> status), one CTA ---------
+// Register-blocked: a 16 x 16 thread grid, thread (ti, tj) holds the B x B block of rows
+// ti*B.., columns tj*B.. in registers (B = ceil(R/16) <= 8); per pivot one barrier: the pivot
+// row and column go through double-buffered shared memory.
+template <int B>
+__global__ void __launch_bounds__(256)
+    gamma_inverse_kernel(const double* __restrict__ S_all, int N, int n, int R, double* __restrict__ Ginv,
+                         int* status) {
+  __shared__ double rowk[2][16 * B], colk[2][16 * B];
+  __shared__ int bad;
+  const int64_t RR = (int64_t)R * R;
+  const int ti = threadIdx.x >> 4, tj = threadIdx.x & 15;
+  if (threadIdx.x == 0) bad = 0;
+  double a[B][B];
+#pragma unroll
+  for (int p = 0; p < B; p++)
+#pragma unroll
+    for (int q = 0; q < B; q++) {
+      const int i = ti * B + p, j = tj * B + q;
+      double gv = (i == j) ? 1.0 : 0.0;  // padding: identity (does not touch the R x R block)
+      if (i < R && j < R) {
+        bool first = true;
+        for (int k = 0; k < N; k++) {
+          if (k == n) continue;
+          const double sv = S_all[k * RR + (int64_t)i * R + j];
+          gv = first ? sv : gv * sv;
+          first = false;
+        }
+      }
+      a[p][q] = gv;
+    }
+  for (int k = 0; k < R; k++) {
+    const int buf = k & 1, kb = k / B, ko = k - kb * B;
+    // publish row k and column k (their owners), then one barrier
+    if (ti == kb) {  // static register indexing: select row ko
+#pragma unroll
+      for (int q = 0; q < B; q++) {
+        double v = a[0][q];
+#pragma unroll
+        for (int p = 1; p < B; p++)
+          if (p == ko) v = a[p][q];
+        rowk[buf][tj * B + q] = v;
+      }
+    }
+    if (tj == kb) {
+#pragma unroll
+      for (int p = 0; p < B; p++) {
+        double v = a[p][0];
+#pragma unroll
+        for (int q = 1; q < B; q++)
+          if (q == ko) v = a[p][q];
+        colk[buf][ti * B + p] = v;
+      }
+    }
+    __syncthreads();
+    const double piv = rowk[buf][k];
+    const double inv = __drcp_rn(piv);  // IEEE reciprocal (= 1.0 / piv), no division subroutine
+    if (threadIdx.x == 0 && (!(piv > 0.0) || !isfinite(piv))) bad = 1;
+    double rk[B], ck[B];
+#pragma unroll
+    for (int q = 0; q < B; q++) rk[q] = rowk[buf][tj * B + q] * inv;
+#pragma unroll
+    for (int p = 0; p < B; p++) ck[p] = colk[buf][ti * B + p];
+#pragma unroll
+    for (int p = 0; p < B; p++)
+#pragma unroll
+      for (int q = 0; q < B; q++) {
+        const int i = ti * B + p, j = tj * B + q;
+        if (i == k) a[p][q] = (j == k) ? inv : rk[q];
+        else if (j == k) a[p][q] = -ck[p] * inv;
+        else a[p][q] = fma(-ck[p], rk[q], a[p][q]);
+      }
+  }
+#pragma unroll
+  for (int p = 0; p < B; p++)
+#pragma unroll
+    for (int q = 0; q < B; q++) {
+      const int i = ti * B + p, j = tj * B + q;
+      if (i < R && j < R) Ginv[(int64_t)i * R + j] = a[p][q];
+    }
+  __syncthreads();
+  if (threadIdx.x == 0) status[0] = bad;
+}
+
 // opt a kernel in to the largest dynamic shared memory the device allows
 template <typename K>
 cudaError_t opt_in_smem(K kern) {
@@ -414,6 +529,37 @@ cudaError_t launch_gamma_chol(const double* S_all, int N, int n, int R, double* 
   }
   g_launches++;
   gamma_chol_kernel<<<1, CH_THREADS, smem, st>>>(S_all, N, n, R, Lp, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gamma_inverse(const double* S_all, int N, int n, int R, double* Ginv, int* status,
+                                 cudaStream_t st) {
+  g_launches++;
+  const int B = (R + 15) / 16;
+  switch (B) {
+    case 1: gamma_inverse_kernel<1><<<1, 256, 0, st>>>(S_all, N, n, R, Ginv, status); break;
+    case 2: gamma_inverse_kernel<2><<<1, 256, 0, st>>>(S_all, N, n, R, Ginv, status); break;
+    case 3: gamma_inverse_kernel<3><<<1, 256, 0, st>>>(S_all, N, n, R, Ginv, status); break;
+    case 4: gamma_inverse_kernel<4><<<1, 256, 0, st>>>(S_all, N, n, R, Ginv, status); break;
+    case 5: gamma_inverse_kernel<5><<<1, 256, 0, st>>>(S_all, N, n, R, Ginv, status); break;
+    case 6: gamma_inverse_kernel<6><<<1, 256, 0, st>>>(S_all, N, n, R, Ginv, status); break;
+    case 7: gamma_inverse_kernel<7><<<1, 256, 0, st>>>(S_all, N, n, R, Ginv, status); break;
+    case 8: gamma_inverse_kernel<8><<<1, 256, 0, st>>>(S_all, N, n, R, Ginv, status); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_chol_inverse(const double* Lp, int R, double* Ginv, cudaStream_t st) {
+  const size_t smem = sizeof(double) * ((size_t)R * (R + 1) / 2 + R + (size_t)R * R);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = opt_in_smem(chol_inverse_kernel);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  g_launches++;
+  chol_inverse_kernel<<<1, 256, smem, st>>>(Lp, R, Ginv);
   return cudaGetLastError();
 }
 

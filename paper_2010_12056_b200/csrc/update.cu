@@ -1,0 +1,230 @@
+// Fused factor update of one mode (Alg. 1 lines 7-8; Eq. 1; PP:
+// Eqs. 5/7/8 P:386-409): one cooperative launch instead of V-term GEMM + row solve +
+// statistics + Gram partials + Gram reduce (five latency-bound launches).
+//
+// Phase 1 (warp per row, lanes own columns c = lane + 32 u):
+//   m   = M[i]  (+ a_old W  for PP: V^(n) = A^(n) W^(n), Eq. 7, with the pre-update row)
+//   x   = m Γ^{-1} ("M Γ†"), Γ^{-1} = L^{-T} L^{-1} formed from the Cholesky factor on the
+//         side stream (launch_chol_inverse) while the MTTKRP streamed; a mat-vec per row,
+//         y_k broadcast by shuffles, independent FMAs per lane
+//   A[i] = x, dA[i] = x - base[i] (base = the row before the update, or A_p in PP),
+//   partial sums of |dA|^2, |A|^2 and <m, x> (Eq. 3 needs <M^(N), A^(N)>) per CTA.
+// grid.sync()
+// Phase 2: S = A^T A and dS = A^T dA (Eq. 8) over all rows, one output element per
+//   thread, rows in ascending order (deterministic; S exactly symmetric); CTA 0 reduces the
+//   statistics partials in CTA order.
+#include <cooperative_groups.h>
+
+#include "kernels.h"
+
+namespace cpd {
+namespace {
+
+namespace cg = cooperative_groups;
+
+constexpr int UPD_THREADS = 256;
+
+
+// dst[0..n) = src[0..n): 8 independent loads in flight per thread
+__device__ __forceinline__ void fill_smem(double* dst, const double* __restrict__ src, int n, int tid) {
+  int e = tid;
+  for (; e + 7 * UPD_THREADS < n; e += 8 * UPD_THREADS) {
+    double v[8];
+#pragma unroll
+    for (int q = 0; q < 8; q++) v[q] = __ldg(src + e + q * UPD_THREADS);
+#pragma unroll
+    for (int q = 0; q < 8; q++) dst[e + q * UPD_THREADS] = v[q];
+  }
+  for (; e < n; e += UPD_THREADS) dst[e] = __ldg(src + e);
+}
+
+template <int U>
+__global__ void __launch_bounds__(UPD_THREADS)
+    update_fused_kernel(int R, int64_t rows, const double* __restrict__ Gi, const double* __restrict__ W,
+                        double* __restrict__ M, double* __restrict__ A, const double* __restrict__ base,
+                        double* __restrict__ dA, double* __restrict__ S, double* __restrict__ dS,
+                        double* __restrict__ part, double* __restrict__ gpart, int RB,
+                        double* __restrict__ o_dA2, double* __restrict__ o_A2, double* __restrict__ o_MA) {
+  extern __shared__ double sm[];
+  double* G = sm;                 // R x R: Γ^{-1}
+  double* Ws = sm + R * R;        // R x R (PP only)
+  double* Xs = Ws + (W ? R * R : 0);  // RB x R: this CTA's new rows
+  double* Ds = Xs + RB * R;           // RB x R: their dA
+  __shared__ double red[3][UPD_THREADS / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  fill_smem(G, Gi, R * R, tid);
+  if (W) fill_smem(Ws, W, R * R, tid);
+  __syncthreads();
+
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  // this CTA owns rows [r0, r0 + RB); warp w solves rows r0 + w, r0 + w + 8, ...
+  const int64_t r0 = (int64_t)blockIdx.x * RB;
+  const int nrows = (int)max((int64_t)0, min((int64_t)RB, rows - r0));
+  for (int lr = warp; lr < nrows; lr += UPD_THREADS / 32) {
+    const int64_t i = r0 + lr;
+    double y[U], ao[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int c = lane + 32 * u;
+      y[u] = c < R ? M[i * R + c] : 0.0;
+      ao[u] = c < R ? A[i * R + c] : 0.0;
+    }
+    if (W) {  // y += a_old W
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) v[u] = 0.0;
+      for (int k = 0; k < R; k++) {
+        double ak = __shfl_sync(0xffffffffu, ao[0], k & 31);
+#pragma unroll
+        for (int u = 1; u < U; u++) {
+          const double t = __shfl_sync(0xffffffffu, ao[u], k & 31);
+          if ((k >> 5) == u) ak = t;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          const int c = lane + 32 * u;
+          if (c < R) v[u] = fma(ak, Ws[k * R + c], v[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        y[u] += v[u];
+        const int c = lane + 32 * u;
+        if (c < R) M[i * R + c] = y[u];  // keep M~ = M_p + ΣU + V readable (cpd_get_last_mttkrp)
+      }
+    }
+    double mm[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) mm[u] = y[u];
+    // x = y Γ^{-1}: lanes own output columns, y_k broadcast by shuffles (independent FMAs)
+    double x[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) x[u] = 0.0;
+    for (int k = 0; k < R; k++) {
+      double yk = __shfl_sync(0xffffffffu, y[0], k & 31);
+#pragma unroll
+      for (int u = 1; u < U; u++) {
+        const double t = __shfl_sync(0xffffffffu, y[u], k & 31);
+        if ((k >> 5) == u) yk = t;
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int c = lane + 32 * u;
+        if (c < R) x[u] = fma(yk, G[k * R + c], x[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) y[u] = x[u];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int c = lane + 32 * u;
+      if (c < R) {
+        const double b = base ? base[i * R + c] : ao[u];
+        const double d = y[u] - b;
+        A[i * R + c] = y[u];
+        dA[i * R + c] = d;
+        Xs[lr * R + c] = y[u];
+        Ds[lr * R + c] = d;
+        s0 = fma(d, d, s0);
+        s1 = fma(y[u], y[u], s1);
+        s2 = fma(mm[u], y[u], s2);
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  }
+  if (lane == 0) {
+    red[0][warp] = s0;
+    red[1][warp] = s1;
+    red[2][warp] = s2;
+  }
+  __syncthreads();
+  if (tid < 3) {
+    double s = red[tid][0];
+    for (int w = 1; w < UPD_THREADS / 32; w++) s += red[tid][w];
+    part[blockIdx.x * 3 + tid] = s;
+  }
+  // phase 2a: this CTA's partial Grams over its rows (ascending), from shared memory
+  const int64_t RR = (int64_t)R * R;
+  const int64_t nout = S ? (dS ? 2 * RR : RR) : 0;
+  __syncthreads();
+  for (int64_t e = tid; e < nout; e += UPD_THREADS) {
+    const bool second = e >= RR;
+    const int64_t f = second ? e - RR : e;
+    const int a = (int)(f / R), b = (int)(f - (int64_t)a * R);
+    const double* Y = second ? Ds : Xs;
+    double acc = 0.0;
+    for (int r = 0; r < nrows; r++) acc = fma(Xs[r * R + a], Y[r * R + b], acc);
+    gpart[(int64_t)blockIdx.x * nout + e] = acc;
+  }
+  cg::this_grid().sync();
+  // phase 2b: S, dS = Σ over CTAs in CTA order (deterministic; S exactly symmetric)
+  for (int64_t e = (int64_t)blockIdx.x * UPD_THREADS + tid; e < nout; e += (int64_t)gridDim.x * UPD_THREADS) {
+    // CTA partials in CTA order; 16 independent loads in flight per batch
+    double acc = gpart[e];
+    unsigned c = 1;
+    for (; c + 16 <= gridDim.x; c += 16) {
+      double v[16];
+#pragma unroll
+      for (int q = 0; q < 16; q++) v[q] = gpart[(int64_t)(c + q) * nout + e];
+#pragma unroll
+      for (int q = 0; q < 16; q++) acc += v[q];
+    }
+    for (; c < gridDim.x; c++) acc += gpart[(int64_t)c * nout + e];
+    if (e < RR) S[e] = acc;
+    else dS[e - RR] = acc;
+  }
+  if (blockIdx.x == 0 && tid < 3) {
+    double s = part[tid];
+    for (unsigned b = 1; b < gridDim.x; b++) s += part[b * 3 + tid];
+    if (tid == 0) *o_dA2 = s;
+    if (tid == 1) *o_A2 = s;
+    if (tid == 2 && o_MA) *o_MA = s;
+  }
+}
+
+template <int U>
+cudaError_t coop_launch(int blocks, size_t smem, void** args, cudaStream_t st) {
+  static bool attr = false;  // per instantiation
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(update_fused_kernel<U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         227 * 1024 - 2048);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  g_launches++;
+  return cudaLaunchCooperativeKernel((void*)update_fused_kernel<U>, blocks, UPD_THREADS, args, smem, st);
+}
+
+}  // namespace
+
+size_t update_fused_smem(int R, bool pp, int RB) {
+  // Γ^{-1}, W (PP), this CTA's rows and their dA
+  return sizeof(double) * ((size_t)R * R + (pp ? (size_t)R * R : 0) + 2 * (size_t)RB * R);
+}
+
+int update_fused_blocks(int64_t rows) { return (int)std::min<int64_t>(kUpdMaxBlocks, (rows + 7) / 8); }
+
+cudaError_t launch_update_fused(int R, int64_t rows, const double* Ginv, const double* W, double* M, double* A,
+                                const double* base, double* dA, double* S, double* dS, double* part, double* gpart,
+                                double* o_dA2, double* o_A2, double* o_MA, cudaStream_t st) {
+  if (R > kUpdMaxR || rows <= 0) return cudaErrorInvalidValue;
+  const int blocks = update_fused_blocks(rows);
+  int RB = (int)((rows + blocks - 1) / blocks);
+  const size_t smem = update_fused_smem(R, W != nullptr, RB);
+  if (smem > 227 * 1024 - 2048) return cudaErrorInvalidValue;
+  void* args[] = {&R, &rows, &Ginv, &W, &M, &A, &base, &dA, &S, &dS, &part, &gpart, &RB, &o_dA2, &o_A2, &o_MA};
+  switch ((R + 31) / 32) {
+    case 1: return coop_launch<1>(blocks, smem, args, st);
+    case 2: return coop_launch<2>(blocks, smem, args, st);
+    case 3: return coop_launch<3>(blocks, smem, args, st);
+    case 4: return coop_launch<4>(blocks, smem, args, st);
+    case 5: return coop_launch<5>(blocks, smem, args, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace cpd
