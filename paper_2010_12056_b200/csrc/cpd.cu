@@ -280,8 +280,15 @@ cpd_status ttm(cpd_ctx* ctx, int j, double* out) {
   for (int m = j + 1; m < ctx->N; m++) post *= ext(ctx, m);
   PhaseScope ps(ctx, PH_TTM);
   if (ctx->engine != CPD_ENGINE_DMMA && ext(ctx, j) <= cpd::kMaxKI8) {
+    cpd::DigitView dv;
+    if (ctx->Td) {
+      dv.planes = ctx->Td;
+      dv.w = ext(ctx, ctx->N - 1);
+      dv.ipad = cpd::digit_inner_pad(dv.w);
+      dv.plane_stride = cpd::digit_plane_bytes(ctx->T_elems, dv.w);
+    }
     CU(cpd::launch_ttm_i8(ctx->T, pre, ext(ctx, j), post, ctx->A[j], ctx->R, out, 0, ctx->texp, ctx->ws_i8,
-                          ctx->ws_i8_bytes, ctx->st, ctx->Td));
+                          ctx->ws_i8_bytes, ctx->st, ctx->Td ? &dv : nullptr));
   } else {
     CU(cpd::launch_ttm(ctx->T, pre, ext(ctx, j), post, ctx->A[j], ctx->R, out, 0, ctx->st));
   }
@@ -767,9 +774,10 @@ cpd_status prepare_tensor(cpd_ctx* ctx) {
       ctx->engine = CPD_ENGINE_INT8_CONVERT;
       // T's digit planes once (7 bytes per element): every first-level TTM then streams them
       // instead of converting T; without the memory the TTM converts T on the fly
-      if (ctx->Td || cudaMallocAsync((void**)&ctx->Td, (size_t)7 * cpd::digit_plane_stride(ctx->T_elems),
+      const int64_t w = ext(ctx, N - 1);
+      if (ctx->Td || cudaMallocAsync((void**)&ctx->Td, (size_t)7 * cpd::digit_plane_bytes(ctx->T_elems, w),
                                      ctx->st) == cudaSuccess) {
-        CU(cpd::launch_slice_digits(ctx->T, ctx->T_elems, ctx->texp, ctx->Td, ctx->st));
+        CU(cpd::launch_slice_digits(ctx->T, ctx->T_elems, w, ctx->texp, ctx->Td, ctx->st));
         ctx->engine = CPD_ENGINE_INT8_DIGITS;
       } else {
         cudaGetLastError();
@@ -1401,13 +1409,39 @@ cpd_status cpd_ttm_i8(const double* T_dev, int64_t pre, int64_t K, int64_t post,
   if (e == cudaSuccess) e = cudaMallocAsync((void**)&ex, sizeof(int), st);
   if (e == cudaSuccess) e = cpd::launch_absmax_exp(T_dev, pre * K * post, part, ex, st);
   uint8_t* Td = nullptr;
+  cpd::DigitView dv;
   if (e == cudaSuccess && use_digits) {
-    e = cudaMallocAsync((void**)&Td, (size_t)7 * cpd::digit_plane_stride(pre * K * post), st);
-    if (e == cudaSuccess) e = cpd::launch_slice_digits(T_dev, pre * K * post, ex, Td, st);
+    // T viewed as [pre, K, post]: innermost extent post (or K when post == 1)
+    dv.w = post > 1 ? post : K;
+    dv.ipad = cpd::digit_inner_pad(dv.w);
+    dv.plane_stride = cpd::digit_plane_bytes(pre * K * post, dv.w);
+    e = cudaMallocAsync((void**)&Td, (size_t)7 * dv.plane_stride, st);
+    if (e == cudaSuccess) e = cpd::launch_slice_digits(T_dev, pre * K * post, dv.w, ex, Td, st);
+    dv.planes = Td;
   }
-  if (e == cudaSuccess) e = cpd::launch_ttm_i8(T_dev, pre, K, post, A_dev, R, out_dev, 0, ex, ws, wsb, st, Td);
+  if (e == cudaSuccess)
+    e = cpd::launch_ttm_i8(T_dev, pre, K, post, A_dev, R, out_dev, 0, ex, ws, wsb, st, Td ? &dv : nullptr);
   if (Td) cudaFreeAsync(Td, st);
   if (ws) cudaFreeAsync(ws, st);
+  if (part) cudaFreeAsync(part, st);
+  if (ex) cudaFreeAsync(ex, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    g_init_error = cudaGetErrorString(e);
+    return CPD_ERR_CUDA;
+  }
+  return CPD_OK;
+}
+
+// debug: T's digit planes (7 x digit_plane_bytes(n, w) bytes) into out_dev (device)
+cpd_status cpd_debug_slice_digits(const double* T_dev, int64_t n, int64_t w, uint8_t* out_dev, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  double* part = nullptr;
+  int* ex = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&part, sizeof(double) * cpd::kNormBlocks, st);
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&ex, sizeof(int), st);
+  if (e == cudaSuccess) e = cpd::launch_absmax_exp(T_dev, n, part, ex, st);
+  if (e == cudaSuccess) e = cpd::launch_slice_digits(T_dev, n, w, ex, out_dev, st);
   if (part) cudaFreeAsync(part, st);
   if (ex) cudaFreeAsync(ex, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);

@@ -24,15 +24,23 @@ cudaError_t launch_ttm(const double* X, int64_t pre, int64_t K, int64_t post, co
 // K <= kMaxKI8 (int32 accumulators), ncols <= 256.
 constexpr int64_t kMaxKI8 = 16384;
 size_t ttm_i8_workspace_bytes(int64_t K, int ncols);
-// Xd (may be null): X's 7 int8 digit planes (launch_slice_digits, 7 bytes per element, plane-major);
-// when given and ttm_i8_digits_ok(pre, K, post), the TTM streams them instead of converting X.
+// X's 7 int8 digit planes (launch_slice_digits): X viewed as [n / w, w] (w = innermost extent),
+// plane a of element (row, c) at planes[a * plane_stride + row * ipad + c], ipad = digit_inner_pad(w)
+struct DigitView {
+  const uint8_t* planes = nullptr;
+  int64_t w = 0, ipad = 0, plane_stride = 0;
+};
+inline int64_t digit_inner_pad(int64_t w) { return (w + 15) / 16 * 16; }
+// dv (may be null): when its layout serves this TTM view, the TTM streams the digit planes
+// instead of converting X
 cudaError_t launch_ttm_i8(const double* X, int64_t pre, int64_t K, int64_t post, const double* B, int ncols,
                           double* out, int beta, const int* Xexp, void* ws, size_t ws_bytes, cudaStream_t st,
-                          const uint8_t* Xd = nullptr);
-bool ttm_i8_digits_ok(int64_t pre, int64_t K, int64_t post);
-// bytes between digit planes for n elements (the planes buffer holds 7 * digit_plane_stride(n) bytes)
+                          const DigitView* dv = nullptr);
+// bytes between digit planes (a multiple of 64); the planes buffer holds 7 * digit_plane_bytes(n, w)
 inline int64_t digit_plane_stride(int64_t n) { return (n + 63) / 64 * 64; }
-cudaError_t launch_slice_digits(const double* X, int64_t n, const int* Xexp, uint8_t* planes, cudaStream_t st);
+inline int64_t digit_plane_bytes(int64_t n, int64_t w) { return digit_plane_stride(n / w * digit_inner_pad(w)); }
+cudaError_t launch_slice_digits(const double* X, int64_t n, int64_t w, const int* Xexp, uint8_t* planes,
+                                cudaStream_t st);
 // *e_out = e with 2^e > max|x_i| (0 if x == 0), *max_out = max|x_i| if given; partial: kNormBlocks doubles
 cudaError_t launch_absmax_exp(const double* x, int64_t n, double* partial, int* e_out, cudaStream_t st,
                               double* max_out = nullptr);

@@ -143,6 +143,9 @@ struct Geo {
   int ncols, Rn, Rp, ntn;   // columns, columns per N tile, padded, number of N tiles
   int64_t nmt, ntiles;      // M tiles, total tiles
   int nkc;                  // K32 steps
+  // padded-digit MC tiling (D_MCP): rows (p, mo, m), m < w in blocks of 128
+  int64_t w = 0, Mo = 0, ipad = 0;
+  int wb = 0;
 };
 
 // 128-byte swizzle of the TMA KC boxes: 16-byte chunk c of row r is stored at c ^ (r % 8)
@@ -650,8 +653,10 @@ cudaError_t dispatch_i8(int L, int grid, const double* X, const Geo& g, const ui
 // Warps: 0 TMA producer, 1 TMEM allocator + MMA issuer, 2-9 epilogue (two per lane quarter).
 // ============================================================================================
 // loader layouts of the digit kernel: KC, or MC with an MN atom of 128 / 64 / 32 bytes
-// (post % 128 == 0, or post == 64 / 32 with 2 / 4 consecutive prefix indices per tile)
-enum { D_KC = 0, D_MC128 = 1, D_MC64 = 2, D_MC32 = 3 };
+// (post % 128 == 0, or post == 64 / 32 with 2 / 4 consecutive prefix indices per tile), or
+// D_MCP: MC over padded digit rows (innermost extent w not a multiple of 16, or post % 128 != 0):
+// tiles (p, mo, 128-block of the innermost mode), 5-D map {w, Mo, K, pre, 7}
+enum { D_KC = 0, D_MC128 = 1, D_MC64 = 2, D_MC32 = 3, D_MCP = 4 };
 constexpr int kStagesD = 5;
 constexpr int kEpiWarps = 16;                        // 4 per TMEM lane quarter
 constexpr int kThreadsD = 32 * (2 + kEpiWarps);
@@ -673,7 +678,7 @@ __global__ void __launch_bounds__(kThreadsD, 1)
   constexpr int NDS = kStagesD;
   // TMEM accumulator buffers: 7 diagonals x Rp columns each; two (ping-pong) when they fit
   constexpr int NACC = (2 * kND * Rp <= 512 && kND * Rp <= 256) ? 2 : 1;
-  constexpr int MCW = L == D_MC128 ? 128 : L == D_MC64 ? 64 : 32;  // MN atom bytes
+  constexpr int MCW = (L == D_MC128 || L == D_MCP) ? 128 : L == D_MC64 ? 64 : 32;  // MN atom bytes
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NDS * kDStage);
   const uint32_t full0 = su32(bars), empty0 = su32(bars + NDS);
@@ -714,10 +719,18 @@ __global__ void __launch_bounds__(kThreadsD, 1)
       uint32_t par = 1;
       for (int64_t tt = 0; tt < my_tiles; tt++) {
         const int64_t tile = blockIdx.x + tt * gridDim.x;
-        const int64_t i0 = (tile / g.ntn) * kBM;
+        const int64_t mt = tile / g.ntn;
+        const int64_t i0 = mt * kBM;
         const int nt = (int)(tile % g.ntn);
-        int p = 0, m0 = 0;
-        if constexpr (L != D_KC) {
+        int p = 0, m0 = 0, mo = 0;
+        if constexpr (L == D_MCP) {
+          // the last block of the innermost mode is shifted back to end at w: boxes never
+          // overhang the tensor edge (an overhanging MN-major box corrupted loads on sm_100a)
+          const int64_t pm = mt / g.wb;
+          m0 = (int)min((mt - pm * g.wb) * kBM, g.ipad - kBM);  // 16-byte aligned start
+          p = (int)(pm / g.Mo);
+          mo = (int)(pm - (int64_t)p * g.Mo);
+        } else if constexpr (L != D_KC) {
           p = (int)(i0 / g.post);
           m0 = (int)(i0 - (int64_t)p * g.post);
         }
@@ -730,6 +743,18 @@ __global__ void __launch_bounds__(kThreadsD, 1)
                 "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
                 "%4}], [%5];" ::"r"(st),
                 "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(kc * 32), "r"((int)i0), "r"(0), "r"(bar)
+                : "memory");
+          } else if (L == D_MCP && g.Mo == 1) {
+            asm volatile(
+                "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+                "%4, %5}], [%6];" ::"r"(st),
+                "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(m0), "r"(kc * 32), "r"(p), "r"(0), "r"(bar)
+                : "memory");
+          } else if constexpr (L == D_MCP) {
+            asm volatile(
+                "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+                "%4, %5, %6}], [%7];" ::"r"(st),
+                "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(m0), "r"(mo), "r"(kc * 32), "r"(p), "r"(0), "r"(bar)
                 : "memory");
           } else {
             asm volatile(
@@ -801,7 +826,16 @@ __global__ void __launch_bounds__(kThreadsD, 1)
     constexpr int CQ = (Rp / 4 + 7) / 8 * 8;  // columns per epilogue warp, a multiple of 8
     for (int64_t tt = 0; tt < my_tiles; tt++) {
       const int64_t tile = blockIdx.x + tt * gridDim.x;
-      const int64_t i = (tile / g.ntn) * kBM + r;
+      const int64_t mt = tile / g.ntn;
+      int64_t i = mt * kBM + r;
+      bool row_ok = i < g.Mrows;
+      if constexpr (L == D_MCP) {
+        const int64_t pm = mt / g.wb;
+        const int64_t mb0 = (mt - pm * g.wb) * kBM;      // first row this tile owns
+        const int64_t m = min(mb0, g.ipad - kBM) + r;    // row held in TMEM lane r
+        i = pm * g.w + m;
+        row_ok = m >= mb0 && m < g.w;                     // overlap rows belong to the previous block
+      }
       const int nt = (int)(tile % g.ntn);
       const int n0 = nt * g.Rn;
       const int ab = NACC == 2 ? (int)(tt & 1) : 0;
@@ -822,7 +856,7 @@ __global__ void __launch_bounds__(kThreadsD, 1)
         }
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         const int cmax = min(8, min(g.Rn - c0, g.ncols - n0 - c0));
-        if (i < g.Mrows && cmax > 0) {
+        if (row_ok && cmax > 0) {
           double v[8];
 #pragma unroll
           for (int j = 0; j < 8; j++) {
@@ -857,70 +891,88 @@ __global__ void __launch_bounds__(kThreadsD, 1)
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
-// digit planes of X: plane a, element e = byte a of (rint(X[e] 2^(54-eX)) + bias) xor 0x80,
-// stored at planes[a * ps + e] (ps = digit_plane_stride(n), a multiple of 64)
-__global__ void slice_digits_kernel(const double* __restrict__ X, int64_t n, int64_t ps, const int* __restrict__ Xexp,
-                                    uint8_t* __restrict__ planes) {
+// digit planes of X viewed as [n / w, w]: plane a of element (row, c) = byte a of
+// (rint(X 2^(54-eX)) + bias) xor 0x80, stored at planes[a * ps + row * ipad + c]
+// (ipad = digit_inner_pad(w); the pad columns stay zero = digit value 0)
+__global__ void slice_digits_kernel(const double* __restrict__ X, int64_t n, int64_t w, int64_t ipad, int64_t ps,
+                                    const int* __restrict__ Xexp, uint8_t* __restrict__ planes, int slow) {
   const double scale = pow2(54 - *Xexp);
-  const int64_t n16 = n / 16;
-  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n16; b += (int64_t)gridDim.x * blockDim.x) {
-    const double2* src = reinterpret_cast<const double2*>(X + 16 * b);
-    uint32_t w[7][4];
+  if (ipad == w && (n % 16) == 0 && !slow) {
+    const int64_t n16 = n / 16;
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n16;
+         b += (int64_t)gridDim.x * blockDim.x) {
+      const double2* src = reinterpret_cast<const double2*>(X + 16 * b);
+      uint32_t wd[7][4];
 #pragma unroll
-    for (int g4 = 0; g4 < 4; g4++) {
-      uint32_t lo[4], hi[4];
+      for (int g4 = 0; g4 < 4; g4++) {
+        uint32_t lo[4], hi[4];
 #pragma unroll
-      for (int q = 0; q < 2; q++) {
-        const double2 v = __ldg(src + 2 * g4 + q);
-        const long long a0 = __double2ll_rn(v.x * scale) + (long long)kBias;
-        const long long a1 = __double2ll_rn(v.y * scale) + (long long)kBias;
-        lo[2 * q] = (uint32_t)a0;
-        hi[2 * q] = (uint32_t)((unsigned long long)a0 >> 32);
-        lo[2 * q + 1] = (uint32_t)a1;
-        hi[2 * q + 1] = (uint32_t)((unsigned long long)a1 >> 32);
+        for (int q = 0; q < 2; q++) {
+          const double2 v = __ldg(src + 2 * g4 + q);
+          const long long a0 = __double2ll_rn(v.x * scale) + (long long)kBias;
+          const long long a1 = __double2ll_rn(v.y * scale) + (long long)kBias;
+          lo[2 * q] = (uint32_t)a0;
+          hi[2 * q] = (uint32_t)((unsigned long long)a0 >> 32);
+          lo[2 * q + 1] = (uint32_t)a1;
+          hi[2 * q + 1] = (uint32_t)((unsigned long long)a1 >> 32);
+        }
+        uint32_t o[4];
+        transpose4(lo[0], lo[1], lo[2], lo[3], o);
+#pragma unroll
+        for (int a = 0; a < 4; a++) wd[a][g4] = o[a] ^ 0x80808080u;
+        transpose4(hi[0], hi[1], hi[2], hi[3], o);
+#pragma unroll
+        for (int a = 0; a < 3; a++) wd[4 + a][g4] = o[a] ^ 0x80808080u;
       }
-      uint32_t o[4];
-      transpose4(lo[0], lo[1], lo[2], lo[3], o);
 #pragma unroll
-      for (int a = 0; a < 4; a++) w[a][g4] = o[a] ^ 0x80808080u;
-      transpose4(hi[0], hi[1], hi[2], hi[3], o);
-#pragma unroll
-      for (int a = 0; a < 3; a++) w[4 + a][g4] = o[a] ^ 0x80808080u;
+      for (int a = 0; a < kND; a++)
+        *reinterpret_cast<uint4*>(planes + a * ps + 16 * b) = make_uint4(wd[a][0], wd[a][1], wd[a][2], wd[a][3]);
     }
-#pragma unroll
-    for (int a = 0; a < kND; a++)
-      *reinterpret_cast<uint4*>(planes + a * ps + 16 * b) = make_uint4(w[a][0], w[a][1], w[a][2], w[a][3]);
+    return;
   }
-  if (blockIdx.x == 0) {
-    for (int64_t e = 16 * n16 + threadIdx.x; e < n; e += blockDim.x) {
-      const unsigned long long u = (unsigned long long)(__double2ll_rn(X[e] * scale) + (long long)kBias);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = e / w, c = e - row * w;
+    const unsigned long long u = (unsigned long long)(__double2ll_rn(X[e] * scale) + (long long)kBias);
 #pragma unroll
-      for (int a = 0; a < kND; a++) planes[a * ps + e] = (uint8_t)(((u >> (8 * a)) & 0xFF) ^ 0x80);
-    }
+    for (int a = 0; a < kND; a++) planes[a * ps + row * ipad + c] = (uint8_t)(((u >> (8 * a)) & 0xFF) ^ 0x80);
   }
 }
 
-bool make_tmap_digits(int L, const uint8_t* Xd, const Geo& g, CUtensorMap* tm) {
+bool make_tmap_digits(int L, const DigitView& dv, const Geo& g, CUtensorMap* tm) {
   auto enc = tensor_map_encoder();
   if (!enc) return false;
-  const cuuint64_t numel = (cuuint64_t)digit_plane_stride(g.Mrows * g.K);  // plane stride
+  uint8_t* base = const_cast<uint8_t*>(dv.planes);
+  const cuuint64_t ps = (cuuint64_t)dv.plane_stride;
   CUresult r;
-  if (L == D_KC) {
+  if (L == D_KC) {  // rows of ipad bytes (K = w)
     cuuint64_t dims[3] = {(cuuint64_t)g.K, (cuuint64_t)g.Mrows, (cuuint64_t)kND};
-    cuuint64_t strides[2] = {(cuuint64_t)g.K, numel};
+    cuuint64_t strides[2] = {(cuuint64_t)dv.ipad, ps};
     cuuint32_t box[3] = {32, (cuuint32_t)kBM, (cuuint32_t)kND}, es[3] = {1, 1, 1};
-    r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(Xd), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  } else {
+    r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else if (L == D_MCP) {
+    if (g.Mo == 1) {
+      cuuint64_t dims[4] = {(cuuint64_t)dv.ipad, (cuuint64_t)g.K, (cuuint64_t)g.pre, (cuuint64_t)kND};
+      cuuint64_t strides[3] = {(cuuint64_t)dv.ipad, (cuuint64_t)dv.ipad * g.K, ps};
+      cuuint32_t box[4] = {(cuuint32_t)kBM, 32, 1, (cuuint32_t)kND}, es[4] = {1, 1, 1, 1};
+      r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+      cuuint64_t dims[5] = {(cuuint64_t)dv.ipad, (cuuint64_t)g.Mo, (cuuint64_t)g.K, (cuuint64_t)g.pre, (cuuint64_t)kND};
+      cuuint64_t strides[4] = {(cuuint64_t)dv.ipad, (cuuint64_t)dv.ipad * g.Mo, (cuuint64_t)dv.ipad * g.Mo * g.K, ps};
+      cuuint32_t box[5] = {(cuuint32_t)kBM, 1, 32, 1, (cuuint32_t)kND}, es[5] = {1, 1, 1, 1, 1};
+      r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
+  } else {  // unpadded: post contiguous
     const int mcw = L == D_MC128 ? 128 : L == D_MC64 ? 64 : 32;
     cuuint64_t dims[4] = {(cuuint64_t)g.post, (cuuint64_t)g.K, (cuuint64_t)g.pre, (cuuint64_t)kND};
-    cuuint64_t strides[3] = {(cuuint64_t)g.post, (cuuint64_t)g.K * g.post, numel};
+    cuuint64_t strides[3] = {(cuuint64_t)g.post, (cuuint64_t)g.K * g.post, ps};
     cuuint32_t box[4] = {(cuuint32_t)mcw, 32, (cuuint32_t)(kBM / mcw), (cuuint32_t)kND}, es[4] = {1, 1, 1, 1};
     const CUtensorMapSwizzle sw =
         mcw == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : mcw == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
-    r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(Xd), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   }
   return r == CUDA_SUCCESS;
 }
@@ -954,22 +1006,36 @@ cudaError_t launch_absmax_exp(const double* x, int64_t n, double* partial, int* 
   return cudaGetLastError();
 }
 
-cudaError_t launch_slice_digits(const double* X, int64_t n, const int* Xexp, uint8_t* planes, cudaStream_t st) {
+cudaError_t launch_slice_digits(const double* X, int64_t n, int64_t w, const int* Xexp, uint8_t* planes,
+                                cudaStream_t st) {
+  if (((uintptr_t)X % 16) != 0 || w <= 0 || n % w != 0) return cudaErrorInvalidValue;
+  const int64_t ipad = digit_inner_pad(w), ps = digit_plane_bytes(n, w);
+  if (ipad != w) {
+    cudaError_t e = cudaMemsetAsync(planes, 0, (size_t)kND * ps, st);
+    if (e != cudaSuccess) return e;
+  }
   g_launches++;
-  if (((uintptr_t)X % 16) != 0) return cudaErrorInvalidValue;
-  slice_digits_kernel<<<148 * 8, 256, 0, st>>>(X, n, digit_plane_stride(n), Xexp, planes);
+  static const int slow = getenv("CPD_SLOW_SLICE") ? 1 : 0;
+  slice_digits_kernel<<<148 * 8, 256, 0, st>>>(X, n, w, ipad, ps, Xexp, planes, slow);
   return cudaGetLastError();
 }
 
-bool ttm_i8_digits_ok(int64_t pre, int64_t K, int64_t post) {
-  if (post == 1) return (K % 16) == 0;
-  if ((post % kBM) == 0) return true;
-  return (post == 64 && pre % 2 == 0) || (post == 32 && pre % 4 == 0);
+// digit-kernel layout for a TTM view [pre, K, post] of a tensor whose digit planes have
+// innermost extent w (padded to ipad); -1 if none applies
+int digit_layout(int64_t pre, int64_t K, int64_t post, int64_t w, int64_t ipad) {
+  if (post == 1) return K == w ? D_KC : -1;
+  if (post % w != 0) return -1;
+  if (ipad == w) {
+    if ((post % kBM) == 0) return D_MC128;
+    if (post == 64 && pre % 2 == 0) return D_MC64;
+    if (post == 32 && pre % 4 == 0) return D_MC32;
+  }
+  return ipad >= kBM ? D_MCP : -1;  // tiles of 128 rows over the innermost mode (no box overhang)
 }
 
 cudaError_t launch_ttm_i8(const double* X, int64_t pre, int64_t K, int64_t post, const double* B, int ncols,
                           double* out, int beta, const int* Xexp, void* ws, size_t ws_bytes, cudaStream_t st,
-                          const uint8_t* Xd) {
+                          const DigitView* dv) {
   if (pre <= 0 || post <= 0 || ncols <= 0) return cudaSuccess;
   if (K <= 0 || K > kMaxKI8 || ncols > 256) return cudaErrorInvalidValue;
   Geo g = make_geo(pre, K, post, ncols);
@@ -986,18 +1052,29 @@ cudaError_t launch_ttm_i8(const double* X, int64_t pre, int64_t K, int64_t post,
   }
   const int grid0 = (int)std::min<int64_t>(g.ntiles, sm_count());
   static const bool no_digits = getenv("CPD_I8_NO_DIGITS") != nullptr;
-  if (Xd && !no_digits && ttm_i8_digits_ok(pre, K, post) && ((uintptr_t)Xd % 16) == 0) {
-    const int Ld = post == 1 ? D_KC : (post % kBM) == 0 ? D_MC128 : post == 64 ? D_MC64 : D_MC32;
+  const int Ld = dv && dv->planes ? digit_layout(pre, K, post, dv->w, dv->ipad) : -1;
+  if (Ld >= 0 && !no_digits && ((uintptr_t)dv->planes % 16) == 0) {
+    Geo gd = g;
+    if (Ld == D_MCP) {
+      gd.w = dv->w;
+      gd.ipad = dv->ipad;
+      gd.Mo = post / dv->w;
+      gd.wb = (int)((dv->w + kBM - 1) / kBM);
+      gd.nmt = pre * gd.Mo * gd.wb;
+      gd.ntiles = gd.nmt * gd.ntn;
+    }
+    const int gridd = (int)std::min<int64_t>(gd.ntiles, sm_count());
     CUtensorMap tmd;
-    if (make_tmap_digits(Ld, Xd, g, &tmd)) {
+    if (make_tmap_digits(Ld, *dv, gd, &tmd)) {
       switch (g.Rp) {
 #define CPD_I8D_CASE(RP_)                                                                         \
   case RP_:                                                                                       \
     switch (Ld) {                                                                                 \
-      case D_KC: return run_i8d<D_KC, RP_>(grid0, g, Bimg, F, Xexp, out, beta, tmd, st);          \
-      case D_MC128: return run_i8d<D_MC128, RP_>(grid0, g, Bimg, F, Xexp, out, beta, tmd, st);    \
-      case D_MC64: return run_i8d<D_MC64, RP_>(grid0, g, Bimg, F, Xexp, out, beta, tmd, st);      \
-      default: return run_i8d<D_MC32, RP_>(grid0, g, Bimg, F, Xexp, out, beta, tmd, st);         \
+      case D_KC: return run_i8d<D_KC, RP_>(gridd, gd, Bimg, F, Xexp, out, beta, tmd, st);         \
+      case D_MC128: return run_i8d<D_MC128, RP_>(gridd, gd, Bimg, F, Xexp, out, beta, tmd, st);   \
+      case D_MC64: return run_i8d<D_MC64, RP_>(gridd, gd, Bimg, F, Xexp, out, beta, tmd, st);     \
+      case D_MC32: return run_i8d<D_MC32, RP_>(gridd, gd, Bimg, F, Xexp, out, beta, tmd, st);     \
+      default: return run_i8d<D_MCP, RP_>(gridd, gd, Bimg, F, Xexp, out, beta, tmd, st);         \
     }
         CPD_I8D_CASE(16)
         CPD_I8D_CASE(32)

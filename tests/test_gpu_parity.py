@@ -170,7 +170,7 @@ def test_c1_early_pp_exercises_second_order(cpd, early):
 
 
 @pytest.mark.parametrize("ttm_impl", [0, 1])
-@pytest.mark.parametrize("N,s,R", [(4, 12, 5), (5, 6, 3), (3, 40, 24), (6, 4, 2)])
+@pytest.mark.parametrize("N,s,R", [(4, 12, 5), (5, 6, 3), (3, 40, 24), (6, 4, 2), (4, 72, 6)])
 def test_msdt_and_dt_sweeps_order_N(cpd, N, s, R, ttm_impl):
     cfg = synth.custom(N, s, R, noise_var=1e-4, seed=N * 10 + s)
     T = dev_tensor(cpd, cfg)
@@ -328,7 +328,8 @@ def test_full_size_sampled_rows(cpd, c, ttm_impl):
 @pytest.mark.parametrize("shape,R", [((37, 29, 41), 8), ((16, 130, 12), 64), ((33, 20, 17), 13), ((9, 10, 11, 12), 100),
                                      ((11, 7, 13), 200), ((6, 5, 3), 1), ((200, 3, 130), 33), ((5, 300, 4), 17),
                                      ((64, 64, 64), 64), ((40, 33, 257), 32), ((3, 256, 128), 48), ((130, 48, 256), 64),
-                                     ((64, 64, 64), 32), ((12, 48, 32), 16), ((6, 8, 64, 64), 24)])
+                                     ((64, 64, 64), 32), ((12, 48, 32), 16), ((6, 8, 64, 64), 24),
+                                     ((9, 30, 200), 64), ((5, 7, 6, 100), 40), ((3, 130, 72), 20)])
 def test_ttm_i8_all_positions(cpd, shape, R, digits):
     """cpd_ttm_i8 (int8 digit slicing on tcgen05) against the oracle's T x_j A at every
     contraction position: ragged M tiles, K tails (odd K, K % 32 != 0), 1-4 N tiles."""
