@@ -1,5 +1,6 @@
 // Internal launchers of libcpd.so (sm_100a).  Citations: P:n = PAPER.md line n.
 #pragma once
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -30,7 +31,10 @@ struct DigitView {
   const uint8_t* planes = nullptr;
   int64_t w = 0, ipad = 0, plane_stride = 0;
 };
-inline int64_t digit_inner_pad(int64_t w) { return (w + 15) / 16 * 16; }
+inline int64_t digit_inner_pad(int64_t w) {
+  static const int64_t pad = getenv("CPD_DIGIT_PAD") ? atoi(getenv("CPD_DIGIT_PAD")) : 16;  // 16 | 32 | 64 | 128
+  return (w + pad - 1) / pad * pad;
+}
 // dv (may be null): when its layout serves this TTM view, the TTM streams the digit planes
 // instead of converting X
 cudaError_t launch_ttm_i8(const double* X, int64_t pre, int64_t K, int64_t post, const double* B, int ncols,

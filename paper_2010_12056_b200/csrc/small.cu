@@ -393,87 +393,129 @@ __global__ void __launch_bounds__(256)
 
 // --------- Γ^{(n)} = ∗_{k≠n} S^(k) (Eq. 1) and Γ^{-1} by in-place Gauss-Jordan (SPD: no pivoting;
 // every pivot is a Schur complement diagonal, > 0 iff Γ is SPD -> status), one CTA ---------
-// Register-blocked: a 16 x 16 thread grid, thread (ti, tj) holds the B x B block of rows
-// ti*B.., columns tj*B.. in registers (B = ceil(R/16) <= 8); per pivot one barrier: the pivot
-// row and column go through double-buffered shared memory.
-template <int B>
-__global__ void __launch_bounds__(256)
+// Blocked by 16 (R padded with the identity to Rp = 16 * ceil(R / 16) <= 128), Γ in shared
+// memory.  Block step K = [k0, k0 + 16):
+//   P = A[K,K]^{-1}                  one warp: 16 scalar pivots, lane j holds column j
+//   Rb = P A[K,:],  Cb = A[:,K]      (old column block)
+//   A[I,J] -= Cb[I] Rb[J],  A[I,K] = -Cb[I] P,  A[K,J] = Rb[J],  A[K,K] = P   (I, J != K)
+// -- the same pivots, in the same order, as the scalar Gauss-Jordan; the rank-16 updates run
+// on all threads with 4 x 4 register tiles (3 barriers per block step instead of one per pivot).
+constexpr int kGjThreads = 512;
+constexpr int kGjB = 16;
+
+__global__ void __launch_bounds__(kGjThreads)
     gamma_inverse_kernel(const double* __restrict__ S_all, int N, int n, int R, double* __restrict__ Ginv,
                          int* status) {
-  __shared__ double rowk[2][16 * B], colk[2][16 * B];
+  extern __shared__ double gsm[];
+  const int Rp = (R + kGjB - 1) / kGjB * kGjB;
+  const int LDA = Rp + 1;
+  double* A = gsm;                        // Rp x LDA
+  double* Rb = A + (size_t)Rp * LDA;      // 16 x Rp: P A[K,:]
+  double* Cb = Rb + kGjB * Rp;            // 16 x Rp: Cb[m * Rp + i] = A[i, k0 + m] (old)
+  double* P = Cb + kGjB * Rp;             // 16 x 16
   __shared__ int bad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t RR = (int64_t)R * R;
-  const int ti = threadIdx.x >> 4, tj = threadIdx.x & 15;
-  if (threadIdx.x == 0) bad = 0;
-  double a[B][B];
+  if (tid == 0) bad = 0;
+  for (int e = tid; e < Rp * Rp; e += kGjThreads) {
+    const int i = e / Rp, j = e - i * Rp;
+    double gv = (i == j) ? 1.0 : 0.0;  // padding: identity (does not touch the R x R block)
+    if (i < R && j < R) {
+      bool first = true;
+      for (int k = 0; k < N; k++) {
+        if (k == n) continue;
+        const double sv = S_all[k * RR + (int64_t)i * R + j];
+        gv = first ? sv : gv * sv;
+        first = false;
+      }
+    }
+    A[i * LDA + j] = gv;
+  }
+  __syncthreads();
+  const int ntj = Rp / 4, ntiles = ntj * ntj;
+  for (int k0 = 0; k0 < Rp; k0 += kGjB) {
+    // ---- P = A[K,K]^{-1}: warp 0, lane j < 16 holds column j ----
+    if (warp == 0) {
+      const int j = lane & 15;
+      double a[kGjB];
 #pragma unroll
-  for (int p = 0; p < B; p++)
+      for (int i = 0; i < kGjB; i++) a[i] = A[(k0 + i) * LDA + k0 + j];
 #pragma unroll
-    for (int q = 0; q < B; q++) {
-      const int i = ti * B + p, j = tj * B + q;
-      double gv = (i == j) ? 1.0 : 0.0;  // padding: identity (does not touch the R x R block)
-      if (i < R && j < R) {
-        bool first = true;
-        for (int k = 0; k < N; k++) {
-          if (k == n) continue;
-          const double sv = S_all[k * RR + (int64_t)i * R + j];
-          gv = first ? sv : gv * sv;
-          first = false;
+      for (int p = 0; p < kGjB; p++) {
+        const double piv = __shfl_sync(0xffffffffu, a[p], p);
+        const double inv = __drcp_rn(piv);  // IEEE reciprocal (= 1.0 / piv)
+        if (lane == 0 && (!(piv > 0.0) || !isfinite(piv))) bad = 1;
+        double c[kGjB];
+#pragma unroll
+        for (int i = 0; i < kGjB; i++) c[i] = __shfl_sync(0xffffffffu, a[i], p);
+        const double r = a[p] * inv;
+#pragma unroll
+        for (int i = 0; i < kGjB; i++) {
+          if (i == p) a[i] = (j == p) ? inv : r;
+          else a[i] = (j == p) ? -c[i] * inv : fma(-c[i], r, a[i]);
         }
       }
-      a[p][q] = gv;
-    }
-  for (int k = 0; k < R; k++) {
-    const int buf = k & 1, kb = k / B, ko = k - kb * B;
-    // publish row k and column k (their owners), then one barrier
-    if (ti == kb) {  // static register indexing: select row ko
+      if (lane < kGjB)
 #pragma unroll
-      for (int q = 0; q < B; q++) {
-        double v = a[0][q];
-#pragma unroll
-        for (int p = 1; p < B; p++)
-          if (p == ko) v = a[p][q];
-        rowk[buf][tj * B + q] = v;
-      }
-    }
-    if (tj == kb) {
-#pragma unroll
-      for (int p = 0; p < B; p++) {
-        double v = a[p][0];
-#pragma unroll
-        for (int q = 1; q < B; q++)
-          if (q == ko) v = a[p][q];
-        colk[buf][ti * B + p] = v;
-      }
+        for (int i = 0; i < kGjB; i++) P[i * kGjB + j] = a[i];
     }
     __syncthreads();
-    const double piv = rowk[buf][k];
-    const double inv = __drcp_rn(piv);  // IEEE reciprocal (= 1.0 / piv), no division subroutine
-    if (threadIdx.x == 0 && (!(piv > 0.0) || !isfinite(piv))) bad = 1;
-    double rk[B], ck[B];
+    // ---- Rb = P A[K,:] (old rows K), Cb = A[:,K] (old) ----
+    for (int e = tid; e < kGjB * Rp; e += kGjThreads) {
+      const int m = e / Rp, c = e - m * Rp;
+      double acc = 0.0;
 #pragma unroll
-    for (int q = 0; q < B; q++) rk[q] = rowk[buf][tj * B + q] * inv;
-#pragma unroll
-    for (int p = 0; p < B; p++) ck[p] = colk[buf][ti * B + p];
-#pragma unroll
-    for (int p = 0; p < B; p++)
-#pragma unroll
-      for (int q = 0; q < B; q++) {
-        const int i = ti * B + p, j = tj * B + q;
-        if (i == k) a[p][q] = (j == k) ? inv : rk[q];
-        else if (j == k) a[p][q] = -ck[p] * inv;
-        else a[p][q] = fma(-ck[p], rk[q], a[p][q]);
-      }
-  }
-#pragma unroll
-  for (int p = 0; p < B; p++)
-#pragma unroll
-    for (int q = 0; q < B; q++) {
-      const int i = ti * B + p, j = tj * B + q;
-      if (i < R && j < R) Ginv[(int64_t)i * R + j] = a[p][q];
+      for (int q = 0; q < kGjB; q++) acc = fma(P[m * kGjB + q], A[(k0 + q) * LDA + c], acc);
+      Rb[m * Rp + c] = acc;
+      Cb[m * Rp + c] = A[c * LDA + k0 + m];
     }
-  __syncthreads();
-  if (threadIdx.x == 0) status[0] = bad;
+    __syncthreads();
+    // ---- rank-16 update, 4 x 4 register tiles ----
+    for (int t = tid; t < ntiles; t += kGjThreads) {
+      const int i0 = (t / ntj) * 4, j0 = (t % ntj) * 4;
+      const bool rowK = i0 >= k0 && i0 < k0 + kGjB, colK = j0 >= k0 && j0 < k0 + kGjB;
+      double acc[4][4];
+      if (rowK) {
+#pragma unroll
+        for (int p = 0; p < 4; p++)
+#pragma unroll
+          for (int q = 0; q < 4; q++)
+            acc[p][q] = colK ? P[(i0 - k0 + p) * kGjB + j0 - k0 + q] : Rb[(i0 - k0 + p) * Rp + j0 + q];
+      } else {
+#pragma unroll
+        for (int p = 0; p < 4; p++)
+#pragma unroll
+          for (int q = 0; q < 4; q++) acc[p][q] = colK ? 0.0 : A[(i0 + p) * LDA + j0 + q];
+#pragma unroll 4
+        for (int m = 0; m < kGjB; m++) {
+          double cv[4], rv[4];
+#pragma unroll
+          for (int p = 0; p < 4; p++) cv[p] = Cb[m * Rp + i0 + p];
+#pragma unroll
+          for (int q = 0; q < 4; q++) rv[q] = colK ? P[m * kGjB + j0 - k0 + q] : Rb[m * Rp + j0 + q];
+#pragma unroll
+          for (int p = 0; p < 4; p++)
+#pragma unroll
+            for (int q = 0; q < 4; q++) acc[p][q] = fma(-cv[p], rv[q], acc[p][q]);
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < 4; p++)
+#pragma unroll
+        for (int q = 0; q < 4; q++) A[(i0 + p) * LDA + j0 + q] = acc[p][q];
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < R * R; e += kGjThreads) {
+    const int i = e / R, j = e - i * R;
+    Ginv[e] = A[i * LDA + j];
+  }
+  if (tid == 0) status[0] = bad;
+}
+
+size_t gamma_inverse_smem(int R) {
+  const size_t Rp = (size_t)(R + kGjB - 1) / kGjB * kGjB;
+  return sizeof(double) * (Rp * (Rp + 1) + 2 * kGjB * Rp + kGjB * kGjB);
 }
 
 // opt a kernel in to the largest dynamic shared memory the device allows
@@ -534,19 +576,15 @@ cudaError_t launch_gamma_chol(const double* S_all, int N, int n, int R, double* 
 
 cudaError_t launch_gamma_inverse(const double* S_all, int N, int n, int R, double* Ginv, int* status,
                                  cudaStream_t st) {
-  g_launches++;
-  const int B = (R + 15) / 16;
-  switch (B) {
-    case 1: gamma_inverse_kernel<1><<<1, 256, 0, st>>>(S_all, N, n, R, Ginv, status); break;
-    case 2: gamma_inverse_kernel<2><<<1, 256, 0, st>>>(S_all, N, n, R, Ginv, status); break;
-    case 3: gamma_inverse_kernel<3><<<1, 256, 0, st>>>(S_all, N, n, R, Ginv, status); break;
-    case 4: gamma_inverse_kernel<4><<<1, 256, 0, st>>>(S_all, N, n, R, Ginv, status); break;
-    case 5: gamma_inverse_kernel<5><<<1, 256, 0, st>>>(S_all, N, n, R, Ginv, status); break;
-    case 6: gamma_inverse_kernel<6><<<1, 256, 0, st>>>(S_all, N, n, R, Ginv, status); break;
-    case 7: gamma_inverse_kernel<7><<<1, 256, 0, st>>>(S_all, N, n, R, Ginv, status); break;
-    case 8: gamma_inverse_kernel<8><<<1, 256, 0, st>>>(S_all, N, n, R, Ginv, status); break;
-    default: return cudaErrorInvalidValue;
+  if (R < 1 || R > 128) return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = opt_in_smem(gamma_inverse_kernel);
+    if (e != cudaSuccess) return e;
+    attr = true;
   }
+  g_launches++;
+  gamma_inverse_kernel<<<1, kGjThreads, gamma_inverse_smem(R), st>>>(S_all, N, n, R, Ginv, status);
   return cudaGetLastError();
 }
 

@@ -134,6 +134,12 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                : "memory");
 }
+__device__ __forceinline__ void mma_commit_mc(uint32_t bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"(mask)
+      : "memory");
+}
 __device__ __forceinline__ double pow2(int e) {  // 2^e for normal range
   return __longlong_as_double((long long)(1023 + e) << 52);
 }
@@ -146,7 +152,32 @@ struct Geo {
   // padded-digit MC tiling (D_MCP): rows (p, mo, m), m < w in blocks of 128
   int64_t w = 0, Mo = 0, ipad = 0;
   int wb = 0;
+  // digit kernel: CTAs per cluster (1, or 2: a pair takes two N tiles of one M tile and the A box
+  // is TMA-multicast to both -- T's digits leave HBM/L2 once per pair)
+  int cl = 1;
 };
+
+// tile tt of this CTA (digit kernel) -> M tile, N tile
+__device__ __forceinline__ void tile_of(const Geo& g, int64_t tt, int64_t& mt, int& nt) {
+  if (g.cl == 1) {
+    const int64_t tile = blockIdx.x + tt * gridDim.x;
+    mt = tile / g.ntn;
+    nt = (int)(tile % g.ntn);
+  } else {  // cluster tile ct = (M tile, group of cl consecutive N tiles); rank = N tile in the group
+    const int ng = g.ntn / g.cl;
+    const int64_t ct = blockIdx.x / g.cl + tt * (gridDim.x / g.cl);
+    mt = ct / ng;
+    nt = (int)(ct - mt * ng) * g.cl + (int)(blockIdx.x % g.cl);
+  }
+}
+__device__ __forceinline__ int64_t tiles_of_cta(const Geo& g) {
+  if (g.cl == 1) return g.ntiles > blockIdx.x ? (g.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t cid = blockIdx.x / g.cl, ncl = gridDim.x / g.cl, nct = g.nmt * (g.ntn / g.cl);
+  return nct > cid ? (nct - 1 - cid) / ncl + 1 : 0;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 
 // 128-byte swizzle of the TMA KC boxes: 16-byte chunk c of row r is stored at c ^ (r % 8)
 __device__ __forceinline__ int swz(int row, int c) { return row * 128 + ((c ^ (row & 7)) << 4); }
@@ -569,8 +600,11 @@ Geo make_geo(int64_t pre, int64_t K, int64_t post, int ncols) {
   g.post = post;
   g.Mrows = pre * post;
   g.ncols = ncols;
-  g.ntn = (ncols + kRpMax - 1) / kRpMax;
+  static const int rpmax = getenv("CPD_I8_RPMAX") ? std::min(kRpMax, std::max(16, atoi(getenv("CPD_I8_RPMAX")) / 16 * 16)) : kRpMax;
+  g.ntn = (ncols + rpmax - 1) / rpmax;
   g.Rn = (ncols + g.ntn - 1) / g.ntn;
+  if (g.ntn > 1) g.Rn = std::min(rpmax, (g.Rn + 3) / 4 * 4);  // 32-byte aligned column blocks
+  g.ntn = (ncols + g.Rn - 1) / g.Rn;
   g.Rp = (g.Rn + 15) / 16 * 16;
   g.nmt = (g.Mrows + kBM - 1) / kBM;
   g.ntiles = g.nmt * g.ntn;
@@ -668,6 +702,98 @@ __device__ __forceinline__ uint64_t sdesc_sw(uint32_t addr, uint32_t lbo, uint32
   return sdesc(addr, lbo, sbo) | ((uint64_t)layout << 61);
 }
 
+// DRAIN epilogue of one warp: rows r (TMEM lane quarter base tq), columns c_lo .. c_lo + CQ.
+// Per tile: the 7 diagonals -> exact int64 partial sums in registers (tcgen05.ld, two diagonals
+// per wait), release the accumulator (tempty), then the FP64 recombination and the global stores
+// overlap the next tile's MMAs.
+template <int L, int Rp, int CQ>
+__device__ __forceinline__ void epilogue_drain(const Geo& g, uint32_t tq, int c_lo, int r, int64_t my_tiles,
+                                               double* __restrict__ out, int beta, const double* colscale,
+                                               uint32_t tfull0, uint32_t tempty0, int dbg) {
+  constexpr int NCH = CQ / 8;
+  const bool active = c_lo < Rp;  // warp-uniform
+  for (int64_t tt = 0; tt < my_tiles; tt++) {
+    int64_t mt;
+    int nt;
+    tile_of(g, tt, mt, nt);
+    int64_t i = mt * kBM + r;
+    bool row_ok = i < g.Mrows;
+    if constexpr (L == D_MCP) {
+      const int64_t pm = mt / g.wb;
+      const int64_t mb0 = (mt - pm * g.wb) * kBM;
+      const int64_t m = min(mb0, g.ipad - kBM) + r;
+      i = pm * g.w + m;
+      row_ok = m >= mb0 && m < g.w;
+    }
+    const int n0 = nt * g.Rn;
+    mbar_wait_sleep(tfull0, (uint32_t)tt & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    long long l0[CQ], l1[CQ];  // diagonals 0-2; diagonals 3-6 (|l1| < 2^56)
+    if (active) {
+#pragma unroll
+      for (int d0 = 0; d0 < kND; d0 += 2) {
+        uint32_t D[2][CQ];
+#pragma unroll
+        for (int dd = 0; dd < 2; dd++)
+#pragma unroll
+          for (int ch = 0; ch < NCH; ch++)
+            if (d0 + dd < kND)
+              asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                           : "=r"(D[dd][8 * ch]), "=r"(D[dd][8 * ch + 1]), "=r"(D[dd][8 * ch + 2]),
+                             "=r"(D[dd][8 * ch + 3]), "=r"(D[dd][8 * ch + 4]), "=r"(D[dd][8 * ch + 5]),
+                             "=r"(D[dd][8 * ch + 6]), "=r"(D[dd][8 * ch + 7])
+                           : "r"(tq + (d0 + dd) * Rp + c_lo + 8 * ch));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int dd = 0; dd < 2; dd++) {
+          const int d = d0 + dd;
+          if (d >= kND) break;
+#pragma unroll
+          for (int j = 0; j < CQ; j++) {
+            const long long v = (long long)(int)D[dd][j];
+            if (d == 0) l0[j] = v;
+            else if (d < 3) l0[j] += v << (8 * d);
+            else if (d == 3) l1[j] = v;
+            else l1[j] += v << (8 * (d - 3));
+          }
+        }
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    mbar_arrive(tempty0);
+    if (!active || (dbg & 32)) continue;
+#pragma unroll
+    for (int ch = 0; ch < NCH; ch++) {
+      const int c0 = c_lo + 8 * ch;
+      const int cmax = min(8, min(g.Rn - c0, g.ncols - n0 - c0));
+      if (!row_ok || cmax <= 0) continue;
+      double v[8];
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        const int jj = 8 * ch + j;
+        // (double)l1 rounds once: the same value as fma(D6, 2^48, l1_{3-5} 2^24) in the ping-pong path
+        v[j] = fma((double)l1[jj], 16777216.0 /* 2^24 */, (double)l0[jj]) * colscale[n0 + c0 + min(j, cmax - 1)];
+      }
+      double* orow = out + i * g.ncols + n0 + c0;
+      const uintptr_t al = reinterpret_cast<uintptr_t>(orow) & 31;
+      if (cmax == 8 && !beta && al == 0) {
+        asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(orow), "d"(v[0]), "d"(v[1]), "d"(v[2]),
+                     "d"(v[3]) : "memory");
+        asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(orow + 4), "d"(v[4]), "d"(v[5]), "d"(v[6]),
+                     "d"(v[7]) : "memory");
+      } else if (cmax == 8 && !beta && (al & 15) == 0) {
+#pragma unroll
+        for (int j = 0; j < 8; j += 2)
+          asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(orow + j), "d"(v[j]), "d"(v[j + 1]) : "memory");
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; j++)
+          if (j < cmax) orow[j] = beta ? orow[j] + v[j] : v[j];
+      }
+    }
+  }
+}
+
 template <int L, int RP>
 __global__ void __launch_bounds__(kThreadsD, 1)
     ttm_i8d_kernel(Geo g, const uint8_t* __restrict__ Bimg, const int* __restrict__ Fexp,
@@ -683,13 +809,17 @@ __global__ void __launch_bounds__(kThreadsD, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NDS * kDStage);
   const uint32_t full0 = su32(bars), empty0 = su32(bars + NDS);
   const uint32_t tfull0 = su32(bars + 2 * NDS), tempty0 = su32(bars + 2 * NDS + 2);
+  // DRAIN (one accumulator set, 7 Rp > 256 columns): the epilogue first moves the diagonals into
+  // exact int64 partial sums in registers and releases the accumulator, then does the FP64
+  // recombination and the global stores while the MMA warp already runs the next tile
+  constexpr bool DRAIN = NACC == 1;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * NDS + 4);
   double* colscale = reinterpret_cast<double*>(smem + NDS * kDStage + 256);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < NDS; s++) {
       mbar_init(full0 + 8 * s, 1);
-      mbar_init(empty0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, g.cl);  // one MMA commit per CTA of the cluster
     }
     for (int b = 0; b < 2; b++) {
       mbar_init(tfull0 + 8 * b, 1);
@@ -707,10 +837,13 @@ __global__ void __launch_bounds__(kThreadsD, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if (g.cl > 1) cluster_sync_all();  // peers' barriers initialised before any multicast
+  else __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tslot;
-  const int64_t my_tiles = g.ntiles > blockIdx.x ? (g.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t my_tiles = tiles_of_cta(g);
+  const uint16_t cmask = (uint16_t)((1u << g.cl) - 1);
+  const bool a_issuer = (blockIdx.x % g.cl) == 0;  // the cluster's rank 0 loads (multicasts) A
 
   if (warp == 0) {
     // ===================== TMA producer =====================
@@ -718,10 +851,10 @@ __global__ void __launch_bounds__(kThreadsD, 1)
       int s = 0;
       uint32_t par = 1;
       for (int64_t tt = 0; tt < my_tiles; tt++) {
-        const int64_t tile = blockIdx.x + tt * gridDim.x;
-        const int64_t mt = tile / g.ntn;
+        int64_t mt;
+        int nt;
+        tile_of(g, tt, mt, nt);
         const int64_t i0 = mt * kBM;
-        const int nt = (int)(tile % g.ntn);
         int p = 0, m0 = 0, mo = 0;
         if constexpr (L == D_MCP) {
           // the last block of the innermost mode is shifted back to end at w: boxes never
@@ -737,8 +870,40 @@ __global__ void __launch_bounds__(kThreadsD, 1)
         for (int kc = 0; kc < g.nkc; kc++) {
           mbar_wait(empty0 + 8 * s, par);
           const uint32_t st = su32(smem + s * kDStage), bar = full0 + 8 * s;
+          if (dbg & 2) {  // profiling: no loads
+            mbar_arrive(bar);
+            if (++s == NDS) {
+              s = 0;
+              par ^= 1;
+            }
+            continue;
+          }
           mbar_arrive_expect_tx(bar, kAStage + Bbytes);
-          if constexpr (L == D_KC) {
+          if (g.cl > 1) {
+            // A box multicast to every CTA of the cluster (same smem offset, each CTA's full[s])
+            if (a_issuer) {
+              if constexpr (L == D_KC) {
+                asm volatile(
+                    "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster "
+                    "[%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(st),
+                    "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(kc * 32), "r"((int)i0), "r"(0), "r"(bar), "h"(cmask)
+                    : "memory");
+              } else if (L == D_MCP && g.Mo > 1) {
+                asm volatile(
+                    "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster "
+                    "[%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(st),
+                    "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(m0), "r"(mo), "r"(kc * 32), "r"(p), "r"(0), "r"(bar),
+                    "h"(cmask)
+                    : "memory");
+              } else {
+                asm volatile(
+                    "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster "
+                    "[%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(st),
+                    "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(m0), "r"(kc * 32), "r"(p), "r"(0), "r"(bar), "h"(cmask)
+                    : "memory");
+              }
+            }
+          } else if constexpr (L == D_KC) {
             asm volatile(
                 "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
                 "%4}], [%5];" ::"r"(st),
@@ -775,6 +940,15 @@ __global__ void __launch_bounds__(kThreadsD, 1)
           }
         }
       }
+      if (g.cl > 1) {  // every stage's last release (peers' MMA commits) has landed before exit
+        for (int q = 0; q < NDS; q++) {
+          mbar_wait(empty0 + 8 * s, par);
+          if (++s == NDS) {
+            s = 0;
+            par ^= 1;
+          }
+        }
+      }
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -801,6 +975,7 @@ __global__ void __launch_bounds__(kThreadsD, 1)
           const uint64_t ad0 = sdesc_sw(abase, A_LBO, A_SBO, A_LAYOUT), bd0 = sdesc(abase + kAStage, 128, 256);
 #pragma unroll
           for (int a = kND - 1; a >= 0; a--) {
+            if (dbg & 1) break;  // profiling: no MMAs
             const uint32_t acc = (kc > 0 || a < kND - 1) ? 1u : 0u;
             const int n = (a + 1) * Rp;  // diagonals 0..a
             const uint64_t ad = ad0 + (uint64_t)((a * kAPlane) >> 4);
@@ -808,7 +983,8 @@ __global__ void __launch_bounds__(kThreadsD, 1)
             mma_i8(dcol, ad, bd, idesc(n > 256 ? 256 : n) | AMAJ, acc);
             if (n > 256) mma_i8(dcol + 256, ad, bd + ((256 * 32) >> 4), idesc(n - 256) | AMAJ, acc);
           }
-          mma_commit(empty0 + 8 * s);
+          if (g.cl > 1) mma_commit_mc(empty0 + 8 * s, cmask);  // release the stage in every CTA
+          else mma_commit(empty0 + 8 * s);
           if (++s == NDS) {
             s = 0;
             par ^= 1;
@@ -824,9 +1000,14 @@ __global__ void __launch_bounds__(kThreadsD, 1)
     const int cq = (warp - 2) >> 2;  // 0..3
     const int r = q * 32 + lane;
     constexpr int CQ = (Rp / 4 + 7) / 8 * 8;  // columns per epilogue warp, a multiple of 8
+    if constexpr (DRAIN) {
+      epilogue_drain<L, Rp, CQ>(g, tmem + ((uint32_t)(q * 32) << 16), cq * CQ, r, my_tiles, out, beta, colscale,
+                                tfull0, tempty0, dbg);
+    } else
     for (int64_t tt = 0; tt < my_tiles; tt++) {
-      const int64_t tile = blockIdx.x + tt * gridDim.x;
-      const int64_t mt = tile / g.ntn;
+      int64_t mt;
+      int nt;
+      tile_of(g, tt, mt, nt);
       int64_t i = mt * kBM + r;
       bool row_ok = i < g.Mrows;
       if constexpr (L == D_MCP) {
@@ -836,7 +1017,6 @@ __global__ void __launch_bounds__(kThreadsD, 1)
         i = pm * g.w + m;
         row_ok = m >= mb0 && m < g.w;                     // overlap rows belong to the previous block
       }
-      const int nt = (int)(tile % g.ntn);
       const int n0 = nt * g.Rn;
       const int ab = NACC == 2 ? (int)(tt & 1) : 0;
       const uint32_t use = NACC == 2 ? (uint32_t)(tt >> 1) : (uint32_t)tt;
@@ -869,11 +1049,16 @@ __global__ void __launch_bounds__(kThreadsD, 1)
             v[j] = (t + (double)l0) * colscale[n0 + c0 + min(j, cmax - 1)];
           }
           double* orow = out + i * g.ncols + n0 + c0;
-          if (cmax == 8 && !beta && ((reinterpret_cast<uintptr_t>(orow) & 31) == 0)) {
+          const uintptr_t al = reinterpret_cast<uintptr_t>(orow) & 31;
+          if (cmax == 8 && !beta && al == 0) {
             asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(orow), "d"(v[0]), "d"(v[1]), "d"(v[2]),
                          "d"(v[3]) : "memory");
             asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(orow + 4), "d"(v[4]), "d"(v[5]), "d"(v[6]),
                          "d"(v[7]) : "memory");
+          } else if (cmax == 8 && !beta && (al & 15) == 0) {
+#pragma unroll
+            for (int j = 0; j < 8; j += 2)
+              asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(orow + j), "d"(v[j]), "d"(v[j + 1]) : "memory");
           } else {
 #pragma unroll
             for (int j = 0; j < 8; j++)
@@ -886,7 +1071,8 @@ __global__ void __launch_bounds__(kThreadsD, 1)
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if (g.cl > 1) cluster_sync_all();  // no CTA leaves while a peer may still signal it
+  else __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
@@ -941,6 +1127,12 @@ __global__ void slice_digits_kernel(const double* __restrict__ X, int64_t n, int
 bool make_tmap_digits(int L, const DigitView& dv, const Geo& g, CUtensorMap* tm) {
   auto enc = tensor_map_encoder();
   if (!enc) return false;
+  // L2 promotion of the MN-major boxes (rows of 128 / 64 / 32 bytes at large strides)
+  static const int promo_env = getenv("CPD_I8_PROMO") ? atoi(getenv("CPD_I8_PROMO")) : 3;
+  const CUtensorMapL2promotion promo_mc = promo_env == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                          : promo_env == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                          : promo_env == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                           : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   uint8_t* base = const_cast<uint8_t*>(dv.planes);
   const cuuint64_t ps = (cuuint64_t)dv.plane_stride;
   CUresult r;
@@ -956,13 +1148,13 @@ bool make_tmap_digits(int L, const DigitView& dv, const Geo& g, CUtensorMap* tm)
       cuuint64_t strides[3] = {(cuuint64_t)dv.ipad, (cuuint64_t)dv.ipad * g.K, ps};
       cuuint32_t box[4] = {(cuuint32_t)kBM, 32, 1, (cuuint32_t)kND}, es[4] = {1, 1, 1, 1};
       r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+              CU_TENSOR_MAP_SWIZZLE_128B, promo_mc, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     } else {
       cuuint64_t dims[5] = {(cuuint64_t)dv.ipad, (cuuint64_t)g.Mo, (cuuint64_t)g.K, (cuuint64_t)g.pre, (cuuint64_t)kND};
       cuuint64_t strides[4] = {(cuuint64_t)dv.ipad, (cuuint64_t)dv.ipad * g.Mo, (cuuint64_t)dv.ipad * g.Mo * g.K, ps};
       cuuint32_t box[5] = {(cuuint32_t)kBM, 1, 32, 1, (cuuint32_t)kND}, es[5] = {1, 1, 1, 1, 1};
       r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+              CU_TENSOR_MAP_SWIZZLE_128B, promo_mc, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     }
   } else {  // unpadded: post contiguous
     const int mcw = L == D_MC128 ? 128 : L == D_MC64 ? 64 : 32;
@@ -972,7 +1164,7 @@ bool make_tmap_digits(int L, const DigitView& dv, const Geo& g, CUtensorMap* tm)
     const CUtensorMapSwizzle sw =
         mcw == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : mcw == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
     r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            promo_mc, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   }
   return r == CUDA_SUCCESS;
 }
@@ -987,8 +1179,23 @@ cudaError_t run_i8d(int grid, const Geo& g, const uint8_t* Bimg, const int* F, c
     attr = true;
   }
   static const int dbg = getenv("CPD_I8_DBG") ? atoi(getenv("CPD_I8_DBG")) : 0;  // profiling switches
-  ttm_i8d_kernel<L, RP><<<grid, kThreadsD, kSmemD, st>>>(g, Bimg, F, Xexp, out, beta, tm, dbg);
-  return cudaGetLastError();
+  if (g.cl == 1) {
+    ttm_i8d_kernel<L, RP><<<grid, kThreadsD, kSmemD, st>>>(g, Bimg, F, Xexp, out, beta, tm, dbg);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kThreadsD);
+  cfg.dynamicSmemBytes = kSmemD;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)g.cl;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, ttm_i8d_kernel<L, RP>, g, Bimg, F, Xexp, out, beta, tm, dbg);
 }
 
 }  // namespace
@@ -1063,7 +1270,15 @@ cudaError_t launch_ttm_i8(const double* X, int64_t pre, int64_t K, int64_t post,
       gd.nmt = pre * gd.Mo * gd.wb;
       gd.ntiles = gd.nmt * gd.ntn;
     }
-    const int gridd = (int)std::min<int64_t>(gd.ntiles, sm_count());
+    // N tiles of one M tile on one cluster with the A box multicast (2 or 4 N tiles)
+    static const bool no_mc = getenv("CPD_I8_NO_MULTICAST") != nullptr;
+    // pairs only: a 4-CTA cluster couples four MMA-bound CTAs to the slowest (C5: 53 -> 73 ms)
+    static const int cl_env = getenv("CPD_I8_CLUSTER") ? atoi(getenv("CPD_I8_CLUSTER")) : 2;
+    if (!no_mc && gd.ntn % 2 == 0 && (cl_env == 2 || cl_env == 4) && gd.ntn % cl_env == 0 &&
+        sm_count() % cl_env == 0)
+      gd.cl = cl_env;
+    const int gridd = gd.cl == 1 ? (int)std::min<int64_t>(gd.ntiles, sm_count())
+                                 : gd.cl * (int)std::min<int64_t>(gd.nmt * (gd.ntn / gd.cl), sm_count() / gd.cl);
     CUtensorMap tmd;
     if (make_tmap_digits(Ld, *dv, gd, &tmd)) {
       switch (g.Rp) {
