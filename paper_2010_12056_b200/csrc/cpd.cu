@@ -73,6 +73,11 @@ struct cpd_ctx {
   int dev = 0;
   cudaStream_t st = nullptr;
   bool own_stream = false;
+  // the library's work runs on its own stream `st` (priority above the default so the PP filler
+  // stream st3 never delays the critical path); `ust` is the caller's stream (opts.stream),
+  // ordered before each call's work and after it by events
+  cudaStream_t ust = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   ncclComm_t comm = nullptr;
   cpd::Comm cm;              // collective backend (NCCL or in-process local group)
   const double* T = nullptr;
@@ -89,6 +94,12 @@ struct cpd_ctx {
   int* pf_status = nullptr;            // Cholesky status per buffer
   cudaStream_t st2 = nullptr;          // side stream: Γ factorisation / W ahead of their mode
   cudaEvent_t ev_s = nullptr, ev_pf = nullptr;
+  // PP sweeps: the operator streams of mode n whose dA is already final (all i != n, n-1) run
+  // on st3 while the main stream still finishes update n-1; ev_pp_a orders st3 after the main
+  // stream's work so far, ev_pp_side[n] hands M_p^(n) + Σ_indep U^(n,i) back to the main stream
+  cudaStream_t st3 = nullptr;
+  cudaEvent_t ev_pp_a = nullptr, ev_pp_side[CPD_MAX_ORDER] = {};
+  double* ws_mttv3 = nullptr;          // st3's mTTV K-split partials
   int pf_mode = -1, pf_buf = 0;        // mode whose Γ factor (and W if pf_pp) is being prepared
   bool pf_pp = false;
   bool pf_fused = false;               // the prefetch formed Γ^{-1} (fused update) rather than L
@@ -635,6 +646,23 @@ void free_pp(cpd_ctx* c) {
   c->pp_valid = false;
 }
 
+// orders a public call's work after the caller's stream and the caller's stream after it
+struct UserSync {
+  cpd_ctx* c;
+  explicit UserSync(cpd_ctx* ctx) : c(ctx) {
+    if (c && c->ev_in) {
+      cudaEventRecord(c->ev_in, c->ust);
+      cudaStreamWaitEvent(c->st, c->ev_in, 0);
+    }
+  }
+  ~UserSync() {
+    if (c && c->ev_out) {
+      cudaEventRecord(c->ev_out, c->st);
+      cudaStreamWaitEvent(c->ust, c->ev_out, 0);
+    }
+  }
+};
+
 cpd_status check_ctx(cpd_ctx* ctx) {
   if (!ctx) return CPD_ERR_INVALID_ARG;
   if (ctx->poisoned) return CPD_ERR_STATE;
@@ -847,6 +875,7 @@ cpd_status cpd_destroy(cpd_ctx* c) {
   dfree(c, c->S_all);
   dfree(c, c->dS_all);
   if (c->st2) cudaStreamSynchronize(c->st2);
+  if (c->st3) cudaStreamSynchronize(c->st3);
   for (int b = 0; b < 2; b++) {
     dfree(c, c->Lp[b]);
     dfree(c, c->Wb[b]);
@@ -855,6 +884,7 @@ cpd_status cpd_destroy(cpd_ctx* c) {
   if (c->pf_status) cudaFreeAsync(c->pf_status, c->st);
   dfree(c, c->ws_gram);
   dfree(c, c->ws_mttv);
+  dfree(c, c->ws_mttv3);
   dfree(c, c->st_part);
   dfree(c, c->upd_part);
   dfree(c, c->upd_gpart);
@@ -879,6 +909,12 @@ cpd_status cpd_destroy(cpd_ctx* c) {
   if (c->ev_s) cudaEventDestroy(c->ev_s);
   if (c->ev_pf) cudaEventDestroy(c->ev_pf);
   if (c->st2) cudaStreamDestroy(c->st2);
+  if (c->ev_in) cudaEventDestroy(c->ev_in);
+  if (c->ev_out) cudaEventDestroy(c->ev_out);
+  if (c->ev_pp_a) cudaEventDestroy(c->ev_pp_a);
+  for (auto e : c->ev_pp_side)
+    if (e) cudaEventDestroy(e);
+  if (c->st3) cudaStreamDestroy(c->st3);
   if (c->own_stream && c->st) cudaStreamDestroy(c->st);
   delete c;
   return CPD_OK;
@@ -954,11 +990,17 @@ cpd_status cp_als_init(cpd_ctx** out, int N, const int64_t* shape, int R, const 
       return bail(CPD_ERR_CUDA);
     }
   }
-  if (o.stream) {
-    ctx->st = (cudaStream_t)o.stream;
-  } else {
-    ICU(cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking));
+  {
+    int lo = 0, hi = 0;
+    ICU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    ICU(cudaStreamCreateWithPriority(&ctx->st, cudaStreamNonBlocking, hi < lo ? hi + 1 : hi));
     ctx->own_stream = true;
+    ctx->ust = (cudaStream_t)o.stream;
+    ICU(cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming));
+    ICU(cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming));
+    // the borrowed T (and anything else the caller enqueued) precedes the library's work
+    ICU(cudaEventRecord(ctx->ev_in, ctx->ust));
+    ICU(cudaStreamWaitEvent(ctx->st, ctx->ev_in, 0));
   }
   {
     cudaMemPool_t pool;
@@ -1014,8 +1056,17 @@ cpd_status cp_als_init(cpd_ctx** out, int N, const int64_t* shape, int R, const 
   }
   ICU(cudaEventCreateWithFlags(&ctx->ev_s, cudaEventDisableTiming));
   ICU(cudaEventCreateWithFlags(&ctx->ev_pf, cudaEventDisableTiming));
+  {
+    // filler stream for PP operator streams off the critical path: lowest priority
+    int lo = 0, hi = 0;
+    ICU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    ICU(cudaStreamCreateWithPriority(&ctx->st3, cudaStreamNonBlocking, lo));
+  }
+  ICU(cudaEventCreateWithFlags(&ctx->ev_pp_a, cudaEventDisableTiming));
+  for (int n = 0; n < N; n++) ICU(cudaEventCreateWithFlags(&ctx->ev_pp_side[n], cudaEventDisableTiming));
   ITRY(dalloc(ctx, &ctx->ws_gram, 32 * RR));
   ITRY(dalloc(ctx, &ctx->ws_mttv, kMttvWs));
+  ITRY(dalloc(ctx, &ctx->ws_mttv3, kMttvWs));
   ITRY(dalloc(ctx, &ctx->st_part, 3 * 64));
   ITRY(dalloc(ctx, &ctx->upd_part, 3 * cpd::kUpdMaxBlocks));
   if (R <= cpd::kUpdMaxR) ITRY(dalloc(ctx, &ctx->upd_gpart, (int64_t)cpd::kUpdMaxBlocks * 2 * RR));
@@ -1063,6 +1114,7 @@ cpd_status cp_als_init(cpd_ctx** out, int N, const int64_t* shape, int R, const 
 
 cpd_status cpd_set_factors(cpd_ctx* ctx, const double* const* A_host) {
   TRY(check_ctx(ctx));
+  UserSync us_(ctx);
   if (!A_host) return fail(ctx, CPD_ERR_INVALID_ARG, "null factors");
   const int R = ctx->R;
   const int64_t RR = (int64_t)R * R;
@@ -1087,6 +1139,7 @@ cpd_status cpd_set_factors(cpd_ctx* ctx, const double* const* A_host) {
 
 cpd_status cpd_set_tensor(cpd_ctx* ctx) {
   TRY(check_ctx(ctx));
+  UserSync us_(ctx);
   TRY(prepare_tensor(ctx));
   CU(cudaStreamSynchronize(ctx->st));
   CU(cudaMemcpy(ctx->hscal, ctx->scal, sizeof(double) * SC_COUNT, cudaMemcpyDeviceToHost));
@@ -1105,16 +1158,19 @@ cpd_status cpd_set_tensor(cpd_ctx* ctx) {
 
 cpd_status msdt_sweep(cpd_ctx* ctx, double* fitness_out) {
   TRY(check_ctx(ctx));
+  UserSync us_(ctx);
   return regular_sweep(ctx, true, fitness_out);
 }
 
 cpd_status dt_sweep(cpd_ctx* ctx, double* fitness_out) {
   TRY(check_ctx(ctx));
+  UserSync us_(ctx);
   return regular_sweep(ctx, false, fitness_out);
 }
 
 cpd_status pp_init(cpd_ctx* ctx) {
   TRY(check_ctx(ctx));
+  UserSync us_(ctx);
   const int N = ctx->N;
   free_pp(ctx);
   // A_p <- A, dA <- 0 (Alg. 2 line 7)
@@ -1192,32 +1248,58 @@ cpd_status pp_init(cpd_ctx* ctx) {
 
 cpd_status pp_approx_sweep(cpd_ctx* ctx, double* fitness_out, int* still_valid) {
   TRY(check_ctx(ctx));
+  UserSync us_(ctx);
   if (!ctx->pp_valid || !ctx->pp_regime) return fail(ctx, CPD_ERR_STATE, "pp_approx_sweep needs a valid pp_init");
   const int N = ctx->N;
+  // operator [s_a, s_b, R] of the pair {n, i}: contract the axis of mode i with dA^(i) (Eq. 6)
+  auto spec = [&](int n, int i, double* bytes) {
+    const int a = std::min(n, i), b = std::max(n, i);
+    cpd::MttvSpec sp;
+    sp.X = ctx->ops[{a, b}];
+    sp.v = ctx->dA[i];
+    sp.K = ext(ctx, i);
+    sp.pre = n < i ? ext(ctx, n) : 1;
+    sp.post = n < i ? 1 : ext(ctx, n);
+    *bytes += 8.0 * ((double)ext(ctx, a) * ext(ctx, b) * ctx->R + (double)ext(ctx, i) * ctx->R);
+    return sp;
+  };
+  // M~_loc^(n) = M_p^(n) + Σ_{i≠n} U^(n,i) (Eqs. 5-6).  Only U^(n,n-1) waits for update n-1;
+  // the other N-2 streams of mode n (their dA are final once update n-2 is done) are issued on
+  // st3 one mode ahead, into Mt[n] = M_p^(n) + Σ_indep U, and the main stream adds U^(n,n-1).
+  // Fixed summation order: ((M_p + Σ_indep U in ascending i) + U^(n,n-1)).
   for (int n = 0; n < N; n++) {
-    // M~_loc^(n) = M_p^(n) + Σ_{i≠n} U^(n,i) (Eqs. 5-6): the N-1 operator streams of this mode
-    // in one launch, summed with M_p^(n) in a fixed order
+    const int nx = n + 1;
+    if (nx < N && N > 2) {
+      cpd::MttvSpec sp[CPD_MAX_ORDER];
+      int J = 0;
+      double bytes = 0.0;
+      for (int i = 0; i < N; i++)
+        if (i != nx && i != n) sp[J++] = spec(nx, i, &bytes);
+      CU(cudaEventRecord(ctx->ev_pp_a, ctx->st));  // update n-1 (and everything before) enqueued
+      CU(cudaStreamWaitEvent(ctx->st3, ctx->ev_pp_a, 0));
+      CU(cpd::launch_mttv_multi(sp, J, ctx->R, ctx->Mp[nx], ctx->Mt[nx], 0, ctx->ws_mttv3, kMttvWs, ctx->st3));
+      CU(cudaEventRecord(ctx->ev_pp_side[nx], ctx->st3));
+      ctx->counters[2] += bytes + 8.0 * 2 * ext(ctx, nx) * ctx->R;
+      ctx->counters[3] += 1;
+    }
+    double* Mt = ctx->Mt[n];
     cpd::MttvSpec sp[CPD_MAX_ORDER];
     int J = 0;
     double bytes = 0.0;
-    for (int i = 0; i < N; i++) {
-      if (i == n) continue;
-      const int a = std::min(n, i), b = std::max(n, i);
-      // operator [s_a, s_b, R]: contract the axis of mode i
-      sp[J].X = ctx->ops[{a, b}];
-      sp[J].v = ctx->dA[i];
-      sp[J].K = ext(ctx, i);
-      sp[J].pre = n < i ? ext(ctx, n) : 1;
-      sp[J].post = n < i ? 1 : ext(ctx, n);
-      bytes += 8.0 * ((double)ext(ctx, a) * ext(ctx, b) * ctx->R + (double)ext(ctx, i) * ctx->R);
-      J++;
-    }
-    double* Mt = ctx->Mt[n];
-    {
+    if (n == 0 || N <= 2) {
+      for (int i = 0; i < N; i++)
+        if (i != n) sp[J++] = spec(n, i, &bytes);
       PhaseScope ps(ctx, PH_MTTV);
       CU(cpd::launch_mttv_multi(sp, J, ctx->R, ctx->Mp[n], Mt, 0, ctx->ws_mttv, kMttvWs, ctx->st));
+      ctx->counters[2] += 8.0 * 2 * ext(ctx, n) * ctx->R;
+    } else {
+      sp[J++] = spec(n, n - 1, &bytes);
+      CU(cudaStreamWaitEvent(ctx->st, ctx->ev_pp_side[n], 0));
+      PhaseScope ps(ctx, PH_MTTV);
+      CU(cpd::launch_mttv_multi(sp, J, ctx->R, nullptr, Mt, 1, ctx->ws_mttv, kMttvWs, ctx->st));
+      ctx->counters[2] += 8.0 * 2 * ext(ctx, n) * ctx->R;
     }
-    ctx->counters[2] += bytes + 8.0 * 2 * ext(ctx, n) * ctx->R;
+    ctx->counters[2] += bytes;
     ctx->counters[3] += 1;
     TRY(update_mode(ctx, n, Mt, true));
   }
@@ -1261,12 +1343,14 @@ static cpd_status gather_rows(cpd_ctx* ctx, int n0, const double* src_local, dou
 
 cpd_status cpd_get_factor(cpd_ctx* ctx, int n0, double* host_out) {
   TRY(check_ctx(ctx));
+  UserSync us_(ctx);
   if (n0 < 0 || n0 >= ctx->N || !host_out) return fail(ctx, CPD_ERR_INVALID_ARG, "bad mode");
   return gather_rows(ctx, n0, ctx->A[n0], host_out);
 }
 
 cpd_status cpd_get_last_mttkrp(cpd_ctx* ctx, int n0, double* host_out) {
   TRY(check_ctx(ctx));
+  UserSync us_(ctx);
   if (n0 < 0 || n0 >= ctx->N || !host_out) return fail(ctx, CPD_ERR_INVALID_ARG, "bad mode");
   if (ctx->Mlast_src[n0]) {
     const int64_t ro = rows_own(ctx, n0), off = own_off(ctx, n0);
@@ -1320,6 +1404,7 @@ cpd_status cpd_reset_counters(cpd_ctx* ctx) {
 
 cpd_status cpd_debug_get_pp_operator(cpd_ctx* ctx, int a0, int b0, double* host_out) {
   TRY(check_ctx(ctx));
+  UserSync us_(ctx);
   if (!ctx->pp_valid) return fail(ctx, CPD_ERR_STATE, "no PP operators");
   if (a0 < 0 || b0 <= a0 || b0 >= ctx->N || !host_out) return fail(ctx, CPD_ERR_INVALID_ARG, "bad pair");
   auto it = ctx->ops.find({a0, b0});
