@@ -122,7 +122,7 @@ cudaError_t launch_update_stats(const double* A, const double* base, double* dA,
 // S == nullptr skips the Gram phase.
 // R <= kUpdMaxR.
 constexpr int kUpdMaxR = 128;  // Γ^{-1} + the packed factor fit one CTA's shared memory
-constexpr int kUpdMaxBlocks = 64;
+constexpr int kUpdMaxBlocks = 148;
 // part: 3 * kUpdMaxBlocks doubles; gpart: kUpdMaxBlocks * 2 * R * R doubles (per-CTA Gram partials)
 size_t update_fused_smem(int R, bool pp, int RB);
 int update_fused_blocks(int64_t rows);

@@ -878,8 +878,9 @@ __global__ void __launch_bounds__(kThreadsD, 1)
             }
             continue;
           }
-          mbar_arrive_expect_tx(bar, kAStage + Bbytes);
-          if (g.cl > 1) {
+          mbar_arrive_expect_tx(bar, ((dbg & 8) ? 0 : kAStage) + ((dbg & 4) ? 0 : Bbytes));
+          if (dbg & 8) {  // profiling: no A loads
+          } else if (g.cl > 1) {
             // A box multicast to every CTA of the cluster (same smem offset, each CTA's full[s])
             if (a_issuer) {
               if constexpr (L == D_KC) {
@@ -929,11 +930,12 @@ __global__ void __launch_bounds__(kThreadsD, 1)
                 : "memory");
           }
           const uint8_t* bsrc = Bimg + ((int64_t)nt * g.nkc + kc) * Bbytes;
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                  st + kAStage),
-              "l"(bsrc), "r"(Bbytes), "r"(bar)
-              : "memory");
+          if (!(dbg & 4))  // profiling switch 4: no B loads
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    st + kAStage),
+                "l"(bsrc), "r"(Bbytes), "r"(bar)
+                : "memory");
           if (++s == NDS) {
             s = 0;
             par ^= 1;

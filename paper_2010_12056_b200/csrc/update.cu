@@ -38,6 +38,39 @@ __device__ __forceinline__ void fill_smem(double* dst, const double* __restrict_
   for (; e < n; e += UPD_THREADS) dst[e] = __ldg(src + e);
 }
 
+// out[c] = Σ_k v[k] Mat[k, c] for the row v held by a warp (lane owns v[lane + 32 u]) and the
+// columns c = lane + 32 u: v_k broadcast by one shuffle per k (block u of k is static), two
+// independent FMA chains (even / odd k) summed at the end -- a fixed order
+template <int U>
+__device__ __forceinline__ void rowvec_mat(const double (&v)[U], const double* __restrict__ Mat, int R, int lane,
+                                           double (&out)[U]) {
+  double e[U], o[U];
+#pragma unroll
+  for (int u = 0; u < U; u++) e[u] = o[u] = 0.0;
+#pragma unroll
+  for (int ub = 0; ub < U; ub++) {
+    const int kmax = min(32, R - 32 * ub);
+#pragma unroll 4
+    for (int kk = 0; kk < 32; kk += 2) {
+      if (kk >= kmax) break;
+      const int k = 32 * ub + kk;
+      const double v0 = __shfl_sync(0xffffffffu, v[ub], kk);
+      const double v1 = __shfl_sync(0xffffffffu, v[ub], kk + 1);
+      const bool has1 = kk + 1 < kmax;
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int c = lane + 32 * u;
+        if (c < R) {
+          e[u] = fma(v0, Mat[k * R + c], e[u]);
+          if (has1) o[u] = fma(v1, Mat[(k + 1) * R + c], o[u]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < U; u++) out[u] = e[u] + o[u];
+}
+
 template <int U>
 __global__ void __launch_bounds__(UPD_THREADS)
     update_fused_kernel(int R, int64_t rows, const double* __restrict__ Gi, const double* __restrict__ W,
@@ -71,21 +104,7 @@ __global__ void __launch_bounds__(UPD_THREADS)
     }
     if (W) {  // y += a_old W
       double v[U];
-#pragma unroll
-      for (int u = 0; u < U; u++) v[u] = 0.0;
-      for (int k = 0; k < R; k++) {
-        double ak = __shfl_sync(0xffffffffu, ao[0], k & 31);
-#pragma unroll
-        for (int u = 1; u < U; u++) {
-          const double t = __shfl_sync(0xffffffffu, ao[u], k & 31);
-          if ((k >> 5) == u) ak = t;
-        }
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-          const int c = lane + 32 * u;
-          if (c < R) v[u] = fma(ak, Ws[k * R + c], v[u]);
-        }
-      }
+      rowvec_mat<U>(ao, Ws, R, lane, v);
 #pragma unroll
       for (int u = 0; u < U; u++) {
         y[u] += v[u];
@@ -98,21 +117,7 @@ __global__ void __launch_bounds__(UPD_THREADS)
     for (int u = 0; u < U; u++) mm[u] = y[u];
     // x = y Γ^{-1}: lanes own output columns, y_k broadcast by shuffles (independent FMAs)
     double x[U];
-#pragma unroll
-    for (int u = 0; u < U; u++) x[u] = 0.0;
-    for (int k = 0; k < R; k++) {
-      double yk = __shfl_sync(0xffffffffu, y[0], k & 31);
-#pragma unroll
-      for (int u = 1; u < U; u++) {
-        const double t = __shfl_sync(0xffffffffu, y[u], k & 31);
-        if ((k >> 5) == u) yk = t;
-      }
-#pragma unroll
-      for (int u = 0; u < U; u++) {
-        const int c = lane + 32 * u;
-        if (c < R) x[u] = fma(yk, G[k * R + c], x[u]);
-      }
-    }
+    rowvec_mat<U>(y, G, R, lane, x);
 #pragma unroll
     for (int u = 0; u < U; u++) y[u] = x[u];
 #pragma unroll
@@ -157,25 +162,53 @@ __global__ void __launch_bounds__(UPD_THREADS)
     const int a = (int)(f / R), b = (int)(f - (int64_t)a * R);
     const double* Y = second ? Ds : Xs;
     double acc = 0.0;
+#pragma unroll 8
     for (int r = 0; r < nrows; r++) acc = fma(Xs[r * R + a], Y[r * R + b], acc);
     gpart[(int64_t)blockIdx.x * nout + e] = acc;
   }
   cg::this_grid().sync();
   // phase 2b: S, dS = Σ over CTAs in CTA order (deterministic; S exactly symmetric)
-  for (int64_t e = (int64_t)blockIdx.x * UPD_THREADS + tid; e < nout; e += (int64_t)gridDim.x * UPD_THREADS) {
-    // CTA partials in CTA order; 16 independent loads in flight per batch
-    double acc = gpart[e];
-    unsigned c = 1;
-    for (; c + 16 <= gridDim.x; c += 16) {
-      double v[16];
+  // 4 lanes per output when the grid has the threads (lane q sums the CTA partials c = q mod 4 in
+  // ascending c, then ((s0 + s1) + (s2 + s3))): a fixed order either way
+  const int64_t nthr = (int64_t)gridDim.x * UPD_THREADS;
+  const int64_t gt = (int64_t)blockIdx.x * UPD_THREADS + tid;
+  if (nout * 4 <= nthr) {
+    const int64_t e = gt >> 2;
+    const int q = (int)(gt & 3);
+    double acc = 0.0;
+    if (e < nout) {
+      unsigned c = q;
+      for (; c + 12 < gridDim.x; c += 16) {
+        double v[4];
 #pragma unroll
-      for (int q = 0; q < 16; q++) v[q] = gpart[(int64_t)(c + q) * nout + e];
+        for (int t = 0; t < 4; t++) v[t] = gpart[(int64_t)(c + 4 * t) * nout + e];
 #pragma unroll
-      for (int q = 0; q < 16; q++) acc += v[q];
+        for (int t = 0; t < 4; t++) acc += v[t];
+      }
+      for (; c < gridDim.x; c += 4) acc += gpart[(int64_t)c * nout + e];
     }
-    for (; c < gridDim.x; c++) acc += gpart[(int64_t)c * nout + e];
-    if (e < RR) S[e] = acc;
-    else dS[e - RR] = acc;
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    if (e < nout && q == 0) {
+      if (e < RR) S[e] = acc;
+      else dS[e - RR] = acc;
+    }
+  } else {
+    for (int64_t e = gt; e < nout; e += nthr) {
+      // CTA partials in CTA order; 16 independent loads in flight per batch
+      double acc = gpart[e];
+      unsigned c = 1;
+      for (; c + 16 <= gridDim.x; c += 16) {
+        double v[16];
+#pragma unroll
+        for (int q = 0; q < 16; q++) v[q] = gpart[(int64_t)(c + q) * nout + e];
+#pragma unroll
+        for (int q = 0; q < 16; q++) acc += v[q];
+      }
+      for (; c < gridDim.x; c++) acc += gpart[(int64_t)c * nout + e];
+      if (e < RR) S[e] = acc;
+      else dS[e - RR] = acc;
+    }
   }
   if (blockIdx.x == 0 && tid < 3) {
     double s = part[tid];

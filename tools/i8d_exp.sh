@@ -1,6 +1,6 @@
 #!/bin/bash
 # int8 digit TTM: kernel-only durations (ncu gpu__time_duration) per mode for BASELINE shapes
-# under the profiling switches CPD_I8_DBG (1 no MMA, 2 no loads, 32 no epilogue body)
+# under the profiling switches CPD_I8_DBG (1 no MMA, 2 no loads, 4 no B loads, 8 no A loads, 32 no epilogue body)
 for sh in ${SHAPES:-1024,3,64 200,4,100 64,5,32}; do
   shape=${sh//,/ }
   for d in ${DBGS:-0 1 2 32 35}; do
