@@ -405,7 +405,7 @@ constexpr int kGjB = 16;
 
 __global__ void __launch_bounds__(kGjThreads)
     gamma_inverse_kernel(const double* __restrict__ S_all, int N, int n, int R, double* __restrict__ Ginv,
-                         int* status) {
+                         int* status, int dbg) {
   extern __shared__ double gsm[];
   const int Rp = (R + kGjB - 1) / kGjB * kGjB;
   const int LDA = Rp + 1;
@@ -414,9 +414,11 @@ __global__ void __launch_bounds__(kGjThreads)
   double* Cb = Rb + kGjB * Rp;            // 16 x Rp: Cb[m * Rp + i] = A[i, k0 + m] (old)
   double* P = Cb + kGjB * Rp;             // 16 x 16
   __shared__ int bad;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ double pr[2][kGjB], pc[2][kGjB];  // pivot row / column of the 16 x 16 block
+  const int tid = threadIdx.x;
   const int64_t RR = (int64_t)R * R;
   if (tid == 0) bad = 0;
+#pragma unroll 4
   for (int e = tid; e < Rp * Rp; e += kGjThreads) {
     const int i = e / Rp, j = e - i * Rp;
     double gv = (i == j) ? 1.0 : 0.0;  // padding: identity (does not touch the R x R block)
@@ -432,36 +434,38 @@ __global__ void __launch_bounds__(kGjThreads)
     A[i * LDA + j] = gv;
   }
   __syncthreads();
-  const int ntj = Rp / 4, ntiles = ntj * ntj;
+  const int ntj = Rp / 4, ntiles = ntj * (Rp / 8);
   for (int k0 = 0; k0 < Rp; k0 += kGjB) {
-    // ---- P = A[K,K]^{-1}: warp 0, lane j < 16 holds column j ----
-    if (warp == 0) {
-      const int j = lane & 15;
-      double a[kGjB];
-#pragma unroll
-      for (int i = 0; i < kGjB; i++) a[i] = A[(k0 + i) * LDA + k0 + j];
-#pragma unroll
+    // ---- P = A[K,K]^{-1}: 256 threads, thread (i, j) holds element (i, j); pivot row and
+    // column through double-buffered shared memory, one barrier per pivot ----
+    {
+      const int i = tid >> 4, j = tid & 15;
+      const bool act = tid < kGjB * kGjB && !(dbg & 1);
+      double a = act ? A[(k0 + i) * LDA + k0 + j] : 0.0;
+      if (act && i == 0) pr[0][j] = a;
+      if (act && j == 0) pc[0][i] = a;
+      __syncthreads();
+#pragma unroll 1
       for (int p = 0; p < kGjB; p++) {
-        const double piv = __shfl_sync(0xffffffffu, a[p], p);
-        const double inv = __drcp_rn(piv);  // IEEE reciprocal (= 1.0 / piv)
-        if (lane == 0 && (!(piv > 0.0) || !isfinite(piv))) bad = 1;
-        double c[kGjB];
-#pragma unroll
-        for (int i = 0; i < kGjB; i++) c[i] = __shfl_sync(0xffffffffu, a[i], p);
-        const double r = a[p] * inv;
-#pragma unroll
-        for (int i = 0; i < kGjB; i++) {
-          if (i == p) a[i] = (j == p) ? inv : r;
-          else a[i] = (j == p) ? -c[i] * inv : fma(-c[i], r, a[i]);
+        const int b = p & 1;
+        if (act) {
+          const double piv = pr[b][p];
+          const double inv = __drcp_rn(piv);  // IEEE reciprocal (= 1.0 / piv)
+          if (tid == 0 && (!(piv > 0.0) || !isfinite(piv))) bad = 1;
+          const double r = pr[b][j] * inv, c = pc[b][i];
+          if (i == p) a = (j == p) ? inv : r;
+          else a = (j == p) ? -c * inv : fma(-c, r, a);
+          if (i == p + 1) pr[b ^ 1][j] = a;
+          if (j == p + 1) pc[b ^ 1][i] = a;
         }
+        __syncthreads();
       }
-      if (lane < kGjB)
-#pragma unroll
-        for (int i = 0; i < kGjB; i++) P[i * kGjB + j] = a[i];
+      if (act) P[i * kGjB + j] = a;
     }
     __syncthreads();
     // ---- Rb = P A[K,:] (old rows K), Cb = A[:,K] (old) ----
     for (int e = tid; e < kGjB * Rp; e += kGjThreads) {
+      if (dbg & 2) break;
       const int m = e / Rp, c = e - m * Rp;
       double acc = 0.0;
 #pragma unroll
@@ -470,39 +474,48 @@ __global__ void __launch_bounds__(kGjThreads)
       Cb[m * Rp + c] = A[c * LDA + k0 + m];
     }
     __syncthreads();
-    // ---- rank-16 update, 4 x 4 register tiles ----
+    // ---- rank-16 update, 8 x 4 register tiles: rows 8 ti .. 8 ti + 7, columns tj + ntj q
+    // (lanes hold consecutive columns: conflict-free shared-memory rows; 12 loads per 32 FMAs) ----
     for (int t = tid; t < ntiles; t += kGjThreads) {
-      const int i0 = (t / ntj) * 4, j0 = (t % ntj) * 4;
-      const bool rowK = i0 >= k0 && i0 < k0 + kGjB, colK = j0 >= k0 && j0 < k0 + kGjB;
-      double acc[4][4];
+      if (dbg & 4) break;
+      const int i0 = (t / ntj) * 8, tj = t % ntj;
+      const bool rowK = i0 >= k0 && i0 < k0 + kGjB;
+      int jq[4];
+      bool colK[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        jq[q] = tj + ntj * q;
+        colK[q] = jq[q] >= k0 && jq[q] < k0 + kGjB;
+      }
+      double acc[8][4];
       if (rowK) {
 #pragma unroll
-        for (int p = 0; p < 4; p++)
+        for (int p = 0; p < 8; p++)
 #pragma unroll
           for (int q = 0; q < 4; q++)
-            acc[p][q] = colK ? P[(i0 - k0 + p) * kGjB + j0 - k0 + q] : Rb[(i0 - k0 + p) * Rp + j0 + q];
+            acc[p][q] = colK[q] ? P[(i0 - k0 + p) * kGjB + jq[q] - k0] : Rb[(i0 - k0 + p) * Rp + jq[q]];
       } else {
 #pragma unroll
-        for (int p = 0; p < 4; p++)
+        for (int p = 0; p < 8; p++)
 #pragma unroll
-          for (int q = 0; q < 4; q++) acc[p][q] = colK ? 0.0 : A[(i0 + p) * LDA + j0 + q];
-#pragma unroll 4
+          for (int q = 0; q < 4; q++) acc[p][q] = colK[q] ? 0.0 : A[(i0 + p) * LDA + jq[q]];
+#pragma unroll 2
         for (int m = 0; m < kGjB; m++) {
-          double cv[4], rv[4];
+          double cv[8], rv[4];
 #pragma unroll
-          for (int p = 0; p < 4; p++) cv[p] = Cb[m * Rp + i0 + p];
+          for (int p = 0; p < 8; p++) cv[p] = Cb[m * Rp + i0 + p];
 #pragma unroll
-          for (int q = 0; q < 4; q++) rv[q] = colK ? P[m * kGjB + j0 - k0 + q] : Rb[m * Rp + j0 + q];
+          for (int q = 0; q < 4; q++) rv[q] = colK[q] ? P[m * kGjB + jq[q] - k0] : Rb[m * Rp + jq[q]];
 #pragma unroll
-          for (int p = 0; p < 4; p++)
+          for (int p = 0; p < 8; p++)
 #pragma unroll
             for (int q = 0; q < 4; q++) acc[p][q] = fma(-cv[p], rv[q], acc[p][q]);
         }
       }
 #pragma unroll
-      for (int p = 0; p < 4; p++)
+      for (int p = 0; p < 8; p++)
 #pragma unroll
-        for (int q = 0; q < 4; q++) A[(i0 + p) * LDA + j0 + q] = acc[p][q];
+        for (int q = 0; q < 4; q++) A[(i0 + p) * LDA + jq[q]] = acc[p][q];
     }
     __syncthreads();
   }
@@ -584,7 +597,8 @@ cudaError_t launch_gamma_inverse(const double* S_all, int N, int n, int R, doubl
     attr = true;
   }
   g_launches++;
-  gamma_inverse_kernel<<<1, kGjThreads, gamma_inverse_smem(R), st>>>(S_all, N, n, R, Ginv, status);
+  static const int dbg = getenv("CPD_GJ_DBG") ? atoi(getenv("CPD_GJ_DBG")) : 0;  // profiling switches
+  gamma_inverse_kernel<<<1, kGjThreads, gamma_inverse_smem(R), st>>>(S_all, N, n, R, Ginv, status, dbg);
   return cudaGetLastError();
 }
 
