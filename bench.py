@@ -406,26 +406,31 @@ def dmma_roof(ttm_tf, fp64, fp64_src, flops, ms, ctr):
 
 
 def dmma_compare(cpd, torch, cfg, T, m, local, rank, world, nccl_id, stream, fp64, fp64_src):
-    """The FP64 DMMA engine on the same tensor and factors (north_star's TTM FP64-TC %): one
-    warm-up MSDT cycle, then two timed cycles; CUDA events on the library stream."""
+    """The FP64 DMMA engine on the same tensor and factors (north_star's TTM FP64-TC %): two
+    warm-up MSDT cycles, then three timed cycles (median); CUDA events on the caller's stream."""
     import torch.distributed as dist
     N = cfg.N
     A = [m.get_factor(n) for n in range(N)]
     md = cpd.cp_als_init(T, cfg.shape, cfg.R, A, device=local, rank=rank, world=world,
                          nccl_id=nccl_id if world == 1 else _new_id(cpd, dist, rank), stream=stream,
                          profile_phases=1, ttm_impl=TTM_IMPL["dmma"])
-    for _ in range(N - 1):
+    for _ in range(2 * (N - 1)):
         md.msdt_sweep()
     torch.cuda.synchronize()
     md.reset_counters()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(2 * (N - 1)):
-        md.msdt_sweep()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / (2 * (N - 1))
+    # whole cycles, each bracketed by events; the median cycle (a second context shares the
+    # device memory pool with the first, so a cycle may pay a one-off pool growth)
+    cyc = []
+    for _ in range(3):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(N - 1):
+            md.msdt_sweep()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        cyc.append(e0.elapsed_time(e1) / (N - 1))
+    ms = float(np.median(cyc))
     ph, ctr = md.phase_ms(), md.counters()
     md.close()
     flops = ctr["ttm_flops"] / max(ctr["ttm_launches"], 1)

@@ -1,5 +1,5 @@
 """Kernel timeline (all streams, CUPTI via torch.profiler) of one MSDT cycle, pp_init and two
-PP-approximated sweeps on a BASELINE config.  usage: python tools/timeline.py [config] [presweeps]
+PP-approximated sweeps on a BASELINE config.  usage: python tools/timeline.py [config] [presweeps] [auto|dmma|int8]
 Prints every kernel with its stream, start offset and duration (us), per sweep."""
 import os
 import sys
@@ -14,13 +14,14 @@ import synth  # noqa: E402
 
 c = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 pres = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+impl = sys.argv[3] if len(sys.argv) > 3 else "auto"
 cfg = synth.config(c)
 stream = torch.cuda.Stream()
 with torch.cuda.stream(stream):
     T = bench.make_slab(cpd, torch, cfg, 0, 1, stream)
 torch.cuda.synchronize()
 m = cpd.cp_als_init(T, cfg.shape, cfg.R, synth.init_factors(cfg), stream=stream,
-                    pp_eps=0.2 if c == 4 else 0.1)
+                    pp_eps=0.2 if c == 4 else 0.1, ttm_impl=bench.TTM_IMPL[impl])
 for _ in range(pres):
     m.msdt_sweep()
 m.pp_init()
