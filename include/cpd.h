@@ -63,7 +63,11 @@ typedef struct {
   int rank, world;            /* 1-D split of mode N (rank owns slab rank*s_N/world ...) */
   const void* nccl_unique_id; /* CPD_NCCL_ID_BYTES bytes from cpd_nccl_unique_id on rank 0,
                                  broadcast by the caller; NULL iff world == 1 */
-  void* stream;               /* cudaStream_t to run on, or NULL (library creates one) */
+  void* stream;               /* caller's cudaStream_t (NULL = the legacy default stream).  The library
+                                 runs on streams it owns (its main stream one priority level above the
+                                 default; a highest-priority side stream for Γ^-1 / W; a lowest-priority
+                                 filler stream for PP operator streams); every call is ordered after the
+                                 work already enqueued on `stream` and `stream` after the call's work */
   double pp_eps;              /* ε in (0,1) for still_valid / cpd_pp_condition (Alg. 2 line 5) */
   int reuse_root_in_pp_init;  /* P:384 footnote: reuse a still-valid MSDT root in pp_init (default 1) */
   int profile_phases;         /* CUDA-event timers: 0 off; 1 TTM and mTTV launches only (the roofline
@@ -98,7 +102,7 @@ typedef struct cpd_local_group cpd_local_group;
 cpd_status cpd_local_group_create(int world, cpd_local_group** out);
 cpd_status cpd_local_group_destroy(cpd_local_group* g);
 
-/* Fill *o with defaults: device 0, rank 0, world 1, no NCCL id, library stream,
+/* Fill *o with defaults: device 0, rank 0, world 1, no NCCL id, default caller stream,
  * pp_eps 0.1, reuse_root_in_pp_init 1, profile_phases 0, ttm_impl CPD_TTM_AUTO. */
 cpd_status cpd_opts_default(cpd_opts* o);
 
