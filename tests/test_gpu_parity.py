@@ -414,3 +414,32 @@ def test_set_tensor_new_contents(cpd, ttm_impl):
         assert abs(f - out["f"]) <= TOL * abs(out["f"])
         A = out["A"]
     m.close()
+
+
+def test_caller_stream_ordering(cpd):
+    """opts.stream semantics (cpd.h): the library runs on its own streams, ordered after the work
+    already enqueued on the caller's stream.  The new tensor contents are written on a caller
+    stream behind a ~1 ms spin and cpd_set_tensor is called with no host synchronisation: the
+    sweeps must see the new contents (the oracle on the new tensor)."""
+    c1 = synth.custom(3, 48, 6, noise_var=1e-4, seed=93)
+    c2 = synth.custom(3, 48, 6, noise_var=1e-4, seed=94)
+    s = torch.cuda.Stream()
+    T = dev_tensor(cpd, c1)
+    T2 = dev_tensor(cpd, c2)
+    torch.cuda.synchronize()
+    m = _model(cpd, c1, T, stream=s.cuda_stream)
+    m.msdt_sweep()
+    with torch.cuda.stream(s):
+        torch.cuda._sleep(2_000_000)  # the copy lands long after the host returns
+        T.copy_(T2)
+    m.set_tensor()                    # no host sync: must be ordered after the copy on `s`
+    A = synth.init_factors(c2)
+    m.set_factors(A)
+    To2 = O.make_tensor(c2)
+    nt2 = O.norm2(To2)
+    for _ in range(2):
+        f = m.msdt_sweep()
+        out = O.als_sweep(To2, A, nt2)
+        assert abs(f - out["f"]) <= TOL * abs(out["f"])
+        A = out["A"]
+    m.close()
