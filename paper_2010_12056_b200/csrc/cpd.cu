@@ -1277,9 +1277,7 @@ cpd_status pp_approx_sweep(cpd_ctx* ctx, double* fitness_out, int* still_valid) 
         if (i != nx && i != n) sp[J++] = spec(nx, i, &bytes);
       CU(cudaEventRecord(ctx->ev_pp_a, ctx->st));  // update n-1 (and everything before) enqueued
       CU(cudaStreamWaitEvent(ctx->st3, ctx->ev_pp_a, 0));
-      static const int side_ctas = getenv("CPD_PP_SIDE_CTAS") ? atoi(getenv("CPD_PP_SIDE_CTAS")) : 0;
-      CU(cpd::launch_mttv_multi(sp, J, ctx->R, ctx->Mp[nx], ctx->Mt[nx], 0, ctx->ws_mttv3, kMttvWs, ctx->st3,
-                                side_ctas));
+      CU(cpd::launch_mttv_multi(sp, J, ctx->R, ctx->Mp[nx], ctx->Mt[nx], 0, ctx->ws_mttv3, kMttvWs, ctx->st3));
       CU(cudaEventRecord(ctx->ev_pp_side[nx], ctx->st3));
       ctx->counters[2] += bytes + 8.0 * 2 * ext(ctx, nx) * ctx->R;
       ctx->counters[3] += 1;

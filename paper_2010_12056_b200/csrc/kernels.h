@@ -64,10 +64,8 @@ struct MttvSpec {
   const double* v;
   int64_t pre, K, post;
 };
-// max_ctas > 0 caps the grid (CTAs stride over the work items): a filler stream that leaves
-// room on every SM for the latency-bound kernels of the critical path
 cudaError_t launch_mttv_multi(const MttvSpec* specs, int J, int R, const double* base, double* out, int beta,
-                              double* ws, int64_t ws_elems, cudaStream_t st, int max_ctas = 0);
+                              double* ws, int64_t ws_elems, cudaStream_t st);
 
 // ---- synthetic tensor (synth/__init__.py recipe) ------------------------------------
 // T[q, z] += std*normal(seed, g) (kind 0) or T = uniform(seed, g) (kind 1) with

@@ -35,8 +35,7 @@ struct MttvJob {
 struct MttvJobs {
   MttvJob j[8];
   int J;
-  int64_t E;      // output elements (pre*C, same for every job)
-  int64_t items;  // work items over all jobs (CTAs stride over them when the grid is capped)
+  int64_t E;  // output elements (pre*C, same for every job)
 };
 
 template <bool VEC2, bool VV>
@@ -44,11 +43,10 @@ __global__ void __launch_bounds__(MT_THREADS)
     mttv_kernel(MttvJobs jobs, int R, double* __restrict__ out, int beta, double* __restrict__ ws) {
   __shared__ double red[8][MT_COLS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int64_t item = blockIdx.x; item < jobs.items; item += gridDim.x) {
   int jj = 0;
-  while (jj + 1 < jobs.J && item >= jobs.j[jj + 1].item0) jj++;
+  while (jj + 1 < jobs.J && (int64_t)blockIdx.x >= jobs.j[jj + 1].item0) jj++;
   const MttvJob& jb = jobs.j[jj];
-  const int64_t local = item - jb.item0;
+  const int64_t local = (int64_t)blockIdx.x - jb.item0;
   const int split = (int)(local % jb.ks);
   const int64_t rest = local / jb.ks;
   const int64_t p = rest / jb.nchunks;
@@ -127,8 +125,6 @@ __global__ void __launch_bounds__(MT_THREADS)
         ws[(jb.slot0 + split) * jobs.E + p * C + c] = s;
       }
     }
-  }
-  __syncthreads();  // red[] is reused by the next item
   }
 }
 
@@ -243,7 +239,7 @@ __global__ void sub_kernel(const double* __restrict__ x, const double* __restric
 }  // namespace
 
 cudaError_t launch_mttv_multi(const MttvSpec* specs, int J, int R, const double* base, double* out, int beta,
-                              double* ws, int64_t ws_elems, cudaStream_t st, int max_ctas) {
+                              double* ws, int64_t ws_elems, cudaStream_t st) {
   if (J < 1 || J > 8) return cudaErrorInvalidValue;
   MttvJobs jobs{};
   jobs.J = J;
@@ -293,8 +289,6 @@ cudaError_t launch_mttv_multi(const MttvSpec* specs, int J, int R, const double*
       one.j[0].item0 = 0;
       one.j[0].slot0 = 0;
       int64_t grid = one.j[0].pre * one.j[0].nchunks;
-      one.items = grid;
-      if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
       g_launches++;
       if (vec2 && vv)
         mttv_kernel<true, true><<<(unsigned)grid, MT_THREADS, 0, st>>>(one, R, out, q > 0 ? 1 : beta, nullptr);
@@ -305,17 +299,15 @@ cudaError_t launch_mttv_multi(const MttvSpec* specs, int J, int R, const double*
     }
     return cudaGetLastError();
   }
-  jobs.items = items;
-  const int64_t grid = (max_ctas > 0 && items > max_ctas) ? max_ctas : items;
-  if (grid > 0x7fffffff) return cudaErrorInvalidConfiguration;
+  if (items > 0x7fffffff) return cudaErrorInvalidConfiguration;
   double* w = direct ? nullptr : ws;
   g_launches++;
   if (vec2 && vv)
-    mttv_kernel<true, true><<<(unsigned)grid, MT_THREADS, 0, st>>>(jobs, R, out, beta, w);
+    mttv_kernel<true, true><<<(unsigned)items, MT_THREADS, 0, st>>>(jobs, R, out, beta, w);
   else if (vec2)
-    mttv_kernel<true, false><<<(unsigned)grid, MT_THREADS, 0, st>>>(jobs, R, out, beta, w);
+    mttv_kernel<true, false><<<(unsigned)items, MT_THREADS, 0, st>>>(jobs, R, out, beta, w);
   else
-    mttv_kernel<false, false><<<(unsigned)grid, MT_THREADS, 0, st>>>(jobs, R, out, beta, w);
+    mttv_kernel<false, false><<<(unsigned)items, MT_THREADS, 0, st>>>(jobs, R, out, beta, w);
   if (!direct) {
     g_launches++;
     int64_t blocks = (jobs.E + 255) / 256;
