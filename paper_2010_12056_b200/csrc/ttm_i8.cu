@@ -982,8 +982,11 @@ __global__ void __launch_bounds__(kThreadsD, 1)
             const int n = (a + 1) * Rp;  // diagonals 0..a
             const uint64_t ad = ad0 + (uint64_t)((a * kAPlane) >> 4);
             const uint64_t bd = bd0 + (uint64_t)(((kND - 1 - a) * Rp * 32) >> 4);  // B planes 6-a..6
-            mma_i8(dcol, ad, bd, idesc(n > 256 ? 256 : n) | AMAJ, acc);
-            if (n > 256) mma_i8(dcol + 256, ad, bd + ((256 * 32) >> 4), idesc(n - 256) | AMAJ, acc);
+            // N > 256 is split in two: at 256 (dbg 64) or in halves (multiples of 16), which keeps
+            // both MMAs wide enough that their A + B shared-memory reads stay under 128 B/clk
+            const int n1 = n <= 256 ? n : ((dbg & 64) ? 256 : (n / 2 + 15) / 16 * 16);
+            mma_i8(dcol, ad, bd, idesc(n1) | AMAJ, acc);
+            if (n > n1) mma_i8(dcol + n1, ad, bd + (uint64_t)((n1 * 32) >> 4), idesc(n - n1) | AMAJ, acc);
           }
           if (g.cl > 1) mma_commit_mc(empty0 + 8 * s, cmask);  // release the stage in every CTA
           else mma_commit(empty0 + 8 * s);
