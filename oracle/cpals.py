@@ -158,16 +158,18 @@ def make_tensor_block(cfg, ranges):
 
 def make_tensor(cfg, rank=0, world=1):
     """Local slab of T for `rank` of a 1-D partition along the last mode."""
-    lo, hi = synth.slab_range(cfg.s, rank, world)
-    ranges = [(0, cfg.s)] * (cfg.N - 1) + [(lo, hi)]
+    shape = cfg.shape
+    lo, hi = synth.slab_range(shape[-1], rank, world)
+    ranges = [(0, d) for d in shape[:-1]] + [(lo, hi)]
     return make_tensor_block(cfg, ranges)
 
 
 def make_tensor_slice(cfg, n, i):
     """The (N-1)-way slice T(..., i_n = i, ...) (for row-sampled MTTKRP checks)."""
-    ranges = [(0, cfg.s)] * cfg.N
+    shape = cfg.shape
+    ranges = [(0, d) for d in shape]
     ranges[n] = (i, i + 1)
-    return make_tensor_block(cfg, ranges).reshape([cfg.s] * (cfg.N - 1))
+    return make_tensor_block(cfg, ranges).reshape([d for m, d in enumerate(shape) if m != n])
 
 
 def mttkrp_rows(cfg, A, n, rows):

@@ -40,14 +40,18 @@ class Config:
     seed_true: int
     seed_noise: int
     seed_init: int
+    dims: tuple = None   # non-equidimensional shape (s_1..s_N); None -> (s,) * N
 
     @property
     def shape(self):
-        return (self.s,) * self.N
+        return tuple(self.dims) if self.dims else (self.s,) * self.N
 
     @property
     def numel(self):
-        return self.s ** self.N
+        n = 1
+        for d in self.shape:
+            n *= d
+        return n
 
 
 def config(c: int) -> Config:
@@ -62,12 +66,17 @@ def config(c: int) -> Config:
     return Config(name=f"C{c}", seed_true=1000 + c, seed_noise=2000 + c, seed_init=3000 + c, **table)
 
 
-def custom(N, s, R, kind="kruskal", true_rank=None, noise_var=1e-6, collinearity=-1.0, seed=7):
-    """A small ad-hoc configuration for tests (same recipe as the BASELINE configs)."""
-    return Config(name=f"N{N}s{s}R{R}", N=N, s=s, R=R, kind=kind,
+def custom(N, s, R, kind="kruskal", true_rank=None, noise_var=1e-6, collinearity=-1.0, seed=7, dims=None):
+    """A small ad-hoc configuration for tests (same recipe as the BASELINE configs); `dims`
+    gives a non-equidimensional shape (then N = len(dims) and s is unused)."""
+    if dims is not None:
+        dims = tuple(int(d) for d in dims)
+        N = len(dims)
+    name = f"N{N}s{s}R{R}" if dims is None else "x".join(map(str, dims)) + f"R{R}"
+    return Config(name=name, N=N, s=s, R=R, kind=kind,
                   true_rank=R if true_rank is None else true_rank, noise_var=noise_var,
                   collinearity=collinearity, seed_true=1000 + seed, seed_noise=2000 + seed,
-                  seed_init=3000 + seed)
+                  seed_init=3000 + seed, dims=dims)
 
 
 def gaussian_factors(shape, R, seed):

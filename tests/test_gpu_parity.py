@@ -33,8 +33,8 @@ def rel(a, b):
 
 
 def dev_tensor(cpd, cfg, rank=0, world=1):
-    lo, hi = synth.slab_range(cfg.s, rank, world)
-    shp = [cfg.s] * (cfg.N - 1) + [hi - lo]
+    lo, hi = synth.slab_range(cfg.shape[-1], rank, world)
+    shp = list(cfg.shape[:-1]) + [hi - lo]
     T = torch.empty(shp, dtype=torch.float64, device="cuda")
     if cfg.kind == "uniform":
         cpd.cpd_gen_tensor(T, cfg.shape, lo, hi, 1, None, 0.0, cfg.seed_noise)
@@ -443,3 +443,36 @@ def test_caller_stream_ordering(cpd):
         assert abs(f - out["f"]) <= TOL * abs(out["f"])
         A = out["A"]
     m.close()
+
+
+@pytest.mark.parametrize("dims,R", [((4520, 280, 280), 64), ((128, 128, 3, 7200), 32), ((1024, 1344, 33, 9), 32)])
+def test_dataset_shaped_sampled_rows(cpd, dims, R):
+    """Non-equidimensional tensors shaped like the paper's datasets (4520x280x280,
+    128x128x3x7200, 1024x1344x33x9; synthetic values only): one msdt_sweep and one
+    dt_sweep, sampled rows of every M^(n) against the oracle's explicit-KRP rows, fitness finite.
+    Exercises extents of 3 and 9 (K tails, KC boxes with one partial K step), inner modes that
+    are not multiples of 128 (D_MCP tiling) and factor images for every position."""
+    cfg = synth.custom(len(dims), 0, R, noise_var=1e-4, seed=sum(dims) % 97, dims=dims)
+    free, total = torch.cuda.mem_get_info()
+    if free < 2.5 * 8 * cfg.numel + 8e9:
+        pytest.skip("not enough device memory")
+    T = dev_tensor(cpd, cfg)
+    m = _model(cpd, cfg, T)
+    rng = np.random.default_rng(len(dims))
+    for sweep in (m.msdt_sweep, m.dt_sweep):
+        A0 = [m.get_factor(n) for n in range(cfg.N)]
+        f = sweep()
+        assert np.isfinite(f) and 0.0 < f <= 1.0
+        A1 = [m.get_factor(n) for n in range(cfg.N)]
+        for n in range(cfg.N):
+            if cfg.numel // dims[n] > 2e7:
+                continue  # the oracle's slice for this mode is too large; every root is still
+                          # exercised through the other modes' MTTKRPs
+            Ause = A1[:n] + A0[n:]   # modes < n already updated in this sweep
+            rows = rng.choice(dims[n], 2, replace=False)
+            ref = O.mttkrp_rows(cfg, Ause, n, rows)
+            got = m.get_last_mttkrp(n)[rows]
+            assert rel(got, ref) <= TOL, (n, rel(got, ref))
+    m.close()
+    del T
+    torch.cuda.empty_cache()
