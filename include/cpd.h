@@ -54,7 +54,9 @@ typedef enum {
 } cpd_status;
 
 #define CPD_MAX_ORDER 8
-#define CPD_MAX_RANK 232      /* packed Cholesky factor must fit in 227 KB of shared memory */
+#define CPD_MAX_RANK 1024     /* R <= 128: fused update with Γ^-1 (one CTA); R <= 232: packed Cholesky in one
+                                 CTA's shared memory + row solves; beyond: Γ^-1 by a grid-wide blocked
+                                 Gauss-Jordan and x = M Γ^-1 as a DMMA GEMM */
 #define CPD_NCCL_ID_BYTES 128
 
 typedef struct {

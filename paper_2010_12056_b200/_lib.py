@@ -9,7 +9,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libcpd.so")
 CPD_NCCL_ID_BYTES = 128
-CPD_MAX_RANK = 232
+CPD_MAX_RANK = 1024
 CPD_MAX_ORDER = 8
 
 STATUS = {0: "CPD_OK", 1: "CPD_ERR_INVALID_ARG", 2: "CPD_ERR_STATE", 3: "CPD_ERR_NUMERIC",

@@ -43,6 +43,7 @@ namespace {
 thread_local std::string g_init_error;
 
 constexpr int64_t kMttvWs = 1 << 22;  // doubles (32 MB) of mTTV K-split partials
+constexpr int kCholMaxR = 232;        // packed Cholesky factor in one CTA's shared memory
 
 enum Phase { PH_TTM = 0, PH_MTTV = 1, PH_SOLVE = 2, PH_HAD = 3, PH_OTHER = 4 };
 
@@ -100,6 +101,7 @@ struct cpd_ctx {
   cudaStream_t st3 = nullptr;
   cudaEvent_t ev_pp_a = nullptr, ev_pp_side[CPD_MAX_ORDER] = {};
   double* ws_mttv3 = nullptr;          // st3's mTTV K-split partials
+  double* ws_gj = nullptr;             // grid-wide Gauss-Jordan workspace (R > kCholMaxR)
   int pf_mode = -1, pf_buf = 0;        // mode whose Γ factor (and W if pf_pp) is being prepared
   bool pf_pp = false;
   bool pf_fused = false;               // the prefetch formed Γ^{-1} (fused update) rather than L
@@ -460,7 +462,7 @@ __global__ void gamma_dot_kernel(const double* __restrict__ S_all, int N, int R,
 bool use_fused(const cpd_ctx* ctx, int n, bool pp) {
   const int64_t ro = rows_own(ctx, n);
   const int blocks = cpd::update_fused_blocks(ro);
-  return ctx->Gi[0] && (ctx->world == 1 || n == ctx->N - 1) &&
+  return ctx->R <= cpd::kUpdMaxR && ctx->Gi[0] && (ctx->world == 1 || n == ctx->N - 1) &&
          cpd::update_fused_smem(ctx->R, pp, (int)((ro + blocks - 1) / blocks)) <= 225 * 1024;
 }
 
@@ -479,6 +481,10 @@ cpd_status prefetch_solve(cpd_ctx* ctx, int m, bool pp) {
   if (fz) {
     // the fused update multiplies by Γ^{-1}: form it directly (Gauss-Jordan, SPD check)
     CU(cpd::launch_gamma_inverse(ctx->S_all, ctx->N, m, ctx->R, ctx->Gi[b], ctx->status + m, ctx->st2));
+  } else if (ctx->R > kCholMaxR) {
+    // beyond the single-CTA packed Cholesky: Γ^{-1} by the grid-wide blocked Gauss-Jordan
+    CU(cpd::launch_gamma_inverse_big(ctx->S_all, ctx->N, m, ctx->R, ctx->ws_gj, ctx->Gi[b], ctx->status + m,
+                                     ctx->st2));
   } else {
     CU(cpd::launch_gamma_chol(ctx->S_all, ctx->N, m, ctx->R, ctx->Lp[b], ctx->status + m, ctx->st2));
   }
@@ -574,7 +580,10 @@ cpd_status update_mode(cpd_ctx* ctx, int n, double* Mloc, bool pp) {
   }
   {
     PhaseScope ps(ctx, PH_SOLVE);
-    CU(cpd::launch_trisolve(ctx->Lp[b], Mown, ro, R, ctx->A[n] + off * R, ctx->st));
+    if (R > kCholMaxR)  // x = M Γ^{-1} as a GEMM on the DMMA kernel
+      CU(cpd::launch_ttm(Mown, ro, R, 1, ctx->Gi[b], R, ctx->A[n] + off * R, 0, ctx->st));
+    else
+      CU(cpd::launch_trisolve(ctx->Lp[b], Mown, ro, R, ctx->A[n] + off * R, ctx->st));
   }
   if (n < ctx->N - 1 && ctx->world > 1) {
     PhaseScope ps(ctx, PH_OTHER);
@@ -885,6 +894,7 @@ cpd_status cpd_destroy(cpd_ctx* c) {
   dfree(c, c->ws_gram);
   dfree(c, c->ws_mttv);
   dfree(c, c->ws_mttv3);
+  dfree(c, c->ws_gj);
   dfree(c, c->st_part);
   dfree(c, c->upd_part);
   dfree(c, c->upd_gpart);
@@ -926,7 +936,7 @@ cpd_status cp_als_init(cpd_ctx** out, int N, const int64_t* shape, int R, const 
   if (!out || !shape || !T_local_dev || !A0_host) return fail(ctx, CPD_ERR_INVALID_ARG, "null argument");
   *out = nullptr;
   if (N < 3 || N > CPD_MAX_ORDER) return fail(ctx, CPD_ERR_INVALID_ARG, "N must be in [3, 8]");
-  if (R < 1 || R > CPD_MAX_RANK) return fail(ctx, CPD_ERR_INVALID_ARG, "R must be in [1, 232]");
+  if (R < 1 || R > CPD_MAX_RANK) return fail(ctx, CPD_ERR_INVALID_ARG, "R must be in [1, 1024]");
   cpd_opts o;
   cpd_opts_default(&o);
   if (opts) {
@@ -1044,7 +1054,7 @@ cpd_status cp_als_init(cpd_ctx** out, int N, const int64_t* shape, int R, const 
   for (int b2 = 0; b2 < 2; b2++) {
     ITRY(dalloc(ctx, &ctx->Lp[b2], RR + R));
     ITRY(dalloc(ctx, &ctx->Wb[b2], RR));
-    if (R <= cpd::kUpdMaxR) ITRY(dalloc(ctx, &ctx->Gi[b2], RR));
+    if (R <= cpd::kUpdMaxR || R > kCholMaxR) ITRY(dalloc(ctx, &ctx->Gi[b2], RR));
   }
   ICU(cudaMallocAsync((void**)&ctx->pf_status, sizeof(int) * 2, ctx->st));
   ICU(cudaMemsetAsync(ctx->pf_status, 0, sizeof(int) * 2, ctx->st));
@@ -1067,6 +1077,7 @@ cpd_status cp_als_init(cpd_ctx** out, int N, const int64_t* shape, int R, const 
   ITRY(dalloc(ctx, &ctx->ws_gram, 32 * RR));
   ITRY(dalloc(ctx, &ctx->ws_mttv, kMttvWs));
   ITRY(dalloc(ctx, &ctx->ws_mttv3, kMttvWs));
+  if (R > kCholMaxR) ITRY(dalloc(ctx, &ctx->ws_gj, (int64_t)cpd::gamma_inverse_big_ws(R)));
   ITRY(dalloc(ctx, &ctx->st_part, 3 * 64));
   ITRY(dalloc(ctx, &ctx->upd_part, 3 * cpd::kUpdMaxBlocks));
   if (R <= cpd::kUpdMaxR) ITRY(dalloc(ctx, &ctx->upd_gpart, (int64_t)cpd::kUpdMaxBlocks * 2 * RR));

@@ -22,7 +22,7 @@ cudaError_t launch_ttm(const double* X, int64_t pre, int64_t K, int64_t post, co
 // ---- the same first-level TTM on the INT8 tensor cores (tcgen05 kind::i8, exact integer
 // slicing of both FP64 operands; ttm_i8.cu).  Xexp: device int with 2^Xexp > max|X|
 // (launch_absmax_exp); ws: ttm_i8_workspace_bytes(K, ncols) bytes (sliced B + exponents).
-// K <= kMaxKI8 (int32 accumulators), ncols <= 256.
+// K <= kMaxKI8 (int32 accumulators), ncols <= 1024.
 constexpr int64_t kMaxKI8 = 16384;
 size_t ttm_i8_workspace_bytes(int64_t K, int ncols);
 // X's 7 int8 digit planes (launch_slice_digits): X viewed as [n / w, w] (w = innermost extent),
@@ -95,6 +95,11 @@ cudaError_t launch_gamma_chol(const double* S_all, int N, int n, int R, double* 
                               cudaStream_t st);
 // Γ^(n) (Eq. 1) and Ginv = Γ^{-1} (dense R x R) by Gauss-Jordan without pivoting (SPD);
 // status[0] = 1 if a pivot is not positive (Γ not SPD).  One CTA, R^2 doubles of shared memory.
+// R beyond one CTA's shared memory: the blocked Gauss-Jordan over a cooperative grid with Γ in
+// global memory; ws holds gamma_inverse_big_ws(R) doubles
+size_t gamma_inverse_big_ws(int R);
+cudaError_t launch_gamma_inverse_big(const double* S_all, int N, int n, int R, double* ws, double* Ginv,
+                                     int* status, cudaStream_t st);
 cudaError_t launch_gamma_inverse(const double* S_all, int N, int n, int R, double* Ginv, int* status,
                                  cudaStream_t st);
 // Ginv = Γ^{-1} = L^{-T} L^{-1} (dense R x R, exactly symmetric) from the packed factor; one CTA,

@@ -5,6 +5,8 @@
 // the PP second-order Hadamard sum W^(n) of Eq. 7, and the per-update
 // statistics (dA = A - base, ||dA||^2, ||A||^2, <M, A>) for Alg. 2 line 5 and Eq. 3.
 // All reductions run in a fixed order (deterministic; no floating-point atomics).
+#include <cooperative_groups.h>
+
 #include "kernels.h"
 
 #define CPD_MAXR 232
@@ -526,6 +528,98 @@ __global__ void __launch_bounds__(kGjThreads)
   if (tid == 0) status[0] = bad;
 }
 
+// --------- large R (beyond one CTA's shared memory): the same blocked Gauss-Jordan over the
+// whole grid, Γ in global memory (L2-resident: R = 1024 is 8 MB).  Per block step K:
+//   every CTA inverts the 16 x 16 pivot block A[K,K] itself (element-parallel, in shared
+//   memory: the same P everywhere, no extra grid barrier);
+//   Rb = P A[K,:] and Cb = A[:,K] by all threads -> grid sync;
+//   A[I,J] -= Cb[I] Rb[J], A[I,K] = -Cb[I] P, A[K,J] = Rb[J], A[K,K] = P -> grid sync.
+// Same pivots and the same per-element operation order as the single-CTA kernel.
+__global__ void __launch_bounds__(256)
+    gamma_inverse_big_kernel(const double* __restrict__ S_all, int N, int n, int R, double* __restrict__ A,
+                             double* __restrict__ Rb, double* __restrict__ Cb, double* __restrict__ Ginv,
+                             int* status) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int Rp = (R + kGjB - 1) / kGjB * kGjB;
+  const int64_t RR = (int64_t)R * R;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ double P[kGjB * kGjB];
+  __shared__ double pr[2][kGjB], pc[2][kGjB];
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  for (int64_t e = gt; e < (int64_t)Rp * Rp; e += nthr) {
+    const int i = (int)(e / Rp), j = (int)(e - (int64_t)i * Rp);
+    double gv = (i == j) ? 1.0 : 0.0;
+    if (i < R && j < R) {
+      bool first = true;
+      for (int k = 0; k < N; k++) {
+        if (k == n) continue;
+        const double sv = S_all[k * RR + (int64_t)i * R + j];
+        gv = first ? sv : gv * sv;
+        first = false;
+      }
+    }
+    A[e] = gv;
+  }
+  grid.sync();
+  for (int k0 = 0; k0 < Rp; k0 += kGjB) {
+    {  // pivot block inverse, redundantly in every CTA
+      const int i = threadIdx.x >> 4, j = threadIdx.x & 15;
+      double a = A[(int64_t)(k0 + i) * Rp + k0 + j];
+      if (i == 0) pr[0][j] = a;
+      if (j == 0) pc[0][i] = a;
+      __syncthreads();
+#pragma unroll 1
+      for (int p = 0; p < kGjB; p++) {
+        const int b = p & 1;
+        const double piv = pr[b][p];
+        const double inv = __drcp_rn(piv);
+        if (threadIdx.x == 0 && (!(piv > 0.0) || !isfinite(piv))) bad = 1;
+        const double r = pr[b][j] * inv, c = pc[b][i];
+        if (i == p) a = (j == p) ? inv : r;
+        else a = (j == p) ? -c * inv : fma(-c, r, a);
+        if (i == p + 1) pr[b ^ 1][j] = a;
+        if (j == p + 1) pc[b ^ 1][i] = a;
+        __syncthreads();
+      }
+      P[i * kGjB + j] = a;
+      __syncthreads();
+    }
+    for (int64_t e = gt; e < (int64_t)kGjB * Rp; e += nthr) {
+      const int m = (int)(e / Rp), c = (int)(e - (int64_t)m * Rp);
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < kGjB; q++) acc = fma(P[m * kGjB + q], A[(int64_t)(k0 + q) * Rp + c], acc);
+      Rb[e] = acc;
+      Cb[e] = A[(int64_t)c * Rp + k0 + m];
+    }
+    grid.sync();
+    for (int64_t e = gt; e < (int64_t)Rp * Rp; e += nthr) {
+      const int i = (int)(e / Rp), j = (int)(e - (int64_t)i * Rp);
+      const bool rowK = i >= k0 && i < k0 + kGjB, colK = j >= k0 && j < k0 + kGjB;
+      double v;
+      if (rowK) {
+        v = colK ? P[(i - k0) * kGjB + j - k0] : Rb[(int64_t)(i - k0) * Rp + j];
+      } else {
+        v = colK ? 0.0 : A[e];
+#pragma unroll
+        for (int m = 0; m < kGjB; m++)
+          v = fma(-Cb[(int64_t)m * Rp + i], colK ? P[m * kGjB + j - k0] : Rb[(int64_t)m * Rp + j], v);
+      }
+      A[e] = v;
+    }
+    grid.sync();
+  }
+  for (int64_t e = gt; e < RR; e += nthr) {
+    const int i = (int)(e / R), j = (int)(e - (int64_t)i * R);
+    Ginv[e] = A[(int64_t)i * Rp + j];
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) status[0] = bad;
+}
+
 size_t gamma_inverse_smem(int R) {
   const size_t Rp = (size_t)(R + kGjB - 1) / kGjB * kGjB;
   return sizeof(double) * (Rp * (Rp + 1) + 2 * kGjB * Rp + kGjB * kGjB);
@@ -545,6 +639,29 @@ cudaError_t opt_in_smem(K kern) {
 }
 
 }  // namespace
+
+size_t gamma_inverse_big_ws(int R) {
+  const size_t Rp = (size_t)(R + kGjB - 1) / kGjB * kGjB;
+  return Rp * Rp + 2 * kGjB * Rp;
+}
+
+cudaError_t launch_gamma_inverse_big(const double* S_all, int N, int n, int R, double* ws, double* Ginv,
+                                     int* status, cudaStream_t st) {
+  if (R < 1) return cudaErrorInvalidValue;
+  const int Rp = (R + kGjB - 1) / kGjB * kGjB;
+  double* A = ws;
+  double* Rb = ws + (size_t)Rp * Rp;
+  double* Cb = Rb + (size_t)kGjB * Rp;
+  int dev = 0, nsm = 148, per = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gamma_inverse_big_kernel, 256, 0);
+  int blocks = std::max(1, std::min(nsm * std::max(per, 1), (int)(((int64_t)Rp * Rp + 255) / 256)));
+  void* args[] = {&S_all, &N, &n, &R, &A, &Rb, &Cb, &Ginv, &status};
+  g_launches++;
+  return cudaLaunchCooperativeKernel((void*)gamma_inverse_big_kernel, blocks, 256, args, 0, st);
+}
+
 
 cudaError_t launch_gram(const double* X, const double* Y1, const double* Y2, int64_t rows, int R,
                         double* G1, double* G2, double* ws, int64_t ws_elems, cudaStream_t st) {

@@ -694,7 +694,8 @@ enum { D_KC = 0, D_MC128 = 1, D_MC64 = 2, D_MC32 = 3, D_MCP = 4 };
 constexpr int kStagesD = 5;
 constexpr int kEpiWarps = 16;                        // 4 per TMEM lane quarter
 constexpr int kThreadsD = 32 * (2 + kEpiWarps);
-constexpr int kSmemD = kStagesD * kDStage + 256 + 256 * 8;  // stages, barriers, column scales
+constexpr int kMaxColsI8 = 1024;  // output columns (R) of one TTM: column scales in shared memory
+constexpr int kSmemD = kStagesD * kDStage + 256 + kMaxColsI8 * 8;  // stages, barriers, column scales
 static_assert(kSmemD <= 232448, "smem");
 
 // UMMA descriptor with a swizzle layout type (2 = 128B, 4 = 64B, 6 = 32B), base offset 0
@@ -1207,7 +1208,7 @@ cudaError_t run_i8d(int grid, const Geo& g, const uint8_t* Bimg, const int* F, c
 
 size_t ttm_i8_workspace_bytes(int64_t K, int ncols) {
   Geo g = make_geo(1, K, 1, ncols);
-  return (size_t)g.ntn * g.nkc * kND * g.Rp * 32 + 256 * sizeof(int);
+  return (size_t)g.ntn * g.nkc * kND * g.Rp * 32 + kMaxColsI8 * sizeof(int);
 }
 
 cudaError_t launch_absmax_exp(const double* x, int64_t n, double* partial, int* e_out, cudaStream_t st,
@@ -1249,10 +1250,10 @@ cudaError_t launch_ttm_i8(const double* X, int64_t pre, int64_t K, int64_t post,
                           double* out, int beta, const int* Xexp, void* ws, size_t ws_bytes, cudaStream_t st,
                           const DigitView* dv) {
   if (pre <= 0 || post <= 0 || ncols <= 0) return cudaSuccess;
-  if (K <= 0 || K > kMaxKI8 || ncols > 256) return cudaErrorInvalidValue;
+  if (K <= 0 || K > kMaxKI8 || ncols > kMaxColsI8) return cudaErrorInvalidValue;
   Geo g = make_geo(pre, K, post, ncols);
   const size_t img = (size_t)g.ntn * g.nkc * kND * g.Rp * 32;
-  if (ws_bytes < img + 256 * sizeof(int)) return cudaErrorInvalidValue;
+  if (ws_bytes < img + kMaxColsI8 * sizeof(int)) return cudaErrorInvalidValue;
   uint8_t* Bimg = static_cast<uint8_t*>(ws);
   int* F = reinterpret_cast<int*>(static_cast<uint8_t*>(ws) + img);
   g_launches += 3;

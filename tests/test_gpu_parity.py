@@ -476,3 +476,30 @@ def test_dataset_shaped_sampled_rows(cpd, dims, R):
     m.close()
     del T
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("ttm_impl", [0, 1])
+@pytest.mark.parametrize("dims,R", [((310, 260, 24), 300), ((40, 36, 530), 520)])
+def test_large_rank_sweeps(cpd, dims, R, ttm_impl):
+    """R beyond one CTA's shared memory (CPD_MAX_RANK 1024): Γ^-1 by the grid-wide blocked
+    Gauss-Jordan, x = M Γ^-1 as a DMMA GEMM, the int8 TTM with 5-9 N tiles; two MSDT sweeps,
+    one DT sweep, pp_init and one approximated sweep, each state-synchronised with the oracle."""
+    cfg = synth.custom(3, 0, R, noise_var=1e-4, seed=R % 89, dims=dims)
+    To = O.make_tensor(cfg)
+    nt2 = O.norm2(To)
+    T = dev_tensor(cpd, cfg)
+    m = _model(cpd, cfg, T, ttm_impl=ttm_impl)
+    A = synth.init_factors(cfg)
+    for sweep in (m.msdt_sweep, m.msdt_sweep, m.dt_sweep):
+        f = sweep()
+        out = O.als_sweep(To, A, nt2)
+        assert abs(f - out["f"]) <= TOL * abs(out["f"]), (f, out["f"])
+        for n in range(3):
+            assert rel(m.get_factor(n), out["A"][n]) <= 1e-8, (n, rel(m.get_factor(n), out["A"][n]))
+        A = [m.get_factor(n) for n in range(3)]   # state-synchronised
+    m.pp_init()
+    st = O.pp_init(To, A)
+    f, _ = m.pp_approx_sweep()
+    out = O.pp_approx_sweep(st, A, nt2)
+    assert abs(f - out["f"]) <= TOL * abs(out["f"]), (f, out["f"])
+    m.close()
