@@ -298,14 +298,20 @@ def pp_approx_sweep(st: PPState, A, normT2, eps=None):
     return dict(A=A, S=S, M=Ms, V=Vs, f=f, r=r, still_valid=valid, dA=dA)
 
 
-def pp_controller_run(T, A0, eps, delta=1e-5, max_sweeps=300, max_pp_run=None):
-    """Alg. 2 driver with reading Q21 (fitness after every sweep, Δ test
-    on consecutive sweeps of any kind).  Returns the list of (kind, f)."""
+def pp_controller_run(T, A0, eps, delta=1e-5, max_sweeps=300, max_pp_run=None, stop_test="any"):
+    """Alg. 2 driver; fitness after every sweep (reading Q21).  Stop test:
+    "any" (default, reading Q21) -- Δ between neighbouring sweeps of any kind (the P:931 wording);
+    "regular" -- Alg. 2 as printed (lines 3-4, 19-21): r is updated only
+      after a regular sweep and the loop ends when |r - r_old| <= Δ between consecutive regular
+      sweeps (r = 1, r_old = 0 initially); approximated sweeps are traced, not tested.
+    Returns (A, [(kind, f)])."""
     normT2 = norm2(T)
     A = [a.copy() for a in A0]
     dA = [a.copy() for a in A]          # Alg. 2 line 2: dA <- A
     trace, f_old = [], None
+    f_reg_old = 0.0                     # r = 1 before the first regular sweep (line 3)
     while len(trace) < max_sweeps:
+        stop = False
         if pp_condition(dA, A, eps):
             st = pp_init(T, A)
             trace.append(("pp_init", None))
@@ -315,19 +321,24 @@ def pp_controller_run(T, A0, eps, delta=1e-5, max_sweeps=300, max_pp_run=None):
                 A = out["A"]
                 trace.append(("pp_approx", out["f"]))
                 n_run += 1
-                stop = f_old is not None and abs(out["f"] - f_old) <= delta
+                if stop_test == "any":
+                    stop = f_old is not None and abs(out["f"] - f_old) <= delta
                 f_old = out["f"]
                 if stop or not out["still_valid"] or len(trace) >= max_sweeps or \
                         (max_pp_run is not None and n_run >= max_pp_run):
                     break
-            if stop:
+            if stop or len(trace) >= max_sweeps:
                 break
         out = als_sweep(T, A, normT2)
         A, dA = out["A"], out["dA"]
         trace.append(("regular", out["f"]))
-        if f_old is not None and abs(out["f"] - f_old) <= delta:
+        if stop_test == "any":
+            if f_old is not None and abs(out["f"] - f_old) <= delta:
+                break
+        elif abs(out["f"] - f_reg_old) <= delta:
             break
         f_old = out["f"]
+        f_reg_old = out["f"]
     return A, trace
 
 

@@ -42,18 +42,19 @@ def _dev_tensor(cpd, cfg):
 CASES = [(3, 64, 8, 1e-6, 1001, 0.2, 1e-9, 4), (4, 12, 4, 1e-3, 17, 0.2, 1e-8, 3)]
 
 
+@pytest.mark.parametrize("stop_test", ["regular", "any"])
 @pytest.mark.parametrize("case", CASES)
-def test_alg2_controller_matches_oracle(cpd, case):
+def test_alg2_controller_matches_oracle(cpd, case, stop_test):
     from paper_2010_12056_b200 import driver
     N, s, R, nv, seed, eps, delta, mpr = case
     cfg = synth.custom(N, s, R, noise_var=nv, seed=seed)
     To = O.make_tensor(cfg)
     A0 = synth.init_factors(cfg)
-    _, tr_o = O.pp_controller_run(To, A0, eps, delta=delta, max_sweeps=80, max_pp_run=mpr)
+    _, tr_o = O.pp_controller_run(To, A0, eps, delta=delta, max_sweeps=80, max_pp_run=mpr, stop_test=stop_test)
     T = _dev_tensor(cpd, cfg)
     m = cpd.cp_als_init(T, cfg.shape, cfg.R, A0, pp_eps=eps)
     buf = io.StringIO()
-    rows = driver.pp_cp_als(m, delta=delta, max_sweeps=80, max_pp_run=mpr, trace=buf)
+    rows = driver.pp_cp_als(m, delta=delta, max_sweeps=80, max_pp_run=mpr, trace=buf, stop_test=stop_test)
     m.close()
     kinds_o = [k for k, _ in tr_o]
     kinds_g = [r[1] for r in rows]

@@ -5,7 +5,9 @@ P:819-853): order-3 exact CP tensors s x s x s whose factor columns have pairwis
 factors (Alg. 2 line 2), stopped at Δf <= 1e-5 between neighbouring sweeps or 300
 sweeps.  The paper uses s = 1600, R = 400 on 64 KNL processes; R here is capped by
 the library (CPD_MAX_RANK 232).
-usage: python tools/collinearity_study.py [s] [R] [seeds] [max_sweeps] -> one JSON line per run"""
+usage: python tools/collinearity_study.py [s] [R] [seeds] [max_sweeps] [any|regular]
+(the Δ stop test: neighbouring sweeps of any kind, reading Q21, or consecutive regular sweeps
+as Alg. 2 prints it) -> one JSON line per run"""
 import json
 import os
 import sys
@@ -24,6 +26,7 @@ s = int(sys.argv[1]) if len(sys.argv) > 1 else 1600
 R = int(sys.argv[2]) if len(sys.argv) > 2 else 200
 seeds = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 max_sweeps = int(sys.argv[4]) if len(sys.argv) > 4 else 300
+stop_test = sys.argv[5] if len(sys.argv) > 5 else "any"
 stream = torch.cuda.Stream()
 for b in range(5):
     lo, hi = 0.2 * b, 0.2 * (b + 1)
@@ -40,13 +43,13 @@ for b in range(5):
             m = cpd.cp_als_init(T, cfg.shape, R, A0, stream=stream, pp_eps=eps)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            rows = pp_cp_als(m, delta=1e-5, max_sweeps=max_sweeps, regular=regular)
+            rows = pp_cp_als(m, delta=1e-5, max_sweeps=max_sweeps, regular=regular, stop_test=stop_test)
             torch.cuda.synchronize()
             wall = time.perf_counter() - t0
             fits = [r[3] for r in rows if r[3] is not None]
             res[name] = {"wall_s": wall, "counts": phase_counts(rows), "final_fitness": fits[-1]}
             m.close()
-        print(json.dumps({"s": s, "R": R, "bin": [round(lo, 1), round(hi, 1)], "C": C, "seed": seed,
+        print(json.dumps({"s": s, "R": R, "stop_test": stop_test, "bin": [round(lo, 1), round(hi, 1)], "C": C, "seed": seed,
                           "runs": res, "pp_speedup_vs_dt": res["dt"]["wall_s"] / res["pp"]["wall_s"],
                           "pp_speedup_vs_msdt": res["msdt"]["wall_s"] / res["pp"]["wall_s"],
                           "msdt_speedup_vs_dt": res["dt"]["wall_s"] / res["msdt"]["wall_s"]}), flush=True)
