@@ -3,8 +3,7 @@ P:819-853): order-3 exact CP tensors s x s x s whose factor columns have pairwis
 (construction Q13), C drawn from [a, b) per bin with a seeded RNG; PP-CP-ALS
 (Alg. 2, ε = 0.2, MSDT regular sweeps), MSDT ALS and DT ALS from the same U[0,1] initial
 factors (Alg. 2 line 2), stopped at Δf <= 1e-5 between neighbouring sweeps or 300
-sweeps.  The paper uses s = 1600, R = 400 on 64 KNL processes; R here is capped by
-the library (CPD_MAX_RANK 232).
+sweeps.  The paper uses s = 1600, R = 400 on 64 KNL processes.
 usage: python tools/collinearity_study.py [s] [R] [seeds] [max_sweeps] [any|regular]
 (the Δ stop test: neighbouring sweeps of any kind, reading Q21, or consecutive regular sweeps
 as Alg. 2 prints it) -> one JSON line per run"""
