@@ -266,7 +266,7 @@ def test_errors(cpd):
     assert e.value.status == 1
     m.close()
     with pytest.raises(cpd.CPDError) as e:
-        cpd.cp_als_init(T, cfg.shape, 300, synth.init_factors(cfg))
+        cpd.cp_als_init(T, cfg.shape, cpd.CPD_MAX_RANK + 1, synth.init_factors(cfg))
     assert e.value.status == 1
     # rank-deficient factors -> Γ not SPD
     A0 = synth.init_factors(cfg)
