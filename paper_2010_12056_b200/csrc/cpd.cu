@@ -85,7 +85,12 @@ struct cpd_ctx {
   int64_t T_elems = 0;
   cpd_opts opts{};
   // factors: mode N-1 holds only the local slab rows
-  std::vector<double*> A, Aold, dA, Mlast, Ap, Mp, Mt;
+  std::vector<double*> A, Aold, dA, Mlast, Ap, Mp, Mt, Mt2;
+  // PP sweeps alternate between the M~ buffer sets Mt / Mt2 (mt_par): at the end of a sweep the
+  // filler stream already starts the next sweep's mode-1 independent streams into the other set
+  // (pp_spec); any call other than pp_approx_sweep first waits for that work and drops it
+  int mt_par = 0;
+  bool pp_spec = false;
   std::vector<double*> Mlast_src;  // non-null: the last M of mode n lives there (PP: Mt[n])
   double* S_all = nullptr;   // N x R x R
   double* dS_all = nullptr;  // N x R x R
@@ -652,16 +657,21 @@ void free_pp(cpd_ctx* c) {
       c->Mlast_src[n] = nullptr;
     }
   for (auto& p : c->Mt) dfree(c, p);
+  for (auto& p : c->Mt2) dfree(c, p);
   c->pp_valid = false;
 }
 
 // orders a public call's work after the caller's stream and the caller's stream after it
 struct UserSync {
   cpd_ctx* c;
-  explicit UserSync(cpd_ctx* ctx) : c(ctx) {
+  explicit UserSync(cpd_ctx* ctx, bool keep_spec = false) : c(ctx) {
     if (c && c->ev_in) {
       cudaEventRecord(c->ev_in, c->ust);
       cudaStreamWaitEvent(c->st, c->ev_in, 0);
+    }
+    if (c && c->pp_spec && !keep_spec) {  // speculative PP work must finish before anything else
+      cudaStreamWaitEvent(c->st, c->ev_pp_side[1], 0);
+      c->pp_spec = false;
     }
   }
   ~UserSync() {
@@ -877,9 +887,11 @@ const char* cpd_last_error(const cpd_ctx* c) { return c ? c->err.c_str() : g_ini
 cpd_status cpd_destroy(cpd_ctx* c) {
   if (!c) return CPD_OK;
   cudaSetDevice(c->dev);
+  if (c->st2) cudaStreamSynchronize(c->st2);  // side and filler (speculative PP) work first
+  if (c->st3) cudaStreamSynchronize(c->st3);
   clear_subtree(c);
   free_pp(c);
-  for (auto* v : {&c->A, &c->Aold, &c->dA, &c->Mlast, &c->Ap, &c->Mp, &c->Mt})
+  for (auto* v : {&c->A, &c->Aold, &c->dA, &c->Mlast, &c->Ap, &c->Mp, &c->Mt, &c->Mt2})
     for (auto& p : *v) dfree(c, p);
   dfree(c, c->S_all);
   dfree(c, c->dS_all);
@@ -1040,6 +1052,7 @@ cpd_status cp_als_init(cpd_ctx** out, int N, const int64_t* shape, int R, const 
   ctx->Ap.assign(N, nullptr);
   ctx->Mp.assign(N, nullptr);
   ctx->Mt.assign(N, nullptr);
+  ctx->Mt2.assign(N, nullptr);
   ctx->Mlast_src.assign(N, nullptr);
   for (int n = 0; n < N; n++) {
     int64_t e = ext(ctx, n) * R;
@@ -1246,6 +1259,7 @@ cpd_status pp_init(cpd_ctx* ctx) {
     int a = std::min(n, o), b = std::max(n, o);
     TRY(dalloc(ctx, &ctx->Mp[n], ext(ctx, n) * ctx->R));
     TRY(dalloc(ctx, &ctx->Mt[n], ext(ctx, n) * ctx->R));
+    TRY(dalloc(ctx, &ctx->Mt2[n], ext(ctx, n) * ctx->R));
     TRY(mttv(ctx, ctx->ops[{a, b}], {a, b}, o, ctx->Ap[o], ctx->Mp[n], 0));
   }
   CU(cudaStreamSynchronize(ctx->st));
@@ -1259,7 +1273,7 @@ cpd_status pp_init(cpd_ctx* ctx) {
 
 cpd_status pp_approx_sweep(cpd_ctx* ctx, double* fitness_out, int* still_valid) {
   TRY(check_ctx(ctx));
-  UserSync us_(ctx);
+  UserSync us_(ctx, true);
   if (!ctx->pp_valid || !ctx->pp_regime) return fail(ctx, CPD_ERR_STATE, "pp_approx_sweep needs a valid pp_init");
   const int N = ctx->N;
   // operator [s_a, s_b, R] of the pair {n, i}: contract the axis of mode i with dA^(i) (Eq. 6)
@@ -1278,22 +1292,30 @@ cpd_status pp_approx_sweep(cpd_ctx* ctx, double* fitness_out, int* still_valid) 
   // the other N-2 streams of mode n (their dA are final once update n-2 is done) are issued on
   // st3 one mode ahead, into Mt[n] = M_p^(n) + Σ_indep U, and the main stream adds U^(n,n-1).
   // Fixed summation order: ((M_p + Σ_indep U in ascending i) + U^(n,n-1)).
+  double* const* Mcur = ctx->mt_par ? ctx->Mt2.data() : ctx->Mt.data();
+  double* const* Mnxt = ctx->mt_par ? ctx->Mt.data() : ctx->Mt2.data();
+  // the independent streams of mode nx (all i != nx, nx-1) on the filler stream into M[nx]
+  auto side = [&](int nx, double* const* M) -> cpd_status {
+    cpd::MttvSpec sp[CPD_MAX_ORDER];
+    int J = 0;
+    double bytes = 0.0;
+    for (int i = 0; i < N; i++)
+      if (i != nx && i != nx - 1) sp[J++] = spec(nx, i, &bytes);
+    CU(cudaEventRecord(ctx->ev_pp_a, ctx->st));  // update nx-2 (and everything before) enqueued
+    CU(cudaStreamWaitEvent(ctx->st3, ctx->ev_pp_a, 0));
+    CU(cpd::launch_mttv_multi(sp, J, ctx->R, ctx->Mp[nx], M[nx], 0, ctx->ws_mttv3, kMttvWs, ctx->st3));
+    CU(cudaEventRecord(ctx->ev_pp_side[nx], ctx->st3));
+    ctx->counters[2] += bytes + 8.0 * 2 * ext(ctx, nx) * ctx->R;
+    ctx->counters[3] += 1;
+    return CPD_OK;
+  };
   for (int n = 0; n < N; n++) {
     const int nx = n + 1;
     if (nx < N && N > 2) {
-      cpd::MttvSpec sp[CPD_MAX_ORDER];
-      int J = 0;
-      double bytes = 0.0;
-      for (int i = 0; i < N; i++)
-        if (i != nx && i != n) sp[J++] = spec(nx, i, &bytes);
-      CU(cudaEventRecord(ctx->ev_pp_a, ctx->st));  // update n-1 (and everything before) enqueued
-      CU(cudaStreamWaitEvent(ctx->st3, ctx->ev_pp_a, 0));
-      CU(cpd::launch_mttv_multi(sp, J, ctx->R, ctx->Mp[nx], ctx->Mt[nx], 0, ctx->ws_mttv3, kMttvWs, ctx->st3));
-      CU(cudaEventRecord(ctx->ev_pp_side[nx], ctx->st3));
-      ctx->counters[2] += bytes + 8.0 * 2 * ext(ctx, nx) * ctx->R;
-      ctx->counters[3] += 1;
+      if (nx == 1 && ctx->pp_spec) ctx->pp_spec = false;  // started at the end of the last sweep
+      else TRY(side(nx, Mcur));
     }
-    double* Mt = ctx->Mt[n];
+    double* Mt = Mcur[n];
     cpd::MttvSpec sp[CPD_MAX_ORDER];
     int J = 0;
     double bytes = 0.0;
@@ -1314,6 +1336,15 @@ cpd_status pp_approx_sweep(cpd_ctx* ctx, double* fitness_out, int* still_valid) 
     ctx->counters[3] += 1;
     TRY(update_mode(ctx, n, Mt, true));
   }
+  // speculation: the next sweep's mode-1 independent streams need only this sweep's final dA,
+  // so they start now and overlap the end of this sweep and the host round trip; this sweep's
+  // M~ (readable through cpd_get_last_mttkrp) stays intact in the other buffer set
+  static const bool no_spec = getenv("CPD_NO_PP_SPEC") != nullptr;
+  if (N > 2 && !no_spec) {
+    TRY(side(1, Mnxt));
+    ctx->pp_spec = true;
+  }
+  ctx->mt_par ^= 1;
   TRY(finish_sweep(ctx, fitness_out));
   if (still_valid) *still_valid = pp_cond(ctx) ? 1 : 0;
   return CPD_OK;
