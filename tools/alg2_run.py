@@ -5,7 +5,7 @@ and Figs. 5-6 compare the same three runs on CPU clusters):
   * DT ALS      plain CP-ALS on the standard dimension tree,
 all from the same seeded tensor and initial factors, stopping when the fitness of two
 neighbouring sweeps differs by <= delta or after max_sweeps.
-usage: python tools/alg2_run.py [config] [max_sweeps] [delta]  -> one JSON line per run"""
+usage: python tools/alg2_run.py [config] [max_sweeps] [delta] [any|regular]  -> one JSON line per run"""
 import json
 import os
 import sys
@@ -22,6 +22,7 @@ from paper_2010_12056_b200.driver import phase_counts, pp_cp_als  # noqa: E402
 c = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 max_sweeps = int(sys.argv[2]) if len(sys.argv) > 2 else 300
 delta = float(sys.argv[3]) if len(sys.argv) > 3 else 1e-5
+stop_test = sys.argv[4] if len(sys.argv) > 4 else "any"
 cfg = synth.config(c)
 eps = 0.2 if c == 4 else 0.1
 stream = torch.cuda.Stream()
@@ -35,7 +36,7 @@ for name, kw, regular in [("pp_cp_als", {"pp_eps": eps}, "msdt"),
     m = cpd.cp_als_init(T, cfg.shape, cfg.R, A0, stream=stream, **kw)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    rows = pp_cp_als(m, delta=delta, max_sweeps=max_sweeps, regular=regular)
+    rows = pp_cp_als(m, delta=delta, max_sweeps=max_sweeps, regular=regular, stop_test=stop_test)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     per = {}
@@ -43,7 +44,7 @@ for name, kw, regular in [("pp_cp_als", {"pp_eps": eps}, "msdt"),
         per.setdefault(r[1], []).append(r[4])
     fits = [r[3] for r in rows if r[3] is not None]
     print(json.dumps({
-        "config": cfg.name, "run": name, "eps": kw["pp_eps"] if name == "pp_cp_als" else None, "delta": delta,
+        "config": cfg.name, "run": name, "stop_test": stop_test, "eps": kw["pp_eps"] if name == "pp_cp_als" else None, "delta": delta,
         "sweeps": len(fits), "phase_counts": phase_counts(rows), "wall_s": wall,
         "ms_per_phase": {k: 1e3 * sum(v) / len(v) for k, v in per.items()},
         "final_fitness": fits[-1] if fits else None, "ttm_engine": m.ttm_engine(),
