@@ -170,7 +170,8 @@ def test_c1_early_pp_exercises_second_order(cpd, early):
 
 
 @pytest.mark.parametrize("ttm_impl", [0, 1])
-@pytest.mark.parametrize("N,s,R", [(4, 12, 5), (5, 6, 3), (3, 40, 24), (6, 4, 2), (4, 72, 6), (7, 3, 2), (8, 3, 3)])
+@pytest.mark.parametrize("N,s,R", [(4, 12, 5), (5, 6, 3), (3, 40, 24), (6, 4, 2), (4, 72, 6), (7, 3, 2), (8, 3, 3),
+                                   (3, 56, 64)])
 def test_msdt_and_dt_sweeps_order_N(cpd, N, s, R, ttm_impl):
     cfg = synth.custom(N, s, R, noise_var=1e-4, seed=N * 10 + s)
     T = dev_tensor(cpd, cfg)
@@ -195,7 +196,7 @@ def test_msdt_and_dt_sweeps_order_N(cpd, N, s, R, ttm_impl):
         m.close()
 
 
-@pytest.mark.parametrize("N,s,R", [(4, 10, 4), (5, 6, 3), (6, 4, 2), (8, 3, 2)])
+@pytest.mark.parametrize("N,s,R", [(4, 10, 4), (5, 6, 3), (6, 4, 2), (8, 3, 2), (3, 48, 64), (4, 20, 128)])
 def test_pp_order_N_state_synchronised(cpd, N, s, R):
     cfg = synth.custom(N, s, R, noise_var=1e-3, seed=N + 40)
     T = dev_tensor(cpd, cfg)
