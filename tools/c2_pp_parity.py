@@ -5,7 +5,7 @@ stream, the speculative next-sweep streams, the fused update with the V term).  
 its own PP state from the GPU's factors at pp_init (Eq. 4 with explicit partial Khatri-Rao
 products) and runs the same number of approximated sweeps from them (Eqs. 5-8): the fitness of
 every sweep (tolerance 1e-10) and the final factors and M~^(n) are compared.
-usage: python tools/c2_pp_parity.py [pp_sweeps] -> one JSON line"""
+usage: python tools/c2_pp_parity.py [pp_sweeps] [config] -> one JSON line (config 2 by default; ε = 0.2 for C4)"""
 import json
 import os
 import sys
@@ -21,12 +21,14 @@ import paper_2010_12056_b200 as cpd  # noqa: E402
 import synth  # noqa: E402
 
 npp = int(sys.argv[1]) if len(sys.argv) > 1 else 3
-cfg = synth.config(2)
+c = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+cfg = synth.config(c)
+eps = 0.2 if c == 4 else 0.1
 stream = torch.cuda.Stream()
 with torch.cuda.stream(stream):
     T = bench.make_slab(cpd, torch, cfg, 0, 1, stream)
 torch.cuda.synchronize()
-m = cpd.cp_als_init(T, cfg.shape, cfg.R, synth.init_factors(cfg), stream=stream, pp_eps=0.1)
+m = cpd.cp_als_init(T, cfg.shape, cfg.R, synth.init_factors(cfg), stream=stream, pp_eps=eps)
 pre = 0
 while pre < 60:
     m.msdt_sweep()
@@ -51,7 +53,7 @@ st = O.pp_init(To, A_init)
 rows = []
 A = A_init
 for k in range(npp):
-    out = O.pp_approx_sweep(st, A, nt2, 0.1)   # the oracle's own trajectory from A_init
+    out = O.pp_approx_sweep(st, A, nt2, eps)   # the oracle's own trajectory from A_init
     A = out["A"]
     f, valid = f_gpu[k]
     row = {"pp_sweep": k + 1, "f_gpu": f, "f_oracle": out["f"], "rel_df": abs(f - out["f"]) / abs(out["f"]),
@@ -62,7 +64,7 @@ for k in range(npp):
                          for n in range(cfg.N)]
     rows.append(row)
     print(json.dumps(row), file=sys.stderr, flush=True)
-print(json.dumps({"config": "C2", "presweeps": pre, "pp_sweeps": npp, "tolerance": 1e-10,
+print(json.dumps({"config": cfg.name, "presweeps": pre, "pp_sweeps": npp, "tolerance": 1e-10,
                   "max_rel_df": max(r["rel_df"] for r in rows), "final_rel_dA": max(rows[-1]["rel_dA"]),
                   "final_rel_dM": max(rows[-1]["rel_dM"]),
                   "pass": all(r["rel_df"] <= 1e-10 for r in rows) and max(rows[-1]["rel_dM"]) <= 1e-10,
