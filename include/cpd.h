@@ -214,6 +214,13 @@ cpd_status cpd_ttm(const double* T_dev, int64_t pre, int64_t K, int64_t post,
  * next sweep is a regular one).  Collective when world > 1. */
 cpd_status cpd_set_tensor(cpd_ctx* ctx);
 
+/* Status of the last completed sweep's fitness (Eq. 3): *flags bit 0 is set when the
+ * radicand ||T||^2 + <Γ^(N),S^(N)> - 2<M^(N),A^(N)> fell below -1e-8 ||T||^2 -- not rounding:
+ * M (an approximated M~) and A are inconsistent, as after a PP sweep forced outside the ε regime
+ * (Alg. 2 line 10), and the reported fitness is the clamped value 1.  *radicand_rel (may be NULL)
+ * = radicand / ||T||^2.  Host values, no device work. */
+cpd_status cpd_last_sweep_status(const cpd_ctx* ctx, int* flags, double* radicand_rel);
+
 /* *engine = the first-level TTM engine this ctx chose at init (CPD_ENGINE_*). */
 cpd_status cpd_ttm_engine(const cpd_ctx* ctx, int* engine);
 

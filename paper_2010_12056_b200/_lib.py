@@ -20,6 +20,7 @@ EXPORTED_SYMBOLS = [
     "pp_approx_sweep", "fitness", "cpd_pp_condition", "cpd_get_factor", "cpd_get_last_mttkrp",
     "cpd_set_factors", "cpd_get_phase_ms", "cpd_get_counters", "cpd_reset_counters",
     "cpd_debug_get_pp_operator", "cpd_last_error", "cpd_destroy", "cpd_gen_tensor", "cpd_ttm", "cpd_ttm_i8", "cpd_ttm_engine", "cpd_set_tensor",
+    "cpd_last_sweep_status",
     "cpd_mttv", "cpd_local_group_create", "cpd_local_group_destroy", "cpd_set_profile_level",
 ]
 
@@ -75,6 +76,7 @@ def load_library():
                                      C.POINTER(_D), C.c_int, C.c_double, C.c_uint64, _P]),
         "cpd_ttm": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, _P, C.c_int, _P, _P]),
         "cpd_ttm_engine": (C.c_int, [_P, C.POINTER(C.c_int)]),
+        "cpd_last_sweep_status": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_double)]),
         "cpd_set_tensor": (C.c_int, [_P]),
         "cpd_ttm_i8": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, _P, C.c_int, _P, C.c_int, _P]),
         "cpd_mttv": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, C.c_int, _P, _P, C.c_int, _P]),

@@ -131,6 +131,8 @@ struct cpd_ctx {
   bool pp_regime = false;    // dA = A - A_p (PP) vs one-sweep update (regular)
   bool have_fit = false;
   double last_f = 0.0, last_r = 0.0;
+  int last_flags = 0;          // cpd_last_sweep_status: bit 0 = Eq. 3 radicand < -1e-8 ||T||^2
+  double last_rad_rel = 0.0;   // the last sweep's Eq. 3 radicand / ||T||^2
   bool have_dA = false;
   double dA2[CPD_MAX_ORDER] = {0}, A2[CPD_MAX_ORDER] = {0};
   // diagnostics
@@ -627,6 +629,10 @@ cpd_status finish_sweep(cpd_ctx* ctx, double* f_out) {
   const double nt2 = ctx->hscal[SC_NT2];
   const double rad = nt2 + ctx->hscal[SC_GS] - 2.0 * ctx->hscal[SC_MA];
   if (!std::isfinite(rad)) return fail(ctx, CPD_ERR_NUMERIC, "non-finite residual");
+  // Eq. 3 cannot be negative beyond rounding: a (forced) approximated sweep outside the ε regime
+  // left M~ and A inconsistent; the fitness is then clamped (f = 1) and flagged
+  ctx->last_flags = rad < -1e-8 * nt2 ? 1 : 0;
+  ctx->last_rad_rel = rad / nt2;
   ctx->last_r = std::sqrt(std::max(rad, 0.0)) / std::sqrt(nt2);
   ctx->last_f = 1.0 - ctx->last_r;
   ctx->have_fit = true;
@@ -1412,6 +1418,13 @@ cpd_status cpd_get_phase_ms(cpd_ctx* ctx, double out[5]) {
   cudaStreamSynchronize(ctx->st);
   drain_timers(ctx);
   for (int i = 0; i < 5; i++) out[i] = ctx->phase_ms[i];
+  return CPD_OK;
+}
+
+cpd_status cpd_last_sweep_status(const cpd_ctx* ctx, int* flags, double* radicand_rel) {
+  if (!ctx || !flags) return CPD_ERR_INVALID_ARG;
+  *flags = ctx->last_flags;
+  if (radicand_rel) *radicand_rel = ctx->last_rad_rel;
   return CPD_OK;
 }
 

@@ -130,6 +130,13 @@ class CPDecomposition:
         check(self._lib.cpd_ttm_engine(self._ctx, C.byref(e)), self._ctx)
         return {0: "dmma", 1: "int8-digits", 2: "int8-convert"}[e.value]
 
+    def last_sweep_status(self) -> dict:
+        """Eq. 3 status of the last sweep: {"radicand_negative": bool, "radicand_rel": float}
+        (cpd_last_sweep_status; a set flag means the reported fitness is the clamped 1)."""
+        fl, rr = C.c_int(), C.c_double()
+        check(self._lib.cpd_last_sweep_status(self._ctx, C.byref(fl), C.byref(rr)), self._ctx)
+        return {"radicand_negative": bool(fl.value & 1), "radicand_rel": rr.value}
+
     def close(self):
         if getattr(self, "_ctx", None) is not None and self._ctx.value:
             self._lib.cpd_destroy(self._ctx)

@@ -504,3 +504,31 @@ def test_large_rank_sweeps(cpd, dims, R, ttm_impl):
     out = O.pp_approx_sweep(st, A, nt2)
     assert abs(f - out["f"]) <= TOL * abs(out["f"]), (f, out["f"])
     m.close()
+
+
+@pytest.mark.parametrize("seed,kind", [(1, "kruskal"), (7, "kruskal"), (3, "uniform")])
+def test_last_sweep_status_flags_inconsistent_eq3(cpd, seed, kind):
+    """cpd_last_sweep_status: an approximated sweep forced from a random state (far outside the ε
+    regime) leaves M~ and A inconsistent -- the Eq. 3 radicand is negative beyond rounding and the
+    fitness is the clamped 1; the flag and the radicand/||T||^2 match the oracle's, and regular
+    sweeps never raise the flag."""
+    cfg = synth.custom(3, 6, 4, kind=kind, noise_var=1e-2, seed=seed)
+    To = O.make_tensor(cfg)
+    A0 = synth.init_factors(cfg)
+    T = dev_tensor(cpd, cfg)
+    m = _model(cpd, cfg, T)
+    m.pp_init()
+    f, _ = m.pp_approx_sweep()
+    stt = m.last_sweep_status()
+    out = O.pp_approx_sweep(O.pp_init(To, A0), A0, O.norm2(To))
+    S = out["S"]
+    G = S[0] * S[1]
+    rad = (O.norm2(To) + float(np.sum(G * S[2])) - 2.0 * float(np.sum(out["M"][2] * out["A"][2]))) / O.norm2(To)
+    assert stt["radicand_negative"] == (rad < -1e-8)
+    assert abs(stt["radicand_rel"] - rad) <= 1e-9 * max(1.0, abs(rad))
+    if rad < -1e-8:
+        assert f == 1.0
+    m.set_factors(A0)
+    m.msdt_sweep()
+    assert not m.last_sweep_status()["radicand_negative"]
+    m.close()
