@@ -27,7 +27,8 @@ __all__ = [
     "residual_eq2", "kruskal", "make_tensor", "make_tensor_block", "make_tensor_slice", "mttkrp_rows",
     "als_sweep", "PPState", "pp_init", "pp_approx_sweep", "pp_condition", "pp_controller_run",
     "ttm", "mttv", "MSDTModel", "DTModel", "msdt_roots", "par_als_sweep_sim",
-    "par_pp_approx_sweep_sim", "dS_of",
+    "par_pp_approx_sweep_sim", "dS_of", "pp_first_order", "pp_second_order", "eq3_radicand",
+    "RADICAND_TOL",
 ]
 
 
@@ -99,13 +100,22 @@ def norm2(T):
     return float(np.dot(T.ravel(), T.ravel()))
 
 
+def eq3_radicand(normT2, G_N, S_N, M_N, A_N):
+    """The quantity under the root of Eq. 3, ||T||^2 + <Γ^(N), S^(N)> - 2<M^(N), A^(N)>
+    (reading Q1: ||T||^2, the printed unsquared norm is a typo).  It equals ||T - T~||^2 when M^(N)
+    is the exact MTTKRP; with an approximated M~^(N) it can be negative (reading R18)."""
+    return normT2 + float(np.sum(G_N * S_N)) - 2.0 * float(np.sum(M_N * A_N))
+
+
 def fitness_eq3(normT2, G_N, S_N, M_N, A_N):
-    """Relative residual from Eq. 3 with ||T||^2 under the root
-    (reading Q1: the printed unsquared norm is a typo) and f = 1 - r.
-    Returns (f, r)."""
-    rad = normT2 + float(np.sum(G_N * S_N)) - 2.0 * float(np.sum(M_N * A_N))
+    """Relative residual from Eq. 3 and f = 1 - r; a negative radicand is
+    clamped to 0.  Returns (f, r)."""
+    rad = eq3_radicand(normT2, G_N, S_N, M_N, A_N)
     r = math.sqrt(max(rad, 0.0)) / math.sqrt(normT2)
     return 1.0 - r, r
+
+
+RADICAND_TOL = 1e-8   # Eq. 3 radicand below -RADICAND_TOL ||T||^2: not a residual (S:207, reading R18)
 
 
 def kruskal(A):
@@ -212,7 +222,8 @@ def als_sweep(T, A, normT2=None):
         Ms.append(M)
         Gs.append(G)
     f, r = fitness_eq3(normT2, Gs[-1], S[-1], Ms[-1], A[-1])
-    return dict(A=A, S=S, M=Ms, dA=dA, G=Gs, f=f, r=r)
+    rad = eq3_radicand(normT2, Gs[-1], S[-1], Ms[-1], A[-1]) / normT2
+    return dict(A=A, S=S, M=Ms, dA=dA, G=Gs, f=f, r=r, rad=rad)
 
 
 # ---------------------------------------------------------------------------
@@ -251,6 +262,36 @@ def pp_condition(dA, A, eps):
     return all(np.linalg.norm(d) < eps * np.linalg.norm(a) for d, a in zip(dA, A))
 
 
+def pp_first_order(st: PPState, dA, n):
+    """M_p^(n) + Σ_{i≠n} U^(n,i) (Eqs. 5-6, P:386-396): U^(n,i)(x,k) = Σ_y M_p^(n,i)(x,y,k) dA^(i)(y,k);
+    the pair {a<b} is stored once as [s_a, s_b, R] and contracted on the axis of mode i."""
+    Mt = st.Mp[n].copy()
+    for i in range(len(dA)):
+        if i == n:
+            continue
+        if n < i:   # operator stored as [s_n, s_i, R]: contract its second axis
+            Mt += np.einsum("xyk,yk->xk", st.ops[(n, i)], dA[i])
+        else:       # stored as [s_i, s_n, R]: contract its first axis
+            Mt += np.einsum("yxk,yk->xk", st.ops[(i, n)], dA[i])
+    return Mt
+
+
+def pp_second_order(A, dA, S, n):
+    """W^(n) = Σ_{i<j; i,j≠n} dS^(i) * dS^(j) * ∗_{k∉{i,j,n}} S^(k) (Eq. 7; reading Q7:
+    i, j range over {1..N}\\{n}) with dS^(i) = A^(i)T dA^(i) (Eq. 8).  The second-order
+    term of Eq. 5 is V^(n) = A^(n) W^(n) (pre-update A^(n), reading Q8)."""
+    N = len(A)
+    dS = [dS_of(A[i], dA[i]) for i in range(N)]
+    W = np.zeros_like(S[0])
+    for i, j in itertools.combinations([m for m in range(N) if m != n], 2):
+        term = dS[i] * dS[j]
+        for k in range(N):
+            if k not in (i, j, n):
+                term = term * S[k]
+        W += term
+    return W
+
+
 def pp_approx_sweep(st: PPState, A, normT2, eps=None):
     """One PP approximated sweep (Alg. 2 lines 11-16; Eqs. 5-8).
 
@@ -258,8 +299,9 @@ def pp_approx_sweep(st: PPState, A, normT2, eps=None):
     dS^(i) (Eq. 8); V^(n) = A^(n) W^(n) with W^(n) = Σ_{i<j; i,j≠n}
     dS^(i)*dS^(j)*∗_{k∉{i,j,n}} S^(k) (Eq. 7, reading Q7/Q8: all current, A^(n)
     pre-update); M~^(n) = M_p^(n) + Σ_i U^(n,i) + V^(n) (Eq. 5); solve; update
-    dA^(n), S^(n).  Fitness by Eq. 3 with M~^(N) (reading Q21).
-    Returns dict(A, S, M=[M~^(n)], U, V, f, r, still_valid).
+    dA^(n), S^(n).  Fitness by Eq. 3 with M~^(N) (reading Q21); `rad` is Eq. 3's
+    radicand / ||T||^2 (negative: the sweep left M~ and A inconsistent, reading R18).
+    Returns dict(A, S, M=[M~^(n)], V, f, r, rad, still_valid, dA).
     """
     N = len(A)
     A = [a.copy() for a in A]
@@ -268,23 +310,8 @@ def pp_approx_sweep(st: PPState, A, normT2, eps=None):
     for n in range(N):
         G = gamma(S, n)
         dA = [A[i] - st.Ap[i] for i in range(N)]
-        Mt = st.Mp[n].copy()
-        for i in range(N):
-            if i == n:
-                continue
-            if n < i:   # operator stored as [s_n, s_i, R]: contract its second axis
-                Mt += np.einsum("xyk,yk->xk", st.ops[(n, i)], dA[i])
-            else:       # stored as [s_i, s_n, R]: contract its first axis
-                Mt += np.einsum("yxk,yk->xk", st.ops[(i, n)], dA[i])
-        dS = [dS_of(A[i], dA[i]) for i in range(N)]
-        W = np.zeros_like(G)
-        for i, j in itertools.combinations([m for m in range(N) if m != n], 2):
-            term = dS[i] * dS[j]
-            for k in range(N):
-                if k not in (i, j, n):
-                    term = term * S[k]
-            W += term
-        V = A[n] @ W
+        Mt = pp_first_order(st, dA, n)
+        V = A[n] @ pp_second_order(A, dA, S, n)
         Mt += V
         new = solve(G, Mt)
         A[n] = new
@@ -293,24 +320,33 @@ def pp_approx_sweep(st: PPState, A, normT2, eps=None):
         Vs.append(V)
         Gs.append(G)
     f, r = fitness_eq3(normT2, Gs[-1], S[-1], Ms[-1], A[-1])
+    rad = eq3_radicand(normT2, Gs[-1], S[-1], Ms[-1], A[-1]) / normT2
     dA = [A[i] - st.Ap[i] for i in range(N)]
     valid = pp_condition(dA, A, eps) if eps is not None else None
-    return dict(A=A, S=S, M=Ms, V=Vs, f=f, r=r, still_valid=valid, dA=dA)
+    return dict(A=A, S=S, M=Ms, V=Vs, f=f, r=r, rad=rad, still_valid=valid, dA=dA)
 
 
 def pp_controller_run(T, A0, eps, delta=1e-5, max_sweeps=300, max_pp_run=None, stop_test="any"):
-    """Alg. 2 driver; fitness after every sweep (reading Q21).  Stop test:
-    "any" (default, reading Q21) -- Δ between neighbouring sweeps of any kind (the P:931 wording);
-    "regular" -- Alg. 2 as printed (lines 3-4, 19-21): r is updated only
-      after a regular sweep and the loop ends when |r - r_old| <= Δ between consecutive regular
-      sweeps (r = 1, r_old = 0 initially); approximated sweeps are traced, not tested.
+    """Alg. 2 driver; fitness after every sweep (reading Q21).
+
+    Stop test: "any" (default, reading Q21) -- Δ between neighbouring sweeps of any kind (the
+    P:931 wording); "regular" -- Alg. 2 as printed (lines 3-4, 19-21): r is
+    updated only after a regular sweep and the loop ends when |r - r_old| <= Δ between consecutive
+    regular sweeps (r = 1, r_old = 0 initially); approximated sweeps are traced, not tested.
+    max_sweeps counts regular and approximated sweeps, not PP initialisations: the paper's
+    iteration cap of 300 against Table 3's separate Num-ALS / Num-PP-init /
+    Num-PP-approx columns.
+    An approximated sweep whose Eq. 3 radicand is below -RADICAND_TOL ||T||^2 (reading R18) has no
+    residual: its row carries fitness None, the PP run ends there (as if the ε test failed), and the
+    Δ test skips it (the next regular sweep is compared with the last valid fitness).
     Returns (A, [(kind, f)])."""
     normT2 = norm2(T)
     A = [a.copy() for a in A0]
     dA = [a.copy() for a in A]          # Alg. 2 line 2: dA <- A
     trace, f_old = [], None
     f_reg_old = 0.0                     # r = 1 before the first regular sweep (line 3)
-    while len(trace) < max_sweeps:
+    n_sweeps = 0
+    while n_sweeps < max_sweeps:
         stop = False
         if pp_condition(dA, A, eps):
             st = pp_init(T, A)
@@ -319,18 +355,23 @@ def pp_controller_run(T, A0, eps, delta=1e-5, max_sweeps=300, max_pp_run=None, s
             while True:
                 out = pp_approx_sweep(st, A, normT2, eps)
                 A = out["A"]
-                trace.append(("pp_approx", out["f"]))
+                n_sweeps += 1
                 n_run += 1
+                flagged = out["rad"] < -RADICAND_TOL
+                trace.append(("pp_approx", None if flagged else out["f"]))
+                if flagged:
+                    break
                 if stop_test == "any":
                     stop = f_old is not None and abs(out["f"] - f_old) <= delta
                 f_old = out["f"]
-                if stop or not out["still_valid"] or len(trace) >= max_sweeps or \
+                if stop or not out["still_valid"] or n_sweeps >= max_sweeps or \
                         (max_pp_run is not None and n_run >= max_pp_run):
                     break
-            if stop or len(trace) >= max_sweeps:
+            if stop or n_sweeps >= max_sweeps:
                 break
         out = als_sweep(T, A, normT2)
         A, dA = out["A"], out["dA"]
+        n_sweeps += 1
         trace.append(("regular", out["f"]))
         if stop_test == "any":
             if f_old is not None and abs(out["f"] - f_old) <= delta:
@@ -512,8 +553,8 @@ def par_als_sweep_sim(T, A, P, normT2=None):
 
 def par_pp_approx_sweep_sim(T, st_full: PPState, A, P, normT2):
     """Alg. 4 on the 1-D grid: Local-PP-init on each slab (no
-    communication), local U, Reduce-Scatter of M~, V on replicated small matrices.
-    Returns the M~^(n) list (global) for comparison with the sequential sweep."""
+    communication), local first-order terms, Reduce-Scatter of M~, V on replicated small
+    matrices.  Returns the M~^(n) list (global) for comparison with the sequential sweep."""
     N = T.ndim
     sN = T.shape[-1]
     rng = [synth.slab_range(sN, p, P) for p in range(P)]
@@ -527,28 +568,9 @@ def par_pp_approx_sweep_sim(T, st_full: PPState, A, P, normT2):
     for n in range(N):
         G = gamma(S, n)
         dA = [A[i] - st_full.Ap[i] for i in range(N)]
-        parts = []
-        for (lo, hi), st in zip(rng, locs):
-            dAl = dA[:-1] + [dA[-1][lo:hi]]
-            Mt = st.Mp[n].copy()
-            for i in range(N):
-                if i == n:
-                    continue
-                if n < i:
-                    Mt += np.einsum("xyk,yk->xk", st.ops[(n, i)], dAl[i])
-                else:
-                    Mt += np.einsum("yxk,yk->xk", st.ops[(i, n)], dAl[i])
-            parts.append(Mt)
+        parts = [pp_first_order(st, dA[:-1] + [dA[-1][lo:hi]], n) for (lo, hi), st in zip(rng, locs)]
         Mt = sum(parts) if n < N - 1 else np.concatenate(parts)
-        dS = [dS_of(A[i], dA[i]) for i in range(N)]
-        W = np.zeros_like(G)
-        for i, j in itertools.combinations([m for m in range(N) if m != n], 2):
-            term = dS[i] * dS[j]
-            for k in range(N):
-                if k not in (i, j, n):
-                    term = term * S[k]
-            W += term
-        Mt = Mt + A[n] @ W
+        Mt = Mt + A[n] @ pp_second_order(A, dA, S, n)
         A[n] = solve(G, Mt)
         S[n] = gram(A[n])
         Ms.append(Mt)

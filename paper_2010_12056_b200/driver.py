@@ -14,7 +14,13 @@ Readings:
     re-entry re-initialises (S:415);
   * fitness after every sweep (reading Q21); the Δ stop test between neighbouring sweeps of
     any kind (the P:931 wording, reading R12, default) or, with stop_test="regular", between
-    consecutive regular sweeps as Alg. 2 prints it; or after max_sweeps sweeps.
+    consecutive regular sweeps as Alg. 2 prints it; or after max_sweeps sweeps, counting
+    regular and approximated sweeps but not PP initialisations (the 300-iteration cap of P:931
+    against Table 3's separate Num-ALS / Num-PP-init / Num-PP-approx columns, P:836-849);
+  * an approximated sweep whose Eq. 3 radicand is negative beyond rounding
+    (`cpd_last_sweep_status`, reading R18) has no residual: its row carries fitness None, the
+    PP run ends there and the Δ test skips it (the next regular sweep is compared with the
+    last valid fitness).
 
 Timing of each sweep is the host wall clock around the blocking ABI call (each call
 returns only after its stream work completed); it is a trace, not a bench number.
@@ -36,7 +42,8 @@ def pp_cp_als(model, delta=1e-5, max_sweeps=300, max_pp_run=None, regular="msdt"
 
     Returns a list of trace rows ``(sweep, phase, residual, fitness, wall_seconds)``
     where phase ∈ {"regular", "pp_init", "pp_approx"} (S:251 CSV columns); pp_init rows
-    carry no fitness.  `regular` selects the regular sweep ("msdt" per P:788, or "dt").
+    and flagged approximated sweeps carry no fitness.  `regular` selects the regular sweep
+    ("msdt" per P:788, or "dt").
     If `trace` is a file-like object the rows are also written to it as CSV.
     """
     if stop_test not in ("regular", "any"):
@@ -67,8 +74,11 @@ def pp_cp_als(model, delta=1e-5, max_sweeps=300, max_pp_run=None, regular="msdt"
                 t0 = time.perf_counter()
                 f, still_valid = model.pp_approx_sweep()
                 n_sweeps += 1
-                log("pp_approx", f, time.perf_counter() - t0)
+                flagged = model.last_sweep_status()["radicand_negative"]
+                log("pp_approx", None if flagged else f, time.perf_counter() - t0)
                 n_run += 1
+                if flagged:
+                    break
                 if stop_test == "any":
                     stop = f_old is not None and abs(f - f_old) <= delta
                 f_old = f

@@ -276,50 +276,38 @@ def test_pp_single_perturbed_factor_is_exact(N):
     assert np.abs(Mt - ref).max() <= 1e-12 * np.abs(ref).max()
 
 
-def _pp_one_mode(st, A, n):
-    """M~^(n) for the current A exactly as pp_approx_sweep forms it (Eqs. 5-8)."""
-    N = len(A)
-    S = [O.gram(a) for a in A]
-    dA = [A[i] - st.Ap[i] for i in range(N)]
-    Mt = st.Mp[n].copy()
-    for i in range(N):
-        if i != n:
-            Mt += (np.einsum("xyk,yk->xk", st.ops[(n, i)], dA[i]) if n < i
-                   else np.einsum("yxk,yk->xk", st.ops[(i, n)], dA[i]))
-    dS = [O.dS_of(A[i], dA[i]) for i in range(N)]
-    W = 0
-    for i, j in itertools.combinations([m for m in range(N) if m != n], 2):
-        t = dS[i] * dS[j]
-        for k in range(N):
-            if k not in (i, j, n):
-                t = t * S[k]
-        W = W + t
-    return Mt + A[n] @ W
+def _kruskal_exactness_err(N=3, R=3, s=6, delta=0.2):
+    """Max over modes of ||M~^(n) - M^(n)|| / ||M^(n)|| for one oracle.pp_approx_sweep with
+    T = [[A]] and A_p = A + δG, M^(n) the exact MTTKRP at the factors current when mode n is formed."""
+    A = [rnd((s, R), 200 + i) for i in range(N)]
+    T = O.kruskal(A)
+    Ap = [a + delta * rnd(a.shape, 300 + i) for i, a in enumerate(A)]
+    st = O.pp_init(T, Ap)
+    out = O.pp_approx_sweep(st, A, O.norm2(T))
+    err = 0.0
+    for n in range(N):
+        cur = out["A"][:n] + A[n:]
+        ref = O.mttkrp(T, cur, n)
+        err = max(err, np.linalg.norm(out["M"][n] - ref) / np.linalg.norm(ref))
+    return err, out, A
 
 
 def test_pp_order3_kruskal_tensor_is_exact():
-    """N=3 and T = [[A]]: the expansion of Eqs. 5-8 is exact for any A_p (second-order
-    is the highest order in the other two factors).  Pins Eq. 7's form and Eq. 8's
-    orientation (a transposed dS fails at ~1e-3)."""
-    A = [rnd((6, 3), 200 + i) for i in range(3)]
-    T = O.kruskal(A)
-    Ap = [a + 0.2 * rnd(a.shape, 300 + i) for i, a in enumerate(A)]
-    st = O.pp_init(T, Ap)
-    for n in range(3):
-        got = _pp_one_mode(st, A, n)
-        ref = O.mttkrp(T, A, n)
-        assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
-    # the transposed orientation is wrong: check the pin can fail
-    dA = [A[i] - Ap[i] for i in range(3)]
-    bad = st.Mp[0] + np.einsum("xyk,yk->xk", st.ops[(0, 1)], dA[1]) + \
-        np.einsum("xyk,yk->xk", st.ops[(0, 2)], dA[2]) + A[0] @ ((dA[1].T @ A[1]) * (dA[2].T @ A[2]))
-    assert np.linalg.norm(bad - O.mttkrp(T, A, 0)) > 1e-6 * np.linalg.norm(O.mttkrp(T, A, 0))
+    """N=3 and T = [[A]]: the expansion of Eqs. 5-8 is exact for any A_p (second order is the
+    highest order in the other two factors), and [[A]] is a fixed point of the exact update, so
+    every mode of a whole oracle.pp_approx_sweep reproduces the exact MTTKRP and keeps A.  Pins
+    Eq. 7's form, Eq. 8's orientation (a transposed dS fails at ~1e-3) and the presence of V."""
+    err, out, A = _kruskal_exactness_err()
+    assert err <= 1e-11, err
+    for a, b in zip(out["A"], A):
+        assert np.linalg.norm(a - b) <= 1e-10 * np.linalg.norm(b)
+    assert np.linalg.norm(out["V"][0]) > 1e-3 * np.linalg.norm(out["M"][0])   # V is not negligible here
+    assert abs(out["rad"]) <= 1e-12 and abs(out["f"] - 1.0) <= 1e-6
 
 
-@pytest.mark.parametrize("N", [3, 4])
-def test_pp_error_decay_third_order(N):
-    """T ≈ low rank, A_p = true factors, A = A_p + δG: halving δ cuts ||M~ - M|| by
-    ≈ 8x (the neglected terms are third order; SPEC S:390 requires ≥ 3.5x)."""
+def _decay_ratios(N):
+    """T ≈ low rank, A_p = true factors, A = A_p + δG: ||M~^(1) - M^(1)|| from oracle.pp_approx_sweep
+    (its first mode sees every other factor perturbed) for δ = 0.1, 0.05, 0.025."""
     s, R = 6, 2
     At = [rnd((s, R), 400 + i) for i in range(N)]
     T = O.kruskal(At) + 1e-3 * rnd((s,) * N, 5)
@@ -328,10 +316,39 @@ def test_pp_error_decay_third_order(N):
     errs = []
     for d in (0.1, 0.05, 0.025):
         A = [a + d * g for a, g in zip(At, G)]
-        e = np.linalg.norm(_pp_one_mode(st, A, 0) - O.mttkrp(T, A, 0))
-        errs.append(e)
-    assert errs[0] / errs[1] >= 3.5 and errs[1] / errs[2] >= 3.5
-    assert 6.0 <= errs[1] / errs[2] <= 10.0
+        out = O.pp_approx_sweep(st, A, O.norm2(T))
+        errs.append(np.linalg.norm(out["M"][0] - O.mttkrp(T, A, 0)))
+    return errs[0] / errs[1], errs[1] / errs[2]
+
+
+@pytest.mark.parametrize("N", [3, 4])
+def test_pp_error_decay_third_order(N):
+    """Halving δ cuts ||M~ - M|| by ≈ 8x: the neglected terms are third order (SPEC S:390 requires
+    ≥ 3.5x); a wrong or missing second-order term leaves a second-order error (≈ 4x)."""
+    r1, r2 = _decay_ratios(N)
+    assert r1 >= 3.5 and r2 >= 3.5
+    assert 6.0 <= r2 <= 10.0, (r1, r2)
+
+
+def test_pp_pins_detect_oracle_mutations(monkeypatch):
+    """The two PP pins above fail when the oracle's Eq. 7/8 is wrong: a transposed dS^(i)
+    (dA^T A instead of A^T dA) or a dropped V term (W = 0).  The mutations are patched into the
+    oracle module itself, so the pins are shown to guard oracle.pp_approx_sweep, not a copy."""
+    good_err, _, _ = _kruskal_exactness_err()
+    assert good_err <= 1e-11
+    mutations = {
+        "dS transposed": ("dS_of", lambda a, d: d.T @ a),
+        "V = 0": ("pp_second_order", lambda A, dA, S, n: np.zeros_like(S[0])),
+    }
+    import oracle.cpals as OC
+    for name, (attr, fn) in mutations.items():
+        with monkeypatch.context() as mp:
+            mp.setattr(OC, attr, fn)
+            err, _, _ = _kruskal_exactness_err()
+            r3 = _decay_ratios(3)
+            r4 = _decay_ratios(4)
+        assert err > 1e-4, (name, err)
+        assert not (6.0 <= r3[1] <= 10.0 and 6.0 <= r4[1] <= 10.0), (name, r3, r4)
 
 
 def test_pp_controller_eps_zero_is_plain_als():
