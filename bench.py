@@ -34,7 +34,6 @@ sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 
 METRIC = "CP-ALS per-sweep time (MSDT, PP-approx) and TTM FP64-TC % / TTV HBM GB/s at 1-8 GPU"
-FP64_PEAK_TFLOPS = 37.1   # measured DMMA m8n8k4 (profiles/r01_peaks_fp64.json); MEASURED_PEAKS.json has no FP64 entry
 
 
 def load_peaks():
@@ -46,12 +45,12 @@ def load_peaks():
 
 
 def fp64_peak():
+    """Measured DMMA peak (profiles/r01_peaks_fp64.json, one JSON object); a missing or
+    unparsable file is an error, not a silent fallback."""
     p = os.path.join(ROOT, "profiles", "r01_peaks_fp64.json")
-    try:
-        d = json.load(open(p))
-        return max(v for k, v in d.items() if k.startswith("dmma")), "measured DMMA (profiles/r01_peaks_fp64.json)"
-    except Exception:
-        return FP64_PEAK_TFLOPS, "measured DMMA (DESIGN.md)"
+    d = json.load(open(p))
+    v = max(v for k, v in d.items() if k.startswith("dmma"))
+    return float(v), "measured DMMA mma.sync.m8n8k4/m16n8k8 f64 (profiles/r01_peaks_fp64.json)"
 
 
 def ncu_traffic(name):
@@ -121,6 +120,22 @@ class Clocks:
                 "samples": len(sm)}
 
 
+def self_launch(n):
+    """`python bench.py --gpus N` outside torchrun: re-run this command under
+    torch.distributed.run with N ranks (one per GPU) on 127.0.0.1; NCCL prints its
+    communicator-init lines (nranks) to stderr."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -139,16 +154,6 @@ def make_slab(cpd, torch, cfg, rank, world, stream):
     return T
 
 
-def oracle_sample(cfg, w):
-    """Bounded CPU sample: one oracle als_sweep on a [s,..,s,w] slab of T (one piece of
-    the 1-D partition); a full sweep is s/w such pieces (Alg. 3 local MTTKRPs)."""
-    import oracle as O
-    T = O.make_tensor_block(cfg, [(0, cfg.s)] * (cfg.N - 1) + [(0, w)])
-    A = synth.init_factors(cfg)
-    A[-1] = np.ascontiguousarray(A[-1][:w])
-    return O, T, A
-
-
 def cpu_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -156,39 +161,114 @@ def cpu_cores():
         return os.cpu_count()
 
 
-def time_oracle(cfg, n_sweeps, w):
+def host_tensor(cfg, rows=None):
+    """T on the host for the oracle timing legs, from the synth recipe: the Kruskal part of the
+    true factors as (explicit KRP of modes 1..N-1) x A^(N)^T plus the counter-hash noise (or the
+    U(0,1) entries), generated in parallel blocks of the leading mode.  `rows` restricts mode 1."""
+    import oracle as O
+    from concurrent.futures import ThreadPoolExecutor
+    shape = list(cfg.shape)
+    lo0, hi0 = (0, shape[0]) if rows is None else rows
+    out = np.empty([hi0 - lo0] + shape[1:])
+    At = synth.true_factors(cfg)
+    inner = int(np.prod(shape[1:]))
+
+    def block(i0):
+        i1 = min(i0 + 8, hi0)
+        idx = (np.arange(i0 * inner, i1 * inner, dtype=np.uint64))
+        v = synth.element_noise(cfg, idx).reshape([i1 - i0] + shape[1:])
+        if At is not None:
+            krp = O.khatri_rao([At[0][i0:i1]] + At[1:-1])
+            v += (krp @ At[-1].T).reshape(v.shape)
+        out[i0 - lo0:i1 - lo0] = v
+
+    with ThreadPoolExecutor(max_workers=cpu_cores()) as ex:
+        list(ex.map(block, range(lo0, hi0, 8)))
+    return out
+
+
+def oracle_full_sweeps(cfg, n_sweeps):
+    """The oracle's als_sweep (explicit unfolding + explicit KRP + Cholesky + Eq. 3) on the FULL
+    tensor of `cfg`, n_sweeps times from the seeded initial factors; per-sweep seconds."""
+    import oracle as O
     from threadpoolctl import threadpool_limits
     cores = cpu_cores()
-    O, T, A = oracle_sample(cfg, w)
+    T = host_tensor(cfg)
+    A = synth.init_factors(cfg)
+    nt2 = O.norm2(T)
     ts = []
     with threadpool_limits(limits=cores):
         for _ in range(n_sweeps):
             t0 = time.perf_counter()
-            out = O.als_sweep(T, A)
+            out = O.als_sweep(T, A, nt2)
             ts.append(time.perf_counter() - t0)
             A = out["A"]
     return ts, cores
 
 
+def cpu_baseline(cfg, n_sweeps):
+    ts, cores = oracle_full_sweeps(cfg, n_sweeps)
+    return {"value": 1e3 * statistics.mean(ts), "unit": "ms/sweep (MSDT)", "cores": cores, "kind": "oracle",
+            "sample": f"{n_sweeps} full oracle als_sweep on the whole {cfg.name} tensor "
+                      f"({'x'.join(map(str, cfg.shape))}, R={cfg.R}; explicit unfolding + explicit KRP + "
+                      f"Cholesky + Eq. 3), mean per sweep; per-sweep s: {[round(t, 2) for t in ts]}"}
+
+
+def workload_config(cfg, world):
+    """The `config` object of both arms (identical, static; run state goes elsewhere)."""
+    return {"workload": cfg.name, "N": cfg.N, "s": cfg.s, "R": cfg.R,
+            "tensor": f"exact rank {cfg.true_rank} + N(0,{cfg.noise_var}) noise" if cfg.kind == "kruskal"
+            else "i.i.d. U(0,1)", "parallelism": f"1-D split of mode N over {world} GPU(s)",
+            "step": f"{cfg.N - 1} msdt_sweep + pp_init + {cfg.N - 1} pp_approx_sweep + 1 dt_sweep",
+            "l2": "inputs larger than L2 (no flush)"}
+
+
 def run_reference(args, rank, world):
-    """--impl reference: the CPU oracle as it stands (the tier's reference arm)."""
+    """--impl reference: the CPU oracle as it stands (the tier's reference arm), rank 0 only.
+    A step is one mode update of the oracle's als_sweep on the FULL tensor (explicit unfolding,
+    explicit KRP, Cholesky solve, Gram), cycling through the modes, so N consecutive steps are one
+    full sweep; `value` = mean step time x N = ms per full sweep, measured over whole sweeps."""
     if rank != 0:
         return
+    import oracle as O
+    from threadpoolctl import threadpool_limits
     cfg = synth.config(args.config)
-    w = args.oracle_slab
-    ts, cores = time_oracle(cfg, args.warmup + args.steps, w)
-    timed = ts[args.warmup:]
-    per_sweep_ms = 1e3 * statistics.mean(timed) * (cfg.s / w)
+    N = cfg.N
+    cores = cpu_cores()
+    T = host_tensor(cfg)
+    A = synth.init_factors(cfg)
+    nt2 = O.norm2(T)
+    S = [O.gram(a) for a in A]
+    ts = []
+    with threadpool_limits(limits=cores):
+        for it in range(args.warmup + args.steps):
+            n = it % N
+            t0 = time.perf_counter()
+            G = O.gamma(S, n)
+            M = O.mttkrp(T, A, n)
+            A[n] = O.solve(G, M)
+            S[n] = O.gram(A[n])
+            if n == N - 1:
+                O.fitness_eq3(nt2, G, S[n], M, A[n])
+            dt = time.perf_counter() - t0
+            if it >= args.warmup:
+                ts.append(dt)
+    per_mode = {}
+    for k, t in enumerate(ts):
+        per_mode.setdefault((args.warmup + k) % N, []).append(t)
+    per_sweep_ms = 1e3 * sum(statistics.mean(v) for v in per_mode.values()) * N / len(per_mode)
+    step_ms = 1e3 * statistics.mean(ts)
     line = {
         "impl": "reference", "metric": METRIC, "value": per_sweep_ms, "unit": "ms/sweep (MSDT)",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": per_sweep_ms * (cfg.N - 1), "higher_is_better": False, "scaling": "strong",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": step_ms, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg.name, "N": cfg.N, "s": cfg.s, "R": cfg.R, "l2": "inputs larger than L2"},
+        "config": workload_config(cfg, world),
         "cpu_baseline": {"value": per_sweep_ms, "unit": "ms/sweep (MSDT)", "cores": cores, "kind": "oracle",
-                         "sample": f"oracle als_sweep (explicit unfolding + explicit KRP + Cholesky) on a "
-                                   f"{'x'.join([str(cfg.s)] * (cfg.N - 1))}x{w} slab, x{cfg.s // w} slabs "
-                                   f"(1-D partition pieces; linear extrapolation)"},
+                         "sample": f"each step = one mode update of the oracle als_sweep (explicit unfolding + "
+                                   f"explicit KRP + Cholesky + Gram) on the full {'x'.join(map(str, cfg.shape))} "
+                                   f"tensor, modes cycling; value = mean step time per mode summed over the "
+                                   f"{N} modes (ms per full sweep)"},
         "e2e": {"value": per_sweep_ms, "unit": "ms/sweep (MSDT)", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -208,12 +288,16 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-dmma-compare", action="store_true", help="skip the FP64-DMMA engine comparison cycles")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--oracle-slab", type=int, default=16)
+    ap.add_argument("--cpu-sweeps", type=int, default=3, help="full oracle sweeps timed for cpu_baseline")
     ap.add_argument("--ttm-impl", default="auto", choices=["dmma", "int8", "auto"],
                     help="first-level TTM engine: FP64 DMMA, FP64 operands as int8 digits on tcgen05, or the "
                          "library's choice (int8 when its error bound is FP64-class)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args.gpus))
     world, rank, local = dist_setup(args)
+    if "WORLD_SIZE" in os.environ and args.gpus != world and rank == 0:
+        print(f"[bench] --gpus {args.gpus} but WORLD_SIZE={world}: measuring {world} rank(s)", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -224,6 +308,8 @@ def main():
 
     torch.cuda.set_device(local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")        # communicator init lines (nranks) on stderr
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.Stream()
     cfg = synth.config(args.config)
@@ -331,12 +417,6 @@ def main():
         e2e = run_e2e(args, cpd, torch, cfg, T, m, rank, world, local, nccl_id, stream)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        ts, cores = time_oracle(cfg, 2, args.oracle_slab)
-        v = 1e3 * min(ts) * (cfg.s / args.oracle_slab)
-        cpu = {"value": v, "unit": "ms/sweep (MSDT)", "cores": cores, "kind": "oracle",
-               "sample": f"oracle als_sweep on a {'x'.join([str(cfg.s)] * (N - 1))}x{args.oracle_slab} slab "
-                         f"(best of 2), x{cfg.s // args.oracle_slab} slabs of the 1-D partition (linear extrapolation)"}
 
     engine = m.ttm_engine()
     if engine == "dmma":
@@ -370,17 +450,24 @@ def main():
         engines = {engine: {"msdt_ms_per_sweep": msdt_ms, "ttm_ms": ttm_ms, "ttm_fp64_equiv_tflops": ttm_tf}}
         if not args.no_dmma_compare:
             engines["dmma"] = dmma_compare(cpd, torch, cfg, T, m, local, rank, world, nccl_id, stream, fp64, fp64_src)
+    m.close()
+    # the oracle on the host cores, after every GPU measurement (rank 0; other ranks wait)
+    if rank == 0 and not args.no_cpu_baseline:
+        if 8 * cfg.numel > 40e9:   # C5: the oracle's full sweep needs ~2x 69 GB of host memory
+            cpu = {"value": None, "unit": "ms/sweep (MSDT)", "cores": cpu_cores(), "kind": "oracle",
+                   "sample": "skipped: the full tensor exceeds the host budget of the timing leg"}
+        else:
+            cpu = cpu_baseline(cfg, args.cpu_sweeps)
+    if world > 1:
+        dist.barrier()
     if rank == 0:
         line = {
             "metric": METRIC, "value": msdt_ms, "unit": "ms/sweep (MSDT)", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg.name, "N": N, "s": cfg.s, "R": cfg.R,
-                       "tensor": f"exact rank {cfg.true_rank} + N(0,{cfg.noise_var}) noise" if cfg.kind == "kruskal"
-                       else "i.i.d. U(0,1)", "parallelism": f"1-D split of mode N over {world} GPU(s)",
-                       "step": f"{N - 1} msdt_sweep + pp_init + {N - 1} pp_approx_sweep + 1 dt_sweep",
-                       "l2": "inputs larger than L2 (no flush)", "presweeps": pre, "pp_condition_held": pp_ok,
-                       "fitness_before_steps": f, "ttm_impl": args.ttm_impl},
+            "config": workload_config(cfg, world),
+            "state": {"presweeps": pre, "pp_condition_held": pp_ok, "fitness_before_steps": f,
+                      "ttm_impl": args.ttm_impl},
             "sweeps_ms": {"msdt": msdt_ms, "pp_approx": ppapprox_ms, "pp_init": ppinit_ms, "dt": dt_ms,
                           "dt_over_msdt": dt_ms / msdt_ms, "dt_over_pp_approx": dt_ms / ppapprox_ms},
             "phase_ms_per_step": {k: v / 2 for k, v in ph_all.items()},
@@ -393,7 +480,6 @@ def main():
             "gpu_launches": launches, "clocks": clk.summary(wall0, wall1), "e2e": e2e, "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
-    m.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -16,10 +16,15 @@
  *  - Layout: T is row-major (last mode fastest), float64.  Factor matrices are s_n x R
  *    row-major float64 (R fastest).  Intermediates live on the device in the layout
  *    [kept modes ascending ..., R] (R innermost).
- *  - Multi-GPU (Alg. 3, Alg. 4) on a 1-D processor grid 1x..x1xP:
- *    rank p holds the contiguous slab T[..., p*s_N/P : (p+1)*s_N/P] (s_N % P == 0,
- *    reading Q20).  With world > 1 every call is collective: all ranks make the same
- *    sequence of calls.  The library owns its NCCL communicator.
+ *  - Multi-GPU (Alg. 3, Alg. 4) on a processor grid I_1 x .. x I_N
+ *    (cpd_opts.grid; default the 1-D grid 1x..x1xP).  Rank r has grid coordinates
+ *    (x_1..x_N), r = row-major index (last mode fastest), and holds the block
+ *    T[x_1 b_1 : (x_1+1) b_1, ..., x_N b_N : (x_N+1) b_N], b_n = s_n / I_n, row-major and
+ *    contiguous (1-D default: the slab T[..., p*s_N/P : (p+1)*s_N/P]).  s_n % I_n == 0 and
+ *    b_n % (P / I_n) == 0 (reading Q20: no padding).  With world > 1 every call is
+ *    collective: all ranks make the same sequence of calls.  The library owns its NCCL
+ *    communicators (the world and, per mode, Proc-Slice(x_n) and the fibre of x_n, split
+ *    with ncclCommSplit).
  *  - Ownership: T is BORROWED (device pointer, read-only, must outlive the ctx).
  *    Factors are copied in.  Outputs are copied into caller buffers.  All device
  *    workspaces (tree intermediates, PP operators) belong to the ctx and are freed by
@@ -62,7 +67,7 @@ typedef enum {
 typedef struct {
   uint32_t struct_size;       /* = sizeof(cpd_opts); ABI versioning */
   int device;                 /* CUDA device ordinal used by this ctx */
-  int rank, world;            /* 1-D split of mode N (rank owns slab rank*s_N/world ...) */
+  int rank, world;            /* this rank and the number of ranks (= prod(grid)) */
   const void* nccl_unique_id; /* CPD_NCCL_ID_BYTES bytes from cpd_nccl_unique_id on rank 0,
                                  broadcast by the caller; NULL iff world == 1 */
   void* stream;               /* caller's cudaStream_t (NULL = the legacy default stream).  The library
@@ -87,6 +92,16 @@ typedef struct {
                                  CPD_TTM_AUTO (2, default) = INT8 when max|T| <= 256 rms(T), i.e. when
                                    its norm-wise error bound 2^-55 max|T|/rms(T) is FP64-class, else DMMA.
                                  Modes with s_j > 16384 always use DMMA. */
+  int grid[CPD_MAX_ORDER];    /* processor grid I_1..I_N (Alg. 3 line 1); all 0 = the 1-D default
+                                 1 x .. x 1 x world; entries beyond N must be 0 */
+  int fused_rs;               /* 0 (default): the partial MTTKRP of each mode is reduce-scattered in
+                                 Proc-Slice(x_n) by a collective (ncclReduceScatter).  1: fused epilogue
+                                 (SURVEY f2): the kernel that completes the local partial M^(n) / M~^(n)
+                                 stores each owner's rows straight into that owner's receive buffer
+                                 (NCCL: a symmetric window from ncclMemAlloc + ncclCommWindowRegister,
+                                 addressed through ncclGetPeerPointer over NVLink; local group: the
+                                 same device), then a stream-ordered barrier and a fixed-order sum of
+                                 the received slots.  Needs <= 8 ranks per slice. */
 } cpd_opts;
 
 #define CPD_TTM_DMMA 0
@@ -114,8 +129,8 @@ cpd_status cpd_nccl_unique_id(void* out /* CPD_NCCL_ID_BYTES */);
 /* Create a ctx (Alg. 1 line 2 / Alg. 3 lines 4-9).
  *  N: order, 3 <= N <= CPD_MAX_ORDER.  shape: global s_1..s_N (each >= 1).
  *  R: rank, 1 <= R <= CPD_MAX_RANK.
- *  T_local_dev: BORROWED device pointer to this rank's row-major slab
- *    [s_1, ..., s_{N-1}, s_N/world] (float64, read-only).
+ *  T_local_dev: BORROWED device pointer to this rank's row-major block
+ *    [s_1/I_1, ..., s_N/I_N] (float64, read-only; 1-D default [s_1, ..., s_{N-1}, s_N/world]).
  *  A0_host: N host pointers, each the GLOBAL s_n x R row-major initial factor (copied).
  *  Computes ||T||^2 once (all-reduced), S^(n) = A^(n)T A^(n), MSDT phase 0.
  */
@@ -181,7 +196,7 @@ cpd_status cpd_set_profile_level(cpd_ctx* ctx, int level);
 /* Zero the phase timers and counters. */
 cpd_status cpd_reset_counters(cpd_ctx* ctx);
 
-/* M_p^(a0,b0) as [s_a, s_b_local, R] (a0 < b0; b0 == N-1 gives the local slab rows):
+/* M_p^(a0,b0) as [s_a/I_a, s_b/I_b, R], the local (block-partial) operator (a0 < b0):
  * checks pp_init directly against the oracle's operators (small configs). */
 cpd_status cpd_debug_get_pp_operator(cpd_ctx* ctx, int a0, int b0, double* host_out);
 
@@ -202,6 +217,12 @@ cpd_status cpd_destroy(cpd_ctx* ctx);
 cpd_status cpd_gen_tensor(double* T_dev, int N, const int64_t* shape, int64_t lo, int64_t hi,
                           int kind, const double* const* At_host, int Rt, double noise_std,
                           uint64_t seed, void* stream);
+
+/* The block [lo_n, hi_n) per mode of the same synthetic tensor (N-D processor grid): T_dev
+ * receives Π (hi_n - lo_n) doubles, row-major; element values depend only on the global index. */
+cpd_status cpd_gen_tensor_block(double* T_dev, int N, const int64_t* shape, const int64_t* lo,
+                                const int64_t* hi, int kind, const double* const* At_host, int Rt,
+                                double noise_std, uint64_t seed, void* stream);
 
 /* First-level TTM: out[p, m, r] = Σ_y T[p, y, m] A[y, r] with T viewed as
  * [pre, K, post]; out is [pre*post, R] row-major.  All device pointers; synchronous. */

@@ -28,7 +28,8 @@ __all__ = [
     "als_sweep", "PPState", "pp_init", "pp_approx_sweep", "pp_condition", "pp_controller_run",
     "ttm", "mttv", "MSDTModel", "DTModel", "msdt_roots", "par_als_sweep_sim",
     "par_pp_approx_sweep_sim", "dS_of", "pp_first_order", "pp_second_order", "eq3_radicand",
-    "RADICAND_TOL",
+    "RADICAND_TOL", "pp_init_rows", "pp_approx_rows", "grid_procs", "par_als_sweep_grid_sim",
+    "par_pp_approx_sweep_grid_sim",
 ]
 
 
@@ -250,6 +251,53 @@ def pp_init(T, A):
         ops[(a, b)] = Tab @ khatri_rao([Ap[m] for m in rest])
     Mp = [mttkrp(T, Ap, n) for n in range(N)]
     return PPState(Ap=Ap, ops=ops, Mp=Mp)
+
+
+def pp_init_rows(cfg, Ap, n, rows, slices=None):
+    """The part of PP initialisation (Alg. 2 lines 6-9; Eq. 4) that Eq. 5 needs for the
+    rows `rows` of mode n: M_p^(n,i)(x, y, k) for x in rows and every i != n, and M_p^(n)(x, :),
+    each from the slice T(..., i_n = x, ...) with an explicit partial Khatri-Rao product of the
+    other A_p^(m) (for full-size tensors whose pair operators the oracle cannot hold).
+    Returns a PPState whose operators are restricted to those rows (the pair {n, i} keeps its
+    [s_a, s_b, R] orientation with mode n's axis cut to len(rows)), so pp_first_order applies
+    unchanged.  `slices` (optional dict) caches T's slices across calls."""
+    N, R = cfg.N, Ap[0].shape[1]
+    ops, mp = {}, []
+    for i in range(N):
+        if i == n:
+            continue
+        rest = [m for m in range(N) if m not in (n, i)]
+        krp = khatri_rao([Ap[m] for m in rest])
+        blk = []
+        for x in rows:
+            key = (n, int(x))
+            sl = slices.get(key) if slices is not None else None
+            if sl is None:
+                sl = make_tensor_slice(cfg, n, int(x))      # modes != n, ascending
+                if slices is not None:
+                    slices[key] = sl
+            kept = [m for m in range(N) if m != n]
+            Ti = np.ascontiguousarray(np.moveaxis(sl, kept.index(i), 0)).reshape(cfg.shape[i], -1)
+            blk.append(Ti @ krp)                             # [s_i, R]
+        blk = np.stack(blk)                                  # [rows, s_i, R]
+        ops[(n, i) if n < i else (i, n)] = blk if n < i else np.ascontiguousarray(blk.transpose(1, 0, 2))
+    # M_p^(n) rows: one more contraction of any pair operator row with A_p^(i) (Eq. 4 -> MTTKRP)
+    i0 = 0 if n != 0 else 1
+    op = ops[(n, i0) if n < i0 else (i0, n)]
+    mp = np.einsum("xyk,yk->xk", op, Ap[i0]) if n < i0 else np.einsum("yxk,yk->xk", op, Ap[i0])
+    Mp = [None] * N
+    Mp[n] = mp
+    return PPState(Ap=[a.copy() for a in Ap], ops=ops, Mp=Mp)
+
+
+def pp_approx_rows(st_rows: PPState, A, n, rows):
+    """M~^(n)(rows, :) of Eq. 5 at the current factors A (modes < n already updated
+    this sweep): the first-order terms from the row-restricted operators, plus V^(n)(rows) =
+    A^(n)(rows) W^(n) (Eqs. 7-8) with W^(n) from the full current factors."""
+    N = len(A)
+    dA = [A[i] - st_rows.Ap[i] for i in range(N)]
+    S = [gram(a) for a in A]
+    return pp_first_order(st_rows, dA, n) + A[n][rows] @ pp_second_order(A, dA, S, n)
 
 
 def dS_of(A_i, dA_i):
@@ -570,6 +618,75 @@ def par_pp_approx_sweep_sim(T, st_full: PPState, A, P, normT2):
         dA = [A[i] - st_full.Ap[i] for i in range(N)]
         parts = [pp_first_order(st, dA[:-1] + [dA[-1][lo:hi]], n) for (lo, hi), st in zip(rng, locs)]
         Mt = sum(parts) if n < N - 1 else np.concatenate(parts)
+        Mt = Mt + A[n] @ pp_second_order(A, dA, S, n)
+        A[n] = solve(G, Mt)
+        S[n] = gram(A[n])
+        Ms.append(Mt)
+    return dict(A=A, M=Ms)
+
+
+# ---------------------------------------------------------------------------
+# Alg. 3 / Alg. 4 on a general N-D processor grid I_1 x ... x I_N (P:419-456, P:468-479,
+# P:596-632): processor x = (x_1..x_N) holds the block T[b_1(x_1), ..., b_N(x_N)] with
+# b_n(k) = synth.slab_range(s_n, k, I_n), and the factor rows b_m(x_m) of every mode.
+# ---------------------------------------------------------------------------
+
+def grid_procs(grid):
+    """Processor coordinates in row-major order (last grid mode fastest): rank -> (x_1..x_N)."""
+    return list(itertools.product(*[range(g) for g in grid]))
+
+
+def _blk(shape, grid, x):
+    return [synth.slab_range(s, k, g) for s, k, g in zip(shape, x, grid)]
+
+
+def par_als_sweep_grid_sim(T, A, grid, normT2=None):
+    """One sweep of Alg. 3 on the grid: Local-MTTKRP of every block with its local factor rows
+    (line 13); the local results of the processors in Proc-Slice(x_n) summed into rows b_n(x_n)
+    (Reduce-Scatter, line 14); solve (line 15); S^(n) as the sum of the Grams of the I = ∏I_n row
+    chunks of the Q distribution (All-Reduce, lines 16-17); fitness by Eq. 3 on M^(N)."""
+    N = T.ndim
+    A = [a.copy() for a in A]
+    S = [gram(a) for a in A]
+    if normT2 is None:
+        normT2 = norm2(T)
+    procs = grid_procs(grid)
+    I = len(procs)
+    for n in range(N):
+        G = gamma(S, n)
+        M = np.zeros((T.shape[n], A[0].shape[1]))
+        for x in procs:
+            b = _blk(T.shape, grid, x)
+            Tx = T[tuple(slice(lo, hi) for lo, hi in b)]
+            Ax = [A[m][lo:hi] for m, (lo, hi) in enumerate(b)]
+            M[b[n][0]:b[n][1]] += mttkrp(Tx, Ax, n)
+        A[n] = solve(G, M)
+        # the Q distribution: ceil(s_n / I) rows per processor (line 5), the last chunks shorter
+        c = -(-T.shape[n] // I)
+        S[n] = sum(gram(A[n][q * c:(q + 1) * c]) for q in range(I) if q * c < T.shape[n])
+        Gl, Ml = G, M
+    f, r = fitness_eq3(normT2, Gl, S[-1], Ml, A[-1])
+    return dict(A=A, S=S, f=f, r=r, M_last=Ml)
+
+
+def par_pp_approx_sweep_grid_sim(T, st_full: PPState, A, grid, normT2):
+    """Alg. 4 on the grid: Local-PP-init of every block with its local A_p rows (line 2, no
+    communication), local first-order terms with the local dA rows (lines 5-7), M~^(n) summed over
+    Proc-Slice(x_n) (line 9), V^(n) on the full small matrices (line 10).  Returns the M~^(n) list."""
+    N = T.ndim
+    procs = grid_procs(grid)
+    blocks = [_blk(T.shape, grid, x) for x in procs]
+    locs = [pp_init(T[tuple(slice(lo, hi) for lo, hi in b)], [st_full.Ap[m][lo:hi] for m, (lo, hi) in enumerate(b)])
+            for b in blocks]
+    A = [a.copy() for a in A]
+    S = [gram(a) for a in A]
+    Ms = []
+    for n in range(N):
+        G = gamma(S, n)
+        dA = [A[i] - st_full.Ap[i] for i in range(N)]
+        Mt = np.zeros((T.shape[n], A[0].shape[1]))
+        for b, st in zip(blocks, locs):
+            Mt[b[n][0]:b[n][1]] += pp_first_order(st, [dA[m][lo:hi] for m, (lo, hi) in enumerate(b)], n)
         Mt = Mt + A[n] @ pp_second_order(A, dA, S, n)
         A[n] = solve(G, Mt)
         S[n] = gram(A[n])

@@ -8,7 +8,7 @@ library raises if ``libcpd.so`` is missing or the device is not an sm_100 GPU.
 """
 from ._lib import (  # noqa: F401
     CPDError, load_library, cpd_opts, CPD_NCCL_ID_BYTES, CPD_MAX_RANK, CPD_MAX_ORDER,
-    cpd_nccl_unique_id, cpd_gen_tensor, cpd_ttm, cpd_ttm_i8, cpd_mttv, EXPORTED_SYMBOLS,
+    cpd_nccl_unique_id, cpd_gen_tensor, cpd_gen_tensor_block, cpd_ttm, cpd_ttm_i8, cpd_mttv, EXPORTED_SYMBOLS,
     cpd_local_group_create, cpd_local_group_destroy,
 )
 from .model import CPDecomposition, cp_als_init  # noqa: F401

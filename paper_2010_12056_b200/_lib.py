@@ -21,7 +21,7 @@ EXPORTED_SYMBOLS = [
     "cpd_set_factors", "cpd_get_phase_ms", "cpd_get_counters", "cpd_reset_counters",
     "cpd_debug_get_pp_operator", "cpd_last_error", "cpd_destroy", "cpd_gen_tensor", "cpd_ttm", "cpd_ttm_i8", "cpd_ttm_engine", "cpd_set_tensor",
     "cpd_last_sweep_status",
-    "cpd_mttv", "cpd_local_group_create", "cpd_local_group_destroy", "cpd_set_profile_level",
+    "cpd_mttv", "cpd_gen_tensor_block", "cpd_local_group_create", "cpd_local_group_destroy", "cpd_set_profile_level",
 ]
 
 
@@ -35,7 +35,8 @@ class cpd_opts(C.Structure):
     _fields_ = [("struct_size", C.c_uint32), ("device", C.c_int), ("rank", C.c_int), ("world", C.c_int),
                 ("nccl_unique_id", C.c_void_p), ("stream", C.c_void_p), ("pp_eps", C.c_double),
                 ("reuse_root_in_pp_init", C.c_int), ("profile_phases", C.c_int), ("local_group", C.c_void_p),
-                ("ttm_impl", C.c_int)]
+                ("ttm_impl", C.c_int), ("grid", C.c_int * CPD_MAX_ORDER),
+                ("fused_rs", C.c_int)]
 
 
 _lib = None
@@ -74,6 +75,9 @@ def load_library():
         "cpd_destroy": (C.c_int, [_P]),
         "cpd_gen_tensor": (C.c_int, [_P, C.c_int, C.POINTER(C.c_int64), C.c_int64, C.c_int64, C.c_int,
                                      C.POINTER(_D), C.c_int, C.c_double, C.c_uint64, _P]),
+        "cpd_gen_tensor_block": (C.c_int, [_P, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                           C.POINTER(C.c_int64), C.c_int, C.POINTER(_D), C.c_int, C.c_double,
+                                           C.c_uint64, _P]),
         "cpd_ttm": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, _P, C.c_int, _P, _P]),
         "cpd_ttm_engine": (C.c_int, [_P, C.POINTER(C.c_int)]),
         "cpd_last_sweep_status": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_double)]),
@@ -129,6 +133,17 @@ def cpd_gen_tensor(T, shape, lo, hi, kind, At, noise_std, seed, stream=None):
     Rt = At[0].shape[1] if At else 0
     check(load_library().cpd_gen_tensor(C.c_void_p(T.data_ptr()), len(shape), shp, lo, hi, kind, arr, Rt,
                                         float(noise_std), C.c_uint64(seed), _stream_ptr(stream)))
+
+
+def cpd_gen_tensor_block(T, shape, lo, hi, kind, At, noise_std, seed, stream=None):
+    """Fill the torch CUDA tensor T with the block [lo_n, hi_n) of the synthetic tensor."""
+    n = len(shape)
+    shp, l, h = (C.c_int64 * n)(*shape), (C.c_int64 * n)(*lo), (C.c_int64 * n)(*hi)
+    At = [np.ascontiguousarray(a, dtype=np.float64) for a in At] if At is not None else None
+    arr = dptr_array(At) if At else None
+    Rt = At[0].shape[1] if At else 0
+    check(load_library().cpd_gen_tensor_block(C.c_void_p(T.data_ptr()), n, shp, l, h, kind, arr, Rt,
+                                              float(noise_std), C.c_uint64(seed), _stream_ptr(stream)))
 
 
 def cpd_ttm(T, pre, K, post, A, R, out, stream=None):

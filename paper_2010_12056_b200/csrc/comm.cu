@@ -1,6 +1,9 @@
 // Collective backends of the 1-D grid (see comm.h).
+#include <algorithm>
 #include <condition_variable>
+#include <map>
 #include <mutex>
+#include <utility>
 #include <vector>
 
 #include "comm.h"
@@ -19,8 +22,12 @@ struct LocalGroup {
   std::vector<cudaEvent_t> ev_in, ev_out;
   std::vector<double*> scratch;
   std::vector<size_t> cap;
+  // sub-groups (N-D processor grid): colour/key published per rank, children by (split number, colour)
+  std::vector<int> colors, keys, nsplit;
+  std::map<std::pair<int, int>, LocalGroup*> children;
   explicit LocalGroup(int w)
-      : world(w), src(w), dst(w), ev_in(w, nullptr), ev_out(w, nullptr), scratch(w, nullptr), cap(w, 0) {}
+      : world(w), src(w), dst(w), ev_in(w, nullptr), ev_out(w, nullptr), scratch(w, nullptr), cap(w, 0),
+        colors(w, 0), keys(w, 0), nsplit(w, 0) {}
   void barrier() {
     std::unique_lock<std::mutex> lk(mu);
     long g = gen;
@@ -111,6 +118,7 @@ LocalGroup* local_group_create(int world) {
 }
 void local_group_destroy(LocalGroup* g) {
   if (!g) return;
+  for (auto& kv : g->children) local_group_destroy(kv.second);
   for (int q = 0; q < g->world; q++) {
     if (g->ev_in[q]) cudaEventDestroy(g->ev_in[q]);
     if (g->ev_out[q]) cudaEventDestroy(g->ev_out[q]);
@@ -119,6 +127,32 @@ void local_group_destroy(LocalGroup* g) {
   delete g;
 }
 int local_group_world(const LocalGroup* g) { return g ? g->world : 0; }
+
+// collective over g's ranks (each from its own thread, same call order): the ranks with equal
+// `color` form one child group, ordered by (key, rank); the child is created once, owned by g
+int local_group_split(LocalGroup* g, int rank, int color, int key, LocalGroup** out, int* out_rank, int* out_size) {
+  g->colors[rank] = color;
+  g->keys[rank] = key;
+  g->barrier();
+  std::vector<std::pair<int, int>> mem;
+  for (int q = 0; q < g->world; q++)
+    if (g->colors[q] == color) mem.push_back({g->keys[q], q});
+  std::sort(mem.begin(), mem.end());
+  int me = 0;
+  for (int k = 0; k < (int)mem.size(); k++)
+    if (mem[k].second == rank) me = k;
+  const int seq = g->nsplit[rank]++;
+  {
+    std::lock_guard<std::mutex> lk(g->mu);
+    auto& ch = g->children[{seq, color}];
+    if (!ch) ch = new LocalGroup((int)mem.size());
+    *out = ch;
+  }
+  *out_rank = me;
+  *out_size = (int)mem.size();
+  g->barrier();  // colours/keys may be overwritten by the next split only after every rank read them
+  return 0;
+}
 
 int comm_reduce_scatter(Comm& c, const double* send, double* recv, int64_t count, std::string* msg) {
   if (c.world == 1) return 0;
@@ -183,6 +217,78 @@ int comm_group_start(Comm& c, std::string* msg) {
 int comm_group_end(Comm& c, std::string* msg) {
   if (c.world == 1 || c.lg) return 0;
   return nccl_fail(ncclGroupEnd(), msg);
+}
+
+}  // namespace cpd
+
+namespace cpd {
+
+int comm_split(const Comm& parent, int color, int key, Comm* out, std::string* msg) {
+  *out = parent;
+  if (parent.world == 1) return 0;
+  if (parent.lg) {
+    LocalGroup* ch = nullptr;
+    int r = 0, w = 1;
+    local_group_split(parent.lg, parent.rank, color, key, &ch, &r, &w);
+    out->lg = ch;
+    out->rank = r;
+    out->world = w;
+    out->nccl = nullptr;
+    return 0;
+  }
+  ncclComm_t nc = nullptr;
+  ncclResult_t e = ncclCommSplit(parent.nccl, color, key, &nc, nullptr);
+  if (e != ncclSuccess) {
+    if (msg) *msg = std::string("ncclCommSplit: ") + ncclGetErrorString(e);
+    return 5;
+  }
+  int r = 0, w = 1;
+  ncclCommUserRank(nc, &r);
+  ncclCommCount(nc, &w);
+  out->nccl = nc;
+  out->lg = nullptr;
+  out->rank = r;
+  out->world = w;
+  out->owns_nccl = true;
+  return 0;
+}
+
+void comm_free(Comm& c) {
+  if (c.owns_nccl && c.nccl) ncclCommDestroy(c.nccl);
+  c.nccl = nullptr;
+  c.owns_nccl = false;
+}
+
+}  // namespace cpd
+
+namespace cpd {
+
+// every rank of c learns every rank's `mine` (host pointer values; local group only)
+int comm_exchange_ptr(Comm& c, void* mine, void** all, std::string* msg) {
+  if (c.world == 1) {
+    all[0] = mine;
+    return 0;
+  }
+  if (!c.lg) {
+    if (msg) *msg = "comm_exchange_ptr: local group only";
+    return 4;
+  }
+  LocalGroup* g = c.lg;
+  g->dst[c.rank] = static_cast<double*>(mine);
+  g->barrier();
+  for (int q = 0; q < g->world; q++) all[q] = g->dst[q];
+  g->barrier();
+  return 0;
+}
+
+// stream-ordered barrier: work enqueued on c.st before it is complete on every rank before any
+// rank's later work runs (local group: events + host barrier; NCCL: a one-element all-reduce)
+int comm_barrier(Comm& c, double* scratch1, std::string* msg) {
+  if (c.world == 1) return 0;
+  if (!c.lg) return nccl_fail(ncclAllReduce(scratch1, scratch1, 1, ncclDouble, ncclSum, c.nccl, c.st), msg);
+  int r;
+  if ((r = local_enter(c, nullptr, nullptr, msg))) return r;
+  return local_leave(c, msg);
 }
 
 }  // namespace cpd

@@ -70,17 +70,35 @@ struct cpd_ctx {
   int N = 0, R = 0;
   int64_t shape[CPD_MAX_ORDER] = {0};
   int rank = 0, world = 1;
-  int64_t sN_loc = 0, lo = 0;
+  // processor grid I_1 x ... x I_N (Alg. 3): this rank's coordinates x_n (row-major rank
+  // order, last mode fastest) and block extents loc[n] = s_n / I_n; the 1-D default is 1 x..x 1 x P
+  int grid[CPD_MAX_ORDER] = {0}, coord[CPD_MAX_ORDER] = {0};
+  int64_t loc[CPD_MAX_ORDER] = {0};
   int dev = 0;
   cudaStream_t st = nullptr;
   bool own_stream = false;
+  // every device allocation of the ctx comes from this private stream-ordered pool (release
+  // threshold unbounded, so the node cache's repeat allocations never map memory again); the
+  // process's default pool (PyTorch, other contexts) is left untouched, and cpd_destroy trims
+  // and destroys the pool so all of it returns to the device
+  cudaMemPool_t pool = nullptr;
   // the library's work runs on its own stream `st` (priority above the default so the PP filler
   // stream st3 never delays the critical path); `ust` is the caller's stream (opts.stream),
   // ordered before each call's work and after it by events
   cudaStream_t ust = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   ncclComm_t comm = nullptr;
-  cpd::Comm cm;              // collective backend (NCCL or in-process local group)
+  cpd::Comm cm;              // collective backend (NCCL or in-process local group), all ranks
+  // per mode: Proc-Slice(x_n) (ranks with the same x_n: reduce-scatter of M^(n), all-gather of the
+  // A^(n) block) and the fiber (ranks that differ only in x_n: gathers of the global A^(n), Grams)
+  cpd::Comm slice[CPD_MAX_ORDER], fiber[CPD_MAX_ORDER];
+  // fused reduce-scatter epilogue (opts.fused_rs): per mode with a multi-rank slice, this
+  // rank's receive buffer [slice world][own rows x R] (NCCL: ncclMemAlloc'd symmetric window) and the
+  // map of its own slot in every slice peer's buffer
+  double* rs_recv[CPD_MAX_ORDER] = {};
+  void* rs_win[CPD_MAX_ORDER] = {};
+  cpd::OutMap rs_map[CPD_MAX_ORDER] = {};
+  double* bar_scratch = nullptr;
   const double* T = nullptr;
   int64_t T_elems = 0;
   cpd_opts opts{};
@@ -193,12 +211,11 @@ cpd_status fail(cpd_ctx* c, cpd_status s, const std::string& msg) {
     if (s_ != CPD_OK) return s_;      \
   } while (0)
 
-inline int64_t ext(const cpd_ctx* c, int m) { return m == c->N - 1 ? c->sN_loc : c->shape[m]; }
-inline int64_t rows_own(const cpd_ctx* c, int n) {
-  return n == c->N - 1 ? c->sN_loc : c->shape[n] / c->world;
-}
-inline int64_t own_off(const cpd_ctx* c, int n) {  // row offset of own rows in the local buffer
-  return n == c->N - 1 ? 0 : c->rank * (c->shape[n] / c->world);
+inline int64_t ext(const cpd_ctx* c, int m) { return c->loc[m]; }
+// own rows of mode n (the Q distribution of Alg. 3): the block's loc[n] rows split over Proc-Slice(x_n)
+inline int64_t rows_own(const cpd_ctx* c, int n) { return c->loc[n] / c->slice[n].world; }
+inline int64_t own_off(const cpd_ctx* c, int n) {  // row offset of own rows in the local block
+  return c->slice[n].rank * rows_own(c, n);
 }
 inline int64_t node_elems(const cpd_ctx* c, const std::vector<int>& kept) {
   int64_t e = c->R;
@@ -221,32 +238,44 @@ struct PhaseScope {
   cpd_ctx* c;
   PhaseRec rec;
   bool on;
+  cudaStream_t s;
   // profile level 1: only the two roofline kernels (TTM, mTTV) are bracketed, so the timers
-  // add ~4 event records per mode update; level 2: every phase (P:748 breakdown)
-  PhaseScope(cpd_ctx* ctx, int phase)
-      : c(ctx), on(ctx->opts.profile_phases >= 2 || (ctx->opts.profile_phases == 1 && phase <= PH_MTTV)) {
+  // add ~4 event records per mode update; level 2: every phase (P:748 breakdown).  `stream`: the
+  // stream the bracketed launch goes to (default the main stream; the PP filler stream's operator
+  // streams are timed on their own stream, so the stream ledger's bytes and times match)
+  PhaseScope(cpd_ctx* ctx, int phase, cudaStream_t stream = nullptr)
+      : c(ctx), on(ctx->opts.profile_phases >= 2 || (ctx->opts.profile_phases == 1 && phase <= PH_MTTV)),
+        s(stream ? stream : ctx->st) {
     if (on) {
       rec.a = get_event(c);
       rec.b = get_event(c);
       rec.phase = phase;
-      cudaEventRecord(rec.a, c->st);
+      cudaEventRecord(rec.a, s);
     }
   }
   ~PhaseScope() {
     if (on) {
-      cudaEventRecord(rec.b, c->st);
+      cudaEventRecord(rec.b, s);
       c->pending.push_back(rec);
     }
   }
 };
-void drain_timers(cpd_ctx* c) {  // call after a stream sync
+// accumulate the completed timers; ones still in flight (filler-stream work) stay pending
+void drain_timers(cpd_ctx* c, bool all = false) {
+  std::vector<PhaseRec> keep;
   for (auto& r : c->pending) {
+    if (!all && cudaEventQuery(r.b) == cudaErrorNotReady) {
+      cudaGetLastError();
+      keep.push_back(r);
+      continue;
+    }
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) c->phase_ms[r.phase] += ms;
+    cudaGetLastError();
     c->free_events.push_back(r.a);
     c->free_events.push_back(r.b);
   }
-  c->pending.clear();
+  c->pending.swap(keep);
 }
 
 // ---------------- memory ----------------
@@ -272,12 +301,13 @@ cpd_status dalloc(cpd_ctx* ctx, double** p, int64_t elems) {
   }
   static const bool dbg = getenv("CPD_DEBUG_ALLOC") != nullptr;
   auto t0 = std::chrono::steady_clock::now();
-  cudaError_t e = cudaMallocAsync((void**)p, bytes, ctx->st);
+  cudaError_t e = cudaMallocFromPoolAsync((void**)p, bytes, ctx->pool, ctx->st);
   if (e == cudaErrorMemoryAllocation) {  // give the cached blocks back and retry once
     cudaGetLastError();
     release_cache(ctx);
     cudaStreamSynchronize(ctx->st);
-    e = cudaMallocAsync((void**)p, bytes, ctx->st);
+    cudaMemPoolTrimTo(ctx->pool, 0);
+    e = cudaMallocFromPoolAsync((void**)p, bytes, ctx->pool, ctx->st);
   }
   CU(e);
   ctx->node_bytes[(void*)*p] = bytes;
@@ -287,6 +317,9 @@ cpd_status dalloc(cpd_ctx* ctx, double** p, int64_t elems) {
   }
   return CPD_OK;
 }
+// raw (non-node) device buffer from the ctx's pool
+cudaError_t palloc(cpd_ctx* c, void** p, size_t bytes) { return cudaMallocFromPoolAsync(p, bytes, c->pool, c->st); }
+
 void dfree(cpd_ctx* c, double*& p) {
   if (p) c->node_cache.emplace(c->node_bytes[(void*)p], (void*)p);
   p = nullptr;
@@ -320,7 +353,7 @@ cpd_status ttm(cpd_ctx* ctx, int j, double* out) {
 
 // out = beta*out + contraction of node X (kept) over mode m with v (ext(m) x R)
 cpd_status mttv(cpd_ctx* ctx, const double* X, const std::vector<int>& kept, int m,
-                const double* v, double* out, int beta) {
+                const double* v, double* out, int beta, const cpd::OutMap* map = nullptr) {
   int a = (int)(std::find(kept.begin(), kept.end(), m) - kept.begin());
   if (a >= (int)kept.size()) return fail(ctx, CPD_ERR_INTERNAL, "mttv: mode not kept");
   int64_t pre = 1, post = 1;
@@ -328,7 +361,10 @@ cpd_status mttv(cpd_ctx* ctx, const double* X, const std::vector<int>& kept, int
   for (int q = a + 1; q < (int)kept.size(); q++) post *= ext(ctx, kept[q]);
   int64_t K = ext(ctx, m);
   PhaseScope ps(ctx, PH_MTTV);
-  CU(cpd::launch_mttv(X, pre, K, post, ctx->R, v, out, beta, ctx->ws_mttv, kMttvWs, ctx->st));
+  {
+    cpd::MttvSpec sp{X, v, pre, K, post};
+    CU(cpd::launch_mttv_multi(&sp, 1, ctx->R, nullptr, out, beta, ctx->ws_mttv, kMttvWs, ctx->st, map));
+  }
   double C = (double)post * ctx->R;
   ctx->counters[2] += 8.0 * ((double)pre * K * C + (double)pre * C * (beta ? 2 : 1) + (double)K * ctx->R);
   ctx->counters[3] += 1;
@@ -336,8 +372,13 @@ cpd_status mttv(cpd_ctx* ctx, const double* X, const std::vector<int>& kept, int
 }
 
 // contract the modes `drop` of a node in `order`, returning a new node (input not freed)
+// `map` (fused reduce-scatter): the contraction that produces the final node stores it into the
+// owners' receive slots instead (the node buffer is then left unwritten)
 cpd_status contract_modes(cpd_ctx* ctx, const Node& in, const std::vector<int>& drop,
-                          const std::vector<int>& order, Node* out) {
+                          const std::vector<int>& order, Node* out, const cpd::OutMap* map = nullptr) {
+  int remaining = 0;
+  for (int m : order)
+    if (std::find(drop.begin(), drop.end(), m) != drop.end()) remaining++;
   Node cur;
   cur.buf = in.buf;
   cur.kept = in.kept;
@@ -348,7 +389,7 @@ cpd_status contract_modes(cpd_ctx* ctx, const Node& in, const std::vector<int>& 
     for (int k : cur.kept)
       if (k != m) nx.kept.push_back(k);
     TRY(dalloc(ctx, &nx.buf, node_elems(ctx, nx.kept)));
-    TRY(mttv(ctx, cur.buf, cur.kept, m, ctx->A[m], nx.buf, 0));
+    TRY(mttv(ctx, cur.buf, cur.kept, m, ctx->A[m], nx.buf, 0, --remaining == 0 ? map : nullptr));
     if (owned) dfree(ctx, cur.buf);
     cur = nx;
     owned = true;
@@ -387,7 +428,12 @@ cpd_status start_subtree(cpd_ctx* ctx, int j, const std::vector<int>& pre, const
 }
 
 // leaf q of the live subtree (lazy binary descent, O3)
-cpd_status subtree_leaf(cpd_ctx* ctx, int q, const double** leaf) {
+// fused reduce-scatter map of mode n, or null
+const cpd::OutMap* rs_map_of(const cpd_ctx* c, int n) { return c->rs_map[n].nq > 0 ? &c->rs_map[n] : nullptr; }
+
+// *scattered: the leaf was computed now straight into the owners' receive slots (fused RS)
+cpd_status subtree_leaf(cpd_ctx* ctx, int q, const double** leaf, bool* scattered) {
+  *scattered = false;
   auto& sub = ctx->sub;
   const auto& L = sub.served;
   int lo = 0, hi = (int)L.size();
@@ -418,7 +464,10 @@ cpd_status subtree_leaf(cpd_ctx* ctx, int q, const double** leaf) {
       const Node& parent = sub.cache[{lo, hi}];
       std::vector<int> order(L.begin() + lo, L.begin() + hi);
       Node nx;
-      TRY(contract_modes(ctx, parent, drop, order, &nx));
+      const bool is_leaf = child.second - child.first == 1;
+      const cpd::OutMap* mp = is_leaf ? rs_map_of(ctx, L[q]) : nullptr;
+      TRY(contract_modes(ctx, parent, drop, order, &nx, mp));
+      if (mp) *scattered = true;
       sub.cache[child] = nx;
     }
     lo = child.first;
@@ -431,17 +480,30 @@ cpd_status subtree_leaf(cpd_ctx* ctx, int q, const double** leaf) {
   return CPD_OK;
 }
 
-cpd_status allreduce_lastmode(cpd_ctx* ctx, bool with_dS) {
+// after the update of mode n's own rows (Alg. 3 lines 15-18, Alg. 4 lines 13-15): S^(n) (and dS^(n))
+// and the ||dA||^2, ||A||^2 (and <M^(N), A^(N)>) partial sums of the own rows all-reduced over all
+// ranks (line 17), then the A^(n) (and dA^(n)) block all-gathered in Proc-Slice(x_n) (line 18)
+cpd_status exchange_mode(cpd_ctx* ctx, int n, bool pp) {
   if (ctx->world == 1) return CPD_OK;
-  const int64_t RR = (int64_t)ctx->R * ctx->R;
+  const int R = ctx->R;
+  const int64_t RR = (int64_t)R * R;
+  const bool last = n == ctx->N - 1;
   PhaseScope ps(ctx, PH_OTHER);
   CM(cpd::comm_group_start(ctx->cm, &m_));
-  CM(cpd::comm_all_reduce(ctx->cm, ctx->S_all + (ctx->N - 1) * RR, RR, &m_));
-  if (with_dS) CM(cpd::comm_all_reduce(ctx->cm, ctx->dS_all + (ctx->N - 1) * RR, RR, &m_));
-  CM(cpd::comm_all_reduce(ctx->cm, ctx->scal + SC_MA, 1, &m_));
-  CM(cpd::comm_all_reduce(ctx->cm, ctx->scal + SC_DA2 + ctx->N - 1, 1, &m_));
-  CM(cpd::comm_all_reduce(ctx->cm, ctx->scal + SC_A2 + ctx->N - 1, 1, &m_));
+  CM(cpd::comm_all_reduce(ctx->cm, ctx->S_all + n * RR, RR, &m_));
+  if (pp) CM(cpd::comm_all_reduce(ctx->cm, ctx->dS_all + n * RR, RR, &m_));
+  if (last) CM(cpd::comm_all_reduce(ctx->cm, ctx->scal + SC_MA, 1, &m_));
+  CM(cpd::comm_all_reduce(ctx->cm, ctx->scal + SC_DA2 + n, 1, &m_));
+  CM(cpd::comm_all_reduce(ctx->cm, ctx->scal + SC_A2 + n, 1, &m_));
   CM(cpd::comm_group_end(ctx->cm, &m_));
+  cpd::Comm& sl = ctx->slice[n];
+  if (sl.world > 1) {
+    const int64_t ro = rows_own(ctx, n), off = own_off(ctx, n);
+    CM(cpd::comm_group_start(sl, &m_));
+    CM(cpd::comm_all_gather(sl, ctx->A[n] + off * R, ctx->A[n], ro * R, &m_));
+    CM(cpd::comm_all_gather(sl, ctx->dA[n] + off * R, ctx->dA[n], ro * R, &m_));
+    CM(cpd::comm_group_end(sl, &m_));
+  }
   return CPD_OK;
 }
 
@@ -469,7 +531,7 @@ __global__ void gamma_dot_kernel(const double* __restrict__ S_all, int N, int R,
 bool use_fused(const cpd_ctx* ctx, int n, bool pp) {
   const int64_t ro = rows_own(ctx, n);
   const int blocks = cpd::update_fused_blocks(ro);
-  return ctx->R <= cpd::kUpdMaxR && ctx->Gi[0] && (ctx->world == 1 || n == ctx->N - 1) &&
+  return ctx->R <= cpd::kUpdMaxR && ctx->Gi[0] &&
          cpd::update_fused_smem(ctx->R, pp, (int)((ro + blocks - 1) / blocks)) <= 225 * 1024;
 }
 
@@ -482,18 +544,19 @@ cpd_status prefetch_solve(cpd_ctx* ctx, int m, bool pp) {
   const int b = ctx->pf_buf ^ 1;
   CU(cudaEventRecord(ctx->ev_s, ctx->st));
   CU(cudaStreamWaitEvent(ctx->st2, ctx->ev_s, 0));
-  // status written straight to status[m]: a prefetch for the next sweep may overwrite it
-  // while finish_sweep reads it -- either value is a valid SPD verdict for Γ^(m)
+  // the SPD verdict goes to pf_status[b] (side stream); the update that consumes buffer b hands
+  // it to status[m] on the main stream (acquire_solve), so every status finish_sweep reads is
+  // ordered on the main stream and a prefetch for the next sweep never touches this sweep's
   const bool fz = use_fused(ctx, m, pp);
+  int* pst = ctx->pf_status + b;
   if (fz) {
     // the fused update multiplies by Γ^{-1}: form it directly (Gauss-Jordan, SPD check)
-    CU(cpd::launch_gamma_inverse(ctx->S_all, ctx->N, m, ctx->R, ctx->Gi[b], ctx->status + m, ctx->st2));
+    CU(cpd::launch_gamma_inverse(ctx->S_all, ctx->N, m, ctx->R, ctx->Gi[b], pst, ctx->st2));
   } else if (ctx->R > kCholMaxR) {
     // beyond the single-CTA packed Cholesky: Γ^{-1} by the grid-wide blocked Gauss-Jordan
-    CU(cpd::launch_gamma_inverse_big(ctx->S_all, ctx->N, m, ctx->R, ctx->ws_gj, ctx->Gi[b], ctx->status + m,
-                                     ctx->st2));
+    CU(cpd::launch_gamma_inverse_big(ctx->S_all, ctx->N, m, ctx->R, ctx->ws_gj, ctx->Gi[b], pst, ctx->st2));
   } else {
-    CU(cpd::launch_gamma_chol(ctx->S_all, ctx->N, m, ctx->R, ctx->Lp[b], ctx->status + m, ctx->st2));
+    CU(cpd::launch_gamma_chol(ctx->S_all, ctx->N, m, ctx->R, ctx->Lp[b], pst, ctx->st2));
   }
   if (pp) CU(cpd::launch_pp_w(ctx->S_all, ctx->dS_all, ctx->N, m, ctx->R, ctx->Wb[b], ctx->st2));
   CU(cudaEventRecord(ctx->ev_pf, ctx->st2));
@@ -506,108 +569,92 @@ cpd_status prefetch_solve(cpd_ctx* ctx, int m, bool pp) {
 
 void invalidate_prefetch(cpd_ctx* ctx) { ctx->pf_mode = -1; }
 
-cpd_status acquire_solve(cpd_ctx* ctx, int n, bool pp, int* buf) {
+// wait for the prepared Γ factor of mode n; `fused`: the fused update kernel copies the SPD
+// verdict pf_status[b] -> status[n] itself, otherwise it is copied here on the main stream
+cpd_status acquire_solve(cpd_ctx* ctx, int n, bool pp, int* buf, bool fused) {
   if (!(ctx->pf_mode == n && (ctx->pf_pp || !pp) && ctx->pf_fused == use_fused(ctx, n, pp)))
     TRY(prefetch_solve(ctx, n, pp));
   CU(cudaStreamWaitEvent(ctx->st, ctx->ev_pf, 0));
   *buf = ctx->pf_buf;
   ctx->pf_mode = -1;
-
+  if (!fused)
+    CU(cudaMemcpyAsync(ctx->status + n, ctx->pf_status + *buf, sizeof(int), cudaMemcpyDeviceToDevice, ctx->st));
   return CPD_OK;
 }
 
-// Solve-and-update for mode n given the local (partial for n<N-1) MTTKRP Mloc
-// (ext(n) x R, may be overwritten).  pp: dA = A - A_p and dS maintained; Vterm: add
-// V = A^(n) W before the solve (Eq. 7).
-cpd_status update_mode(cpd_ctx* ctx, int n, double* Mloc, bool pp) {
+// Solve-and-update for mode n given the local (block-partial) MTTKRP Mloc (ext(n) x R, may be
+// overwritten): reduce-scatter in Proc-Slice(x_n) to the own rows (Alg. 3 line 14), solve them
+// (line 15; pp: V = A^(n) W added first, Eq. 7), dA, statistics, S (and dS) of the own rows, then
+// exchange_mode (all-reduce, all-gather of the block).
+cpd_status update_mode(cpd_ctx* ctx, int n, double* Mloc, bool pp, bool scattered = false) {
   const int R = ctx->R;
   const int64_t RR = (int64_t)R * R;
   const int64_t ro = rows_own(ctx, n), off = own_off(ctx, n);
-  const int64_t rows_full = ext(ctx, n);
   double* Mown = Mloc + off * R;
   const bool last = n == ctx->N - 1;
   const bool fused = use_fused(ctx, n, pp);
-  if (fused) {
-    // fused: V term, row solve, dA, statistics, S (and dS) in one cooperative launch
-    int b;
-    TRY(acquire_solve(ctx, n, pp, &b));
-    {
-      PhaseScope ps(ctx, PH_OTHER);
-      if (pp) {
-        ctx->Mlast_src[n] = Mloc;  // persistent M~ buffer: no copy, read on demand
-      } else {
-        ctx->Mlast_src[n] = nullptr;
-        CU(cudaMemcpyAsync(ctx->Mlast[n] + off * R, Mown, sizeof(double) * ro * R, cudaMemcpyDeviceToDevice,
-                           ctx->st));
-      }
-    }
-    {
-      PhaseScope ps(ctx, PH_SOLVE);
-      CU(cpd::launch_update_fused(R, ro, ctx->Gi[b], pp ? ctx->Wb[b] : nullptr, Mown, ctx->A[n] + off * R,
-                                  pp ? ctx->Ap[n] + off * R : nullptr, ctx->dA[n] + off * R, ctx->S_all + n * RR,
-                                  pp ? ctx->dS_all + n * RR : nullptr, ctx->upd_part, ctx->upd_gpart,
-                                  ctx->scal + SC_DA2 + n, ctx->scal + SC_A2 + n, last ? ctx->scal + SC_MA : nullptr,
-                                  ctx->st));
-    }
-    if (last) {
-      TRY(allreduce_lastmode(ctx, pp));
-      PhaseScope ps(ctx, PH_OTHER);
-      cpd::g_launches++;
-      gamma_dot_kernel<<<1, 1024, 0, ctx->st>>>(ctx->S_all, ctx->N, R, ctx->scal + SC_GS);
-      CU(cudaGetLastError());
-    }
-    TRY(prefetch_solve(ctx, (n + 1) % ctx->N, pp));
-    return CPD_OK;
-  }
-  if (n < ctx->N - 1 && ctx->world > 1) {
+  if (scattered) {
+    // fused reduce-scatter: every slice rank stored its partial rows into its slot of the owner's
+    // receive buffer; after the stream-ordered barrier the owner sums the slots in rank order
     PhaseScope ps(ctx, PH_OTHER);
-    CM(cpd::comm_reduce_scatter(ctx->cm, Mloc, Mown, ro * R, &m_));
+    CM(cpd::comm_barrier(ctx->slice[n], ctx->bar_scratch, &m_));
+    CU(cpd::launch_slot_sum(ctx->rs_recv[n], ctx->slice[n].world, ro * R, Mown, ctx->st));
+  } else if (ctx->slice[n].world > 1) {
+    PhaseScope ps(ctx, PH_OTHER);
+    CM(cpd::comm_reduce_scatter(ctx->slice[n], Mloc, Mown, ro * R, &m_));
   }
-  // Γ^(n) factor (and W^(n) for PP): prepared on the side stream while the MTTKRP of
-  // mode n streamed, or computed here if no matching prefetch is pending
+  // Γ^(n) factor (and W^(n) for PP): prepared on the side stream while the MTTKRP of mode n
+  // streamed, or computed here if no matching prefetch is pending
   int b;
-  TRY(acquire_solve(ctx, n, pp, &b));
-  if (pp) {
-    // V^(n) = A^(n) W^(n) with the current (pre-update) A^(n): Eq. 7; M~ += V (Eq. 5)
-    PhaseScope ps(ctx, PH_HAD);
-    CU(cpd::launch_ttm(ctx->A[n] + off * R, ro, R, 1, ctx->Wb[b], R, Mown, 1, ctx->st));
-  }
+  TRY(acquire_solve(ctx, n, pp, &b, fused));
   {
     PhaseScope ps(ctx, PH_OTHER);
     if (pp) {
       ctx->Mlast_src[n] = Mloc;  // persistent M~ buffer: no copy, read on demand
     } else {
       ctx->Mlast_src[n] = nullptr;
-      CU(cudaMemcpyAsync(ctx->Mlast[n] + off * R, Mown, sizeof(double) * ro * R, cudaMemcpyDeviceToDevice,
-                         ctx->st));
+      CU(cudaMemcpyAsync(ctx->Mlast[n] + off * R, Mown, sizeof(double) * ro * R, cudaMemcpyDeviceToDevice, ctx->st));
     }
-    if (!pp)
-      CU(cudaMemcpyAsync(ctx->Aold[n], ctx->A[n], sizeof(double) * rows_full * R,
-                         cudaMemcpyDeviceToDevice, ctx->st));
   }
-  {
+  if (fused) {
+    // fused: V term, row solve, dA, statistics, S (and dS) of the own rows in one cooperative launch
     PhaseScope ps(ctx, PH_SOLVE);
-    if (R > kCholMaxR)  // x = M Γ^{-1} as a GEMM on the DMMA kernel
-      CU(cpd::launch_ttm(Mown, ro, R, 1, ctx->Gi[b], R, ctx->A[n] + off * R, 0, ctx->st));
-    else
-      CU(cpd::launch_trisolve(ctx->Lp[b], Mown, ro, R, ctx->A[n] + off * R, ctx->st));
+    CU(cpd::launch_update_fused(R, ro, ctx->Gi[b], pp ? ctx->Wb[b] : nullptr, Mown, ctx->A[n] + off * R,
+                                pp ? ctx->Ap[n] + off * R : nullptr, ctx->dA[n] + off * R, ctx->S_all + n * RR,
+                                pp ? ctx->dS_all + n * RR : nullptr, ctx->upd_part, ctx->upd_gpart,
+                                ctx->scal + SC_DA2 + n, ctx->scal + SC_A2 + n, last ? ctx->scal + SC_MA : nullptr,
+                                ctx->pf_status + b, ctx->status + n, ctx->st));
+  } else {
+    if (pp) {
+      // V^(n) = A^(n) W^(n) with the current (pre-update) A^(n): Eq. 7; M~ += V (Eq. 5)
+      PhaseScope ps(ctx, PH_HAD);
+      CU(cpd::launch_ttm(ctx->A[n] + off * R, ro, R, 1, ctx->Wb[b], R, Mown, 1, ctx->st));
+    }
+    if (!pp) {
+      PhaseScope ps(ctx, PH_OTHER);
+      CU(cudaMemcpyAsync(ctx->Aold[n] + off * R, ctx->A[n] + off * R, sizeof(double) * ro * R,
+                         cudaMemcpyDeviceToDevice, ctx->st));
+    }
+    {
+      PhaseScope ps(ctx, PH_SOLVE);
+      if (R > kCholMaxR)  // x = M Γ^{-1} as a GEMM on the DMMA kernel
+        CU(cpd::launch_ttm(Mown, ro, R, 1, ctx->Gi[b], R, ctx->A[n] + off * R, 0, ctx->st));
+      else
+        CU(cpd::launch_trisolve(ctx->Lp[b], Mown, ro, R, ctx->A[n] + off * R, ctx->st));
+    }
+    {
+      PhaseScope ps(ctx, PH_HAD);
+      const double* base = (pp ? ctx->Ap[n] : ctx->Aold[n]) + off * R;
+      // dA, ||dA||^2, ||A||^2 (and <M^(N), A^(N)> of Eq. 3 for the last mode) of the own rows in one pass
+      CU(cpd::launch_update_stats(ctx->A[n] + off * R, base, ctx->dA[n] + off * R, last ? Mown : nullptr, ro * R,
+                                  ctx->st_part, ctx->st_counter, ctx->scal + SC_DA2 + n, ctx->scal + SC_A2 + n,
+                                  ctx->scal + SC_MA, ctx->st));
+      CU(cpd::launch_gram(ctx->A[n] + off * R, ctx->A[n] + off * R, pp ? ctx->dA[n] + off * R : nullptr, ro, R,
+                          ctx->S_all + n * RR, pp ? ctx->dS_all + n * RR : nullptr, ctx->ws_gram, 32 * RR, ctx->st));
+    }
   }
-  if (n < ctx->N - 1 && ctx->world > 1) {
-    PhaseScope ps(ctx, PH_OTHER);
-    CM(cpd::comm_all_gather(ctx->cm, ctx->A[n] + off * R, ctx->A[n], ro * R, &m_));
-  }
-  {
-    PhaseScope ps(ctx, PH_HAD);
-    const double* base = pp ? ctx->Ap[n] : ctx->Aold[n];
-    // dA, ||dA||^2, ||A||^2 (and <M^(N), A^(N)> of Eq. 3 for the last mode) in one pass
-    CU(cpd::launch_update_stats(ctx->A[n], base, ctx->dA[n], last ? Mown : nullptr, rows_full * R, ctx->st_part,
-                                ctx->st_counter, ctx->scal + SC_DA2 + n, ctx->scal + SC_A2 + n,
-                                ctx->scal + SC_MA, ctx->st));
-    CU(cpd::launch_gram(ctx->A[n], ctx->A[n], pp ? ctx->dA[n] : nullptr, rows_full, R, ctx->S_all + n * RR,
-                        pp ? ctx->dS_all + n * RR : nullptr, ctx->ws_gram, 32 * RR, ctx->st));
-  }
-  if (n == ctx->N - 1) {
-    TRY(allreduce_lastmode(ctx, pp));
+  TRY(exchange_mode(ctx, n, pp));
+  if (last) {
     PhaseScope ps(ctx, PH_OTHER);
     cpd::g_launches++;
     gamma_dot_kernel<<<1, 1024, 0, ctx->st>>>(ctx->S_all, ctx->N, R, ctx->scal + SC_GS);
@@ -667,6 +714,15 @@ void free_pp(cpd_ctx* c) {
   c->pp_valid = false;
 }
 
+// the speculative next-sweep PP streams (filler stream st3) read the operators, M_p and dA and
+// write the spare M~ set: the main stream waits for them before it writes any of those
+void drop_spec(cpd_ctx* c) {
+  if (c->pp_spec) {
+    cudaStreamWaitEvent(c->st, c->ev_pp_side[1], 0);
+    c->pp_spec = false;
+  }
+}
+
 // orders a public call's work after the caller's stream and the caller's stream after it
 struct UserSync {
   cpd_ctx* c;
@@ -675,10 +731,7 @@ struct UserSync {
       cudaEventRecord(c->ev_in, c->ust);
       cudaStreamWaitEvent(c->st, c->ev_in, 0);
     }
-    if (c && c->pp_spec && !keep_spec) {  // speculative PP work must finish before anything else
-      cudaStreamWaitEvent(c->st, c->ev_pp_side[1], 0);
-      c->pp_spec = false;
-    }
+    if (c && !keep_spec) drop_spec(c);  // speculative PP work must finish before anything else
   }
   ~UserSync() {
     if (c && c->ev_out) {
@@ -719,8 +772,10 @@ cpd_status regular_sweep(cpd_ctx* ctx, bool msdt, double* f_out) {
       }
       if (ctx->sub.served[q] != n) return fail(ctx, CPD_ERR_INTERNAL, "MSDT schedule out of phase");
       const double* leaf;
-      TRY(subtree_leaf(ctx, q, &leaf));
-      TRY(update_mode(ctx, n, const_cast<double*>(leaf), false));
+      bool sc = false;
+      TRY(subtree_leaf(ctx, q, &leaf, &sc));
+      drop_spec(ctx);  // first write of factor state (dA) in this sweep
+      TRY(update_mode(ctx, n, const_cast<double*>(leaf), false, sc));
       ctx->t++;
     }
   } else {
@@ -742,8 +797,10 @@ cpd_status regular_sweep(cpd_ctx* ctx, bool msdt, double* f_out) {
       }
       int q = n < h ? n : n - h;
       const double* leaf;
-      TRY(subtree_leaf(ctx, q, &leaf));
-      TRY(update_mode(ctx, n, const_cast<double*>(leaf), false));
+      bool sc = false;
+      TRY(subtree_leaf(ctx, q, &leaf, &sc));
+      drop_spec(ctx);
+      TRY(update_mode(ctx, n, const_cast<double*>(leaf), false, sc));
     }
     clear_subtree(ctx);
   }
@@ -786,7 +843,8 @@ cpd_status pp_descend(cpd_ctx* ctx, const Node& node, std::vector<std::pair<int,
 }
 
 // ||T||^2 (all-reduced) and the TTM engine's view of T: exponent and digit planes
-// (cp_als_init, cpd_set_tensor).  Buffers from a previous call are reused.
+// (cp_als_init, cpd_set_tensor).  Buffers from a previous call (exponent, factor-digit
+// workspace, digit planes: all sized by the shape, not the contents) are reused.
 cpd_status prepare_tensor(cpd_ctx* ctx) {
   CU(cpd::launch_norm2(ctx->T, ctx->T_elems, ctx->partial, ctx->scal + SC_NT2, ctx->st));
   {
@@ -802,7 +860,7 @@ cpd_status prepare_tensor(cpd_ctx* ctx) {
   if (o.ttm_impl == CPD_TTM_INT8 || o.ttm_impl == CPD_TTM_AUTO) {
     // one exponent for this rank's slab (T is read-only, so once per ctx); ranks may differ,
     // which changes results only at the rounding level
-    CU(cudaMallocAsync((void**)&ctx->texp, sizeof(int), ctx->st));
+    if (!ctx->texp) CU(palloc(ctx, (void**)&ctx->texp, sizeof(int)));
     CU(cpd::launch_absmax_exp(ctx->T, ctx->T_elems, ctx->partial, ctx->texp, ctx->st, ctx->scal + SC_TMAX));
     bool use_i8 = true;
     if (o.ttm_impl == CPD_TTM_AUTO) {
@@ -815,21 +873,27 @@ cpd_status prepare_tensor(cpd_ctx* ctx) {
       const double rms = std::sqrt(h[SC_NT2] / numel);
       use_i8 = h[SC_TMAX] <= 256.0 * rms;
     }
-    if (!use_i8 && ctx->Td) {
-      cudaFreeAsync(ctx->Td, ctx->st);
+    if (!use_i8) {  // AUTO chose DMMA for these contents: the int8 engine's buffers go back
+      if (ctx->Td) cudaFreeAsync(ctx->Td, ctx->st);
+      if (ctx->ws_i8) cudaFreeAsync(ctx->ws_i8, ctx->st);
       ctx->Td = nullptr;
+      ctx->ws_i8 = nullptr;
+      ctx->ws_i8_bytes = 0;
     }
     if (use_i8) {
       int64_t kmax = 1;
       for (int n = 0; n < N; n++) kmax = std::max(kmax, ext(ctx, n));
-      ctx->ws_i8_bytes = cpd::ttm_i8_workspace_bytes(std::min(kmax, cpd::kMaxKI8), R);
-      CU(cudaMallocAsync(&ctx->ws_i8, ctx->ws_i8_bytes, ctx->st));
+      // the workspace depends only on the shape and R, so a later cpd_set_tensor reuses it
+      if (!ctx->ws_i8) {
+        ctx->ws_i8_bytes = cpd::ttm_i8_workspace_bytes(std::min(kmax, cpd::kMaxKI8), R);
+        CU(palloc(ctx, &ctx->ws_i8, ctx->ws_i8_bytes));
+      }
       ctx->engine = CPD_ENGINE_INT8_CONVERT;
       // T's digit planes once (7 bytes per element): every first-level TTM then streams them
       // instead of converting T; without the memory the TTM converts T on the fly
       const int64_t w = ext(ctx, N - 1);
-      if (ctx->Td || cudaMallocAsync((void**)&ctx->Td, (size_t)7 * cpd::digit_plane_bytes(ctx->T_elems, w),
-                                     ctx->st) == cudaSuccess) {
+      if (ctx->Td || palloc(ctx, (void**)&ctx->Td, (size_t)7 * cpd::digit_plane_bytes(ctx->T_elems, w)) ==
+                         cudaSuccess) {
         CU(cpd::launch_slice_digits(ctx->T, ctx->T_elems, w, ctx->texp, ctx->Td, ctx->st));
         ctx->engine = CPD_ENGINE_INT8_DIGITS;
       } else {
@@ -920,12 +984,20 @@ cpd_status cpd_destroy(cpd_ctx* c) {
   dfree(c, c->scal);
   dfree(c, c->partial);
   dfree(c, c->gather_tmp);
+  dfree(c, c->bar_scratch);
+  for (int n = 0; n < CPD_MAX_ORDER; n++)
+    if (!c->rs_win[n]) dfree(c, c->rs_recv[n]);
   release_cache(c);
   if (c->status) cudaFreeAsync(c->status, c->st);
   if (c->texp) cudaFreeAsync(c->texp, c->st);
   if (c->ws_i8) cudaFreeAsync(c->ws_i8, c->st);
   if (c->Td) cudaFreeAsync(c->Td, c->st);
   cudaStreamSynchronize(c->st);
+  if (c->pool) {  // everything was freed above (stream-ordered): hand the memory back to the device
+    cudaMemPoolTrimTo(c->pool, 0);
+    cudaMemPoolDestroy(c->pool);
+    c->pool = nullptr;
+  }
   for (auto& r : c->pending) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
@@ -933,6 +1005,14 @@ cpd_status cpd_destroy(cpd_ctx* c) {
   for (auto e : c->free_events) cudaEventDestroy(e);
   if (c->hscal) cudaFreeHost(c->hscal);
   if (c->hstatus) cudaFreeHost(c->hstatus);
+  for (int n = 0; n < CPD_MAX_ORDER; n++) {
+    if (c->rs_win[n]) {
+      cpd::nccl_window_free(c->slice[n].nccl, c->rs_recv[n], c->rs_win[n]);
+      c->rs_recv[n] = nullptr;
+    }
+    cpd::comm_free(c->slice[n]);
+    cpd::comm_free(c->fiber[n]);
+  }
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->ev_s) cudaEventDestroy(c->ev_s);
   if (c->ev_pf) cudaEventDestroy(c->ev_pf);
@@ -971,10 +1051,27 @@ cpd_status cp_als_init(cpd_ctx** out, int N, const int64_t* shape, int R, const 
     return fail(ctx, CPD_ERR_INVALID_ARG, "local_group size != world");
   for (int n = 0; n < N; n++)
     if (shape[n] < 1 || !A0_host[n]) return fail(ctx, CPD_ERR_INVALID_ARG, "bad shape or factor");
-  if (shape[N - 1] % o.world != 0) return fail(ctx, CPD_ERR_INVALID_ARG, "s_N must be divisible by world");
-  for (int n = 0; n < N - 1; n++)
-    if (shape[n] % o.world != 0)
-      return fail(ctx, CPD_ERR_INVALID_ARG, "s_n must be divisible by world (reduce-scatter blocks)");
+  // processor grid (Alg. 3 line 1): opts.grid, or the 1-D default 1 x .. x 1 x world
+  int grid[CPD_MAX_ORDER];
+  {
+    bool given = false;
+    for (int n = 0; n < CPD_MAX_ORDER; n++) given |= o.grid[n] != 0;
+    int64_t prod = 1;
+    for (int n = 0; n < N; n++) {
+      grid[n] = given ? o.grid[n] : (n == N - 1 ? o.world : 1);
+      if (grid[n] < 1) return fail(ctx, CPD_ERR_INVALID_ARG, "grid entries must be >= 1");
+      prod *= grid[n];
+    }
+    for (int n = N; n < CPD_MAX_ORDER; n++)
+      if (given && o.grid[n] != 0) return fail(ctx, CPD_ERR_INVALID_ARG, "grid entries beyond N must be 0");
+    if (prod != o.world) return fail(ctx, CPD_ERR_INVALID_ARG, "prod(grid) must equal world");
+    for (int n = 0; n < N; n++) {
+      // blocks of s_n / I_n rows (reading Q20: no padding), own rows of loc / (P / I_n)
+      if (shape[n] % grid[n] != 0) return fail(ctx, CPD_ERR_INVALID_ARG, "s_n must be divisible by grid[n]");
+      if ((shape[n] / grid[n]) % (o.world / grid[n]) != 0)
+        return fail(ctx, CPD_ERR_INVALID_ARG, "s_n / grid[n] must be divisible by world / grid[n] (reduce-scatter)");
+    }
+  }
 
   ctx = new cpd_ctx();
   ctx->N = N;
@@ -982,13 +1079,20 @@ cpd_status cp_als_init(cpd_ctx** out, int N, const int64_t* shape, int R, const 
   for (int n = 0; n < N; n++) ctx->shape[n] = shape[n];
   ctx->rank = o.rank;
   ctx->world = o.world;
-  ctx->sN_loc = shape[N - 1] / o.world;
-  ctx->lo = o.rank * ctx->sN_loc;
+  {
+    int rem = o.rank;
+    for (int n = N - 1; n >= 0; n--) {  // row-major rank order, last mode fastest
+      ctx->grid[n] = grid[n];
+      ctx->coord[n] = rem % grid[n];
+      rem /= grid[n];
+      ctx->loc[n] = shape[n] / grid[n];
+    }
+  }
   ctx->dev = o.device;
   ctx->opts = o;
   ctx->T = T_local_dev;
-  ctx->T_elems = ctx->sN_loc;
-  for (int n = 0; n < N - 1; n++) ctx->T_elems *= shape[n];
+  ctx->T_elems = 1;
+  for (int n = 0; n < N; n++) ctx->T_elems *= ctx->loc[n];
 
   auto bail = [&](cpd_status s) {
     g_init_error = ctx->err;
@@ -1031,10 +1135,14 @@ cpd_status cp_als_init(cpd_ctx** out, int N, const int64_t* shape, int R, const 
     ICU(cudaStreamWaitEvent(ctx->st, ctx->ev_in, 0));
   }
   {
-    cudaMemPool_t pool;
-    ICU(cudaDeviceGetDefaultMemPool(&pool, ctx->dev));
+    cudaMemPoolProps pp{};
+    pp.allocType = cudaMemAllocationTypePinned;
+    pp.handleTypes = cudaMemHandleTypeNone;
+    pp.location.type = cudaMemLocationTypeDevice;
+    pp.location.id = ctx->dev;
+    ICU(cudaMemPoolCreate(&ctx->pool, &pp));
     uint64_t thr = UINT64_MAX;
-    ICU(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    ICU(cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &thr));
   }
   if (o.world > 1 && !o.local_group) {
     ncclUniqueId id;
@@ -1050,6 +1158,30 @@ cpd_status cp_als_init(cpd_ctx** out, int N, const int64_t* shape, int R, const 
   ctx->cm.rank = o.rank;
   ctx->cm.world = o.world;
   ctx->cm.st = ctx->st;
+  {
+    // Proc-Slice(x_n) and the fibre of mode n; the whole world or a single rank need no new
+    // communicator (the 1-D grid: slices of modes < N are the world, of mode N single ranks)
+    cpd::Comm self;
+    self.st = ctx->st;
+    for (int n = 0; n < N; n++) {
+      std::string m;
+      int rest = 0;  // rank with x_n removed
+      for (int k = 0; k < N; k++)
+        if (k != n) rest = rest * grid[k] + ctx->coord[k];
+      if (grid[n] == 1) ctx->slice[n] = ctx->cm;
+      else if (grid[n] == o.world) ctx->slice[n] = self;
+      else if (cpd::comm_split(ctx->cm, ctx->coord[n], o.rank, &ctx->slice[n], &m)) {
+        fail(ctx, CPD_ERR_NCCL, m);
+        return bail(CPD_ERR_NCCL);
+      }
+      if (grid[n] == 1) ctx->fiber[n] = self;
+      else if (grid[n] == o.world) ctx->fiber[n] = ctx->cm;
+      else if (cpd::comm_split(ctx->cm, rest, ctx->coord[n], &ctx->fiber[n], &m)) {
+        fail(ctx, CPD_ERR_NCCL, m);
+        return bail(CPD_ERR_NCCL);
+      }
+    }
+  }
   const int64_t RR = (int64_t)R * R;
   ctx->A.assign(N, nullptr);
   ctx->Aold.assign(N, nullptr);
@@ -1075,7 +1207,7 @@ cpd_status cp_als_init(cpd_ctx** out, int N, const int64_t* shape, int R, const 
     ITRY(dalloc(ctx, &ctx->Wb[b2], RR));
     if (R <= cpd::kUpdMaxR || R > kCholMaxR) ITRY(dalloc(ctx, &ctx->Gi[b2], RR));
   }
-  ICU(cudaMallocAsync((void**)&ctx->pf_status, sizeof(int) * 2, ctx->st));
+  ICU(palloc(ctx, (void**)&ctx->pf_status, sizeof(int) * 2));
   ICU(cudaMemsetAsync(ctx->pf_status, 0, sizeof(int) * 2, ctx->st));
   {
     // the side stream (Γ factor / inverse, W) must not queue behind the MTTKRP stream's CTAs
@@ -1100,16 +1232,51 @@ cpd_status cp_als_init(cpd_ctx** out, int N, const int64_t* shape, int R, const 
   ITRY(dalloc(ctx, &ctx->st_part, 3 * 64));
   ITRY(dalloc(ctx, &ctx->upd_part, 3 * cpd::kUpdMaxBlocks));
   if (R <= cpd::kUpdMaxR) ITRY(dalloc(ctx, &ctx->upd_gpart, (int64_t)cpd::kUpdMaxBlocks * 2 * RR));
-  ICU(cudaMallocAsync((void**)&ctx->st_counter, sizeof(unsigned int), ctx->st));
+  ICU(palloc(ctx, (void**)&ctx->st_counter, sizeof(unsigned int)));
   ICU(cudaMemsetAsync(ctx->st_counter, 0, sizeof(unsigned int), ctx->st));
   ITRY(dalloc(ctx, &ctx->scal, SC_COUNT));
   ITRY(dalloc(ctx, &ctx->partial, cpd::kNormBlocks));
-  ICU(cudaMallocAsync((void**)&ctx->status, sizeof(int) * CPD_MAX_ORDER, ctx->st));
+  ICU(palloc(ctx, (void**)&ctx->status, sizeof(int) * CPD_MAX_ORDER));
   ICU(cudaMemsetAsync(ctx->status, 0, sizeof(int) * CPD_MAX_ORDER, ctx->st));
   ICU(cudaMemsetAsync(ctx->scal, 0, sizeof(double) * SC_COUNT, ctx->st));
   ICU(cudaMemsetAsync(ctx->dS_all, 0, sizeof(double) * N * RR, ctx->st));
   ICU(cudaMallocHost((void**)&ctx->hscal, sizeof(double) * SC_COUNT));
   ICU(cudaMallocHost((void**)&ctx->hstatus, sizeof(int) * CPD_MAX_ORDER));
+  if (o.fused_rs && o.world > 1) {
+    // fused reduce-scatter epilogue: receive buffers and every rank's slot map
+    ITRY(dalloc(ctx, &ctx->bar_scratch, 1));
+    ICU(cudaMemsetAsync(ctx->bar_scratch, 0, sizeof(double), ctx->st));
+    for (int n = 0; n < N; n++) {
+      cpd::Comm& sl = ctx->slice[n];
+      if (sl.world == 1) continue;
+      if (sl.world > 8) {
+        fail(ctx, CPD_ERR_INVALID_ARG, "fused_rs: at most 8 ranks per slice");
+        return bail(CPD_ERR_INVALID_ARG);
+      }
+      const int64_t chunk = (ctx->loc[n] / sl.world) * R;
+      void* peers[8] = {};
+      std::string m;
+      if (sl.lg) {
+        ITRY(dalloc(ctx, &ctx->rs_recv[n], sl.world * chunk));
+        ICU(cudaStreamSynchronize(ctx->st));
+        if (cpd::comm_exchange_ptr(sl, ctx->rs_recv[n], peers, &m)) {
+          fail(ctx, CPD_ERR_CUDA, m);
+          return bail(CPD_ERR_CUDA);
+        }
+      } else {
+        void* buf = nullptr;
+        if (cpd::nccl_window_peers(sl.nccl, sizeof(double) * sl.world * chunk, sl.world, &buf, peers, &ctx->rs_win[n],
+                                   ctx->st, &m)) {
+          fail(ctx, CPD_ERR_NCCL, m);
+          return bail(CPD_ERR_NCCL);
+        }
+        ctx->rs_recv[n] = static_cast<double*>(buf);
+      }
+      ctx->rs_map[n].nq = sl.world;
+      ctx->rs_map[n].chunk = chunk;
+      for (int q = 0; q < sl.world; q++) ctx->rs_map[n].dst[q] = static_cast<double*>(peers[q]) + sl.rank * chunk;
+    }
+  }
   *out = ctx;  // provisional for cpd_set_factors
   // ||T||^2 once, all-reduced
   {
@@ -1150,12 +1317,13 @@ cpd_status cpd_set_factors(cpd_ctx* ctx, const double* const* A_host) {
   const int64_t RR = (int64_t)R * R;
   for (int n = 0; n < ctx->N; n++) {
     if (!A_host[n]) return fail(ctx, CPD_ERR_INVALID_ARG, "null factor");
-    const double* src = A_host[n] + (n == ctx->N - 1 ? ctx->lo * R : 0);
+    // the block rows of mode n (Alg. 3 lines 4-8); S^(n) = the sum of the blocks' Grams over the fibre
+    const double* src = A_host[n] + ctx->coord[n] * ext(ctx, n) * R;
     CU(cudaMemcpyAsync(ctx->A[n], src, sizeof(double) * ext(ctx, n) * R, cudaMemcpyHostToDevice, ctx->st));
     CU(cpd::launch_gram(ctx->A[n], ctx->A[n], nullptr, ext(ctx, n), R, ctx->S_all + n * RR, nullptr,
                         ctx->ws_gram, 32 * RR, ctx->st));
+    CM(cpd::comm_all_reduce(ctx->fiber[n], ctx->S_all + n * RR, RR, &m_));
   }
-  CM(cpd::comm_all_reduce(ctx->cm, ctx->S_all + (ctx->N - 1) * RR, RR, &m_));
   clear_subtree(ctx);
   ctx->t = 0;
   ctx->sub_is_msdt = false;
@@ -1186,15 +1354,18 @@ cpd_status cpd_set_tensor(cpd_ctx* ctx) {
   return CPD_OK;
 }
 
+// a regular sweep after a PP sweep drops the speculative next-sweep PP streams without waiting
+// for them up front: its first-level TTM (reads T and A only) overlaps them, and the main stream
+// waits for them just before its first factor update (drop_spec in regular_sweep)
 cpd_status msdt_sweep(cpd_ctx* ctx, double* fitness_out) {
   TRY(check_ctx(ctx));
-  UserSync us_(ctx);
+  UserSync us_(ctx, true);
   return regular_sweep(ctx, true, fitness_out);
 }
 
 cpd_status dt_sweep(cpd_ctx* ctx, double* fitness_out) {
   TRY(check_ctx(ctx));
-  UserSync us_(ctx);
+  UserSync us_(ctx, true);
   return regular_sweep(ctx, false, fitness_out);
 }
 
@@ -1309,7 +1480,10 @@ cpd_status pp_approx_sweep(cpd_ctx* ctx, double* fitness_out, int* still_valid) 
       if (i != nx && i != nx - 1) sp[J++] = spec(nx, i, &bytes);
     CU(cudaEventRecord(ctx->ev_pp_a, ctx->st));  // update nx-2 (and everything before) enqueued
     CU(cudaStreamWaitEvent(ctx->st3, ctx->ev_pp_a, 0));
-    CU(cpd::launch_mttv_multi(sp, J, ctx->R, ctx->Mp[nx], M[nx], 0, ctx->ws_mttv3, kMttvWs, ctx->st3));
+    {
+      PhaseScope ps(ctx, PH_MTTV, ctx->st3);
+      CU(cpd::launch_mttv_multi(sp, J, ctx->R, ctx->Mp[nx], M[nx], 0, ctx->ws_mttv3, kMttvWs, ctx->st3));
+    }
     CU(cudaEventRecord(ctx->ev_pp_side[nx], ctx->st3));
     ctx->counters[2] += bytes + 8.0 * 2 * ext(ctx, nx) * ctx->R;
     ctx->counters[3] += 1;
@@ -1325,22 +1499,24 @@ cpd_status pp_approx_sweep(cpd_ctx* ctx, double* fitness_out, int* still_valid) 
     cpd::MttvSpec sp[CPD_MAX_ORDER];
     int J = 0;
     double bytes = 0.0;
+    // the launch that completes M~_loc^(n) stores it into the owners' slots under the fused RS
+    const cpd::OutMap* mp = rs_map_of(ctx, n);
     if (n == 0 || N <= 2) {
       for (int i = 0; i < N; i++)
         if (i != n) sp[J++] = spec(n, i, &bytes);
       PhaseScope ps(ctx, PH_MTTV);
-      CU(cpd::launch_mttv_multi(sp, J, ctx->R, ctx->Mp[n], Mt, 0, ctx->ws_mttv, kMttvWs, ctx->st));
+      CU(cpd::launch_mttv_multi(sp, J, ctx->R, ctx->Mp[n], Mt, 0, ctx->ws_mttv, kMttvWs, ctx->st, mp));
       ctx->counters[2] += 8.0 * 2 * ext(ctx, n) * ctx->R;
     } else {
       sp[J++] = spec(n, n - 1, &bytes);
       CU(cudaStreamWaitEvent(ctx->st, ctx->ev_pp_side[n], 0));
       PhaseScope ps(ctx, PH_MTTV);
-      CU(cpd::launch_mttv_multi(sp, J, ctx->R, nullptr, Mt, 1, ctx->ws_mttv, kMttvWs, ctx->st));
+      CU(cpd::launch_mttv_multi(sp, J, ctx->R, nullptr, Mt, 1, ctx->ws_mttv, kMttvWs, ctx->st, mp));
       ctx->counters[2] += 8.0 * 2 * ext(ctx, n) * ctx->R;
     }
     ctx->counters[2] += bytes;
     ctx->counters[3] += 1;
-    TRY(update_mode(ctx, n, Mt, true));
+    TRY(update_mode(ctx, n, Mt, true, rs_map_of(ctx, n) != nullptr));
   }
   // speculation: the next sweep's mode-1 independent streams need only this sweep's final dA,
   // so they start now and overlap the end of this sweep and the host round trip; this sweep's
@@ -1369,21 +1545,23 @@ cpd_status cpd_pp_condition(cpd_ctx* ctx, int* ok) {
   return CPD_OK;
 }
 
-static cpd_status gather_rows(cpd_ctx* ctx, int n0, const double* src_local, double* host_out) {
-  // src_local: for n0 < N-1 a full-size buffer whose own rows are valid after RS (Mlast)
-  // or fully valid (A); for N-1 the local slab rows.
+// the GLOBAL s_n x R matrix from this rank's block rows (valid on every rank of the slice):
+// all-gathered over the fibre of mode n0 (fibre ranks are ordered by x_n)
+static cpd_status gather_rows(cpd_ctx* ctx, int n0, const double* src_block, double* host_out) {
   const int R = ctx->R;
-  if (n0 == ctx->N - 1) {
-    if (ctx->world == 1) {
-      CU(cudaMemcpyAsync(host_out, src_local, sizeof(double) * ctx->sN_loc * R, cudaMemcpyDeviceToHost, ctx->st));
-    } else {
-      if (!ctx->gather_tmp) TRY(dalloc(ctx, &ctx->gather_tmp, ctx->shape[n0] * R));
-      CM(cpd::comm_all_gather(ctx->cm, src_local, ctx->gather_tmp, ctx->sN_loc * R, &m_));
-      CU(cudaMemcpyAsync(host_out, ctx->gather_tmp, sizeof(double) * ctx->shape[n0] * R, cudaMemcpyDeviceToHost,
-                         ctx->st));
-    }
+  const int64_t e = ext(ctx, n0) * R;
+  cpd::Comm& fb = ctx->fiber[n0];
+  if (fb.world == 1) {
+    CU(cudaMemcpyAsync(host_out, src_block, sizeof(double) * e, cudaMemcpyDeviceToHost, ctx->st));
   } else {
-    CU(cudaMemcpyAsync(host_out, src_local, sizeof(double) * ctx->shape[n0] * R, cudaMemcpyDeviceToHost, ctx->st));
+    if (!ctx->gather_tmp) {
+      int64_t mx = 0;
+      for (int n = 0; n < ctx->N; n++) mx = std::max(mx, ctx->shape[n]);
+      TRY(dalloc(ctx, &ctx->gather_tmp, mx * R));
+    }
+    CM(cpd::comm_all_gather(fb, src_block, ctx->gather_tmp, e, &m_));
+    CU(cudaMemcpyAsync(host_out, ctx->gather_tmp, sizeof(double) * ctx->shape[n0] * R, cudaMemcpyDeviceToHost,
+                       ctx->st));
   }
   CU(cudaStreamSynchronize(ctx->st));
   return CPD_OK;
@@ -1400,23 +1578,21 @@ cpd_status cpd_get_last_mttkrp(cpd_ctx* ctx, int n0, double* host_out) {
   TRY(check_ctx(ctx));
   UserSync us_(ctx);
   if (n0 < 0 || n0 >= ctx->N || !host_out) return fail(ctx, CPD_ERR_INVALID_ARG, "bad mode");
-  if (ctx->Mlast_src[n0]) {
-    const int64_t ro = rows_own(ctx, n0), off = own_off(ctx, n0);
+  const int64_t ro = rows_own(ctx, n0), off = own_off(ctx, n0);
+  if (ctx->Mlast_src[n0])
     CU(cudaMemcpyAsync(ctx->Mlast[n0] + off * ctx->R, ctx->Mlast_src[n0] + off * ctx->R,
                        sizeof(double) * ro * ctx->R, cudaMemcpyDeviceToDevice, ctx->st));
-  }
-  if (n0 < ctx->N - 1 && ctx->world > 1) {
-    int64_t ro = rows_own(ctx, n0);
-    CM(cpd::comm_all_gather(ctx->cm, ctx->Mlast[n0] + own_off(ctx, n0) * ctx->R, ctx->Mlast[n0], ro * ctx->R,
-                            &m_));
-  }
+  // own rows (after the reduce-scatter) -> the block (slice) -> the global matrix (fibre)
+  if (ctx->slice[n0].world > 1)
+    CM(cpd::comm_all_gather(ctx->slice[n0], ctx->Mlast[n0] + off * ctx->R, ctx->Mlast[n0], ro * ctx->R, &m_));
   return gather_rows(ctx, n0, ctx->Mlast[n0], host_out);
 }
 
 cpd_status cpd_get_phase_ms(cpd_ctx* ctx, double out[5]) {
   if (!ctx || !out) return CPD_ERR_INVALID_ARG;
   cudaStreamSynchronize(ctx->st);
-  drain_timers(ctx);
+  cudaStreamSynchronize(ctx->st3);
+  drain_timers(ctx, true);
   for (int i = 0; i < 5; i++) out[i] = ctx->phase_ms[i];
   return CPD_OK;
 }
@@ -1444,7 +1620,8 @@ cpd_status cpd_get_counters(cpd_ctx* ctx, double out[6]) {
 cpd_status cpd_set_profile_level(cpd_ctx* ctx, int level) {
   if (!ctx || level < 0 || level > 2) return CPD_ERR_INVALID_ARG;
   cudaStreamSynchronize(ctx->st);
-  drain_timers(ctx);
+  cudaStreamSynchronize(ctx->st3);
+  drain_timers(ctx, true);
   ctx->opts.profile_phases = level;
   return CPD_OK;
 }
@@ -1452,7 +1629,8 @@ cpd_status cpd_set_profile_level(cpd_ctx* ctx, int level) {
 cpd_status cpd_reset_counters(cpd_ctx* ctx) {
   if (!ctx) return CPD_ERR_INVALID_ARG;
   cudaStreamSynchronize(ctx->st);
-  drain_timers(ctx);
+  cudaStreamSynchronize(ctx->st3);
+  drain_timers(ctx, true);
   for (int i = 0; i < 5; i++) ctx->phase_ms[i] = ctx->counters[i] = 0.0;
   return CPD_OK;
 }
@@ -1472,16 +1650,24 @@ cpd_status cpd_debug_get_pp_operator(cpd_ctx* ctx, int a0, int b0, double* host_
 
 // ---------------- generators and single-kernel entry points ----------------
 
-cpd_status cpd_gen_tensor(double* T_dev, int N, const int64_t* shape, int64_t lo, int64_t hi, int kind,
-                          const double* const* At_host, int Rt, double noise_std, uint64_t seed,
-                          void* stream) {
+cpd_status cpd_gen_tensor_block(double* T_dev, int N, const int64_t* shape, const int64_t* lo, const int64_t* hi,
+                                int kind, const double* const* At_host, int Rt, double noise_std, uint64_t seed,
+                                void* stream) {
   cpd_ctx* ctx = nullptr;
-  if (!T_dev || !shape || N < 1 || N > CPD_MAX_ORDER || lo < 0 || hi <= lo || hi > shape[N - 1])
+  if (!T_dev || !shape || !lo || !hi || N < 1 || N > CPD_MAX_ORDER)
     return fail(ctx, CPD_ERR_INVALID_ARG, "bad generator arguments");
+  cpd::BlockGeo bg{};
+  bg.N = N;
+  for (int n = 0; n < N; n++) {
+    if (lo[n] < 0 || hi[n] <= lo[n] || hi[n] > shape[n]) return fail(ctx, CPD_ERR_INVALID_ARG, "bad block range");
+    bg.shape[n] = shape[n];
+    bg.lo[n] = lo[n];
+    bg.ext[n] = hi[n] - lo[n];
+  }
   cudaStream_t st = (cudaStream_t)stream;
   int64_t Q = 1;
-  for (int n = 0; n < N - 1; n++) Q *= shape[n];
-  const int64_t w = hi - lo;
+  for (int n = 0; n < N - 1; n++) Q *= bg.ext[n];
+  const int64_t w = bg.ext[N - 1];
   auto cuerr = [&](cudaError_t e) {
     g_init_error = cudaGetErrorString(e);
     return CPD_ERR_CUDA;
@@ -1489,22 +1675,24 @@ cpd_status cpd_gen_tensor(double* T_dev, int N, const int64_t* shape, int64_t lo
   cudaError_t e;
   if (kind == 0 && Rt > 0) {
     if (!At_host) return fail(ctx, CPD_ERR_INVALID_ARG, "kind 0 needs factors");
+    // Kruskal part of the block: KRP of the block rows of modes 0..N-2 times A_N[lo:hi]^T
     std::vector<double*> Ad(N - 1, nullptr);
     double *KR = nullptr, *Bt = nullptr;
     for (int n = 0; n < N - 1; n++) {
-      if ((e = cudaMalloc(&Ad[n], sizeof(double) * shape[n] * Rt)) != cudaSuccess) return cuerr(e);
-      if ((e = cudaMemcpy(Ad[n], At_host[n], sizeof(double) * shape[n] * Rt, cudaMemcpyHostToDevice)) != cudaSuccess)
+      if ((e = cudaMalloc(&Ad[n], sizeof(double) * bg.ext[n] * Rt)) != cudaSuccess) return cuerr(e);
+      if ((e = cudaMemcpy(Ad[n], At_host[n] + lo[n] * Rt, sizeof(double) * bg.ext[n] * Rt,
+                          cudaMemcpyHostToDevice)) != cudaSuccess)
         return cuerr(e);
     }
     // B = A_N[lo:hi]^T  (Rt x w) so that T[q, z] = Σ_r KR[q, r] B[r, z]
     std::vector<double> bt((size_t)Rt * w);
     for (int64_t z = 0; z < w; z++)
-      for (int r = 0; r < Rt; r++) bt[(size_t)r * w + z] = At_host[N - 1][(lo + z) * Rt + r];
+      for (int r = 0; r < Rt; r++) bt[(size_t)r * w + z] = At_host[N - 1][(lo[N - 1] + z) * Rt + r];
     if ((e = cudaMalloc(&Bt, sizeof(double) * bt.size())) != cudaSuccess) return cuerr(e);
     if ((e = cudaMemcpy(Bt, bt.data(), sizeof(double) * bt.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
       return cuerr(e);
     if ((e = cudaMalloc(&KR, sizeof(double) * Q * Rt)) != cudaSuccess) return cuerr(e);
-    if ((e = cpd::launch_krp(Ad.data(), shape, N - 1, Rt, KR, st)) != cudaSuccess) return cuerr(e);
+    if ((e = cpd::launch_krp(Ad.data(), bg.ext, N - 1, Rt, KR, st)) != cudaSuccess) return cuerr(e);
     if ((e = cpd::launch_ttm(KR, Q, Rt, 1, Bt, (int)w, T_dev, 0, st)) != cudaSuccess) return cuerr(e);
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuerr(e);
     cudaFree(KR);
@@ -1514,11 +1702,24 @@ cpd_status cpd_gen_tensor(double* T_dev, int N, const int64_t* shape, int64_t lo
     if ((e = cudaMemsetAsync(T_dev, 0, sizeof(double) * Q * w, st)) != cudaSuccess) return cuerr(e);
   }
   if (kind == 1 || noise_std != 0.0) {
-    if ((e = cpd::launch_noise(T_dev, Q, w, shape[N - 1], lo, kind, noise_std, seed, st)) != cudaSuccess)
-      return cuerr(e);
+    if ((e = cpd::launch_noise(T_dev, bg, kind, noise_std, seed, st)) != cudaSuccess) return cuerr(e);
   }
   if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuerr(e);
   return CPD_OK;
+}
+
+cpd_status cpd_gen_tensor(double* T_dev, int N, const int64_t* shape, int64_t lo, int64_t hi, int kind,
+                          const double* const* At_host, int Rt, double noise_std, uint64_t seed,
+                          void* stream) {
+  if (!shape || N < 1 || N > CPD_MAX_ORDER) return fail(nullptr, CPD_ERR_INVALID_ARG, "bad generator arguments");
+  int64_t l[CPD_MAX_ORDER], h[CPD_MAX_ORDER];
+  for (int n = 0; n < N; n++) {
+    l[n] = 0;
+    h[n] = shape[n];
+  }
+  l[N - 1] = lo;
+  h[N - 1] = hi;
+  return cpd_gen_tensor_block(T_dev, N, shape, l, h, kind, At_host, Rt, noise_std, seed, stream);
 }
 
 cpd_status cpd_ttm(const double* T_dev, int64_t pre, int64_t K, int64_t post, const double* A_dev, int R,

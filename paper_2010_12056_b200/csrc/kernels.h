@@ -64,14 +64,29 @@ struct MttvSpec {
   const double* v;
   int64_t pre, K, post;
 };
+// Fused reduce-scatter epilogue (Alg. 3 line 14, Alg. 4 line 9): the final value of
+// output element e (the local partial MTTKRP, read-modify-write of `out` when beta = 1) is
+// stored at dst[e / chunk] + e % chunk instead of out + e -- this rank's slot in the receive
+// buffer of the owner of those rows (a peer's memory over NVLink, or the same device for the
+// local group).  nq == 0: plain output.
+struct OutMap {
+  double* dst[8];
+  int64_t chunk;
+  int nq;
+};
 cudaError_t launch_mttv_multi(const MttvSpec* specs, int J, int R, const double* base, double* out, int beta,
-                              double* ws, int64_t ws_elems, cudaStream_t st);
+                              double* ws, int64_t ws_elems, cudaStream_t st, const OutMap* map = nullptr);
+// dst[e] = Σ_{q < nq} src[q * n + e], q in fixed order (the owner's sum of the received slots)
+cudaError_t launch_slot_sum(const double* src, int nq, int64_t n, double* dst, cudaStream_t st);
 
 // ---- synthetic tensor (synth/__init__.py recipe) ------------------------------------
 // T[q, z] += std*normal(seed, g) (kind 0) or T = uniform(seed, g) (kind 1) with
 // g = q*sN + lo + z the global index, T viewed as [Q, w] (w = hi - lo).
-cudaError_t launch_noise(double* T, int64_t Q, int64_t w, int64_t sN, int64_t lo, int kind,
-                         double stdv, uint64_t seed, cudaStream_t st);
+struct BlockGeo {  // a block of a row-major tensor: global shape, first index and extent per mode
+  int N;
+  int64_t shape[8], lo[8], ext[8];
+};
+cudaError_t launch_noise(double* T, const BlockGeo& b, int kind, double stdv, uint64_t seed, cudaStream_t st);
 // KR[q, r] = Π_{n<N-1} A_n[i_n(q), r]  (Khatri-Rao rows, first mode slowest)
 cudaError_t launch_krp(const double* const* A_dev, const int64_t* shape, int nf, int R,
                        double* KR, cudaStream_t st);
@@ -128,11 +143,13 @@ cudaError_t launch_update_stats(const double* A, const double* base, double* dA,
 // R <= kUpdMaxR.
 constexpr int kUpdMaxR = 128;  // Γ^{-1} + the packed factor fit one CTA's shared memory
 constexpr int kUpdMaxBlocks = 148;
-// part: 3 * kUpdMaxBlocks doubles; gpart: kUpdMaxBlocks * 2 * R * R doubles (per-CTA Gram partials)
+// part: 3 * kUpdMaxBlocks doubles; gpart: kUpdMaxBlocks * 2 * R * R doubles (per-CTA Gram partials).
+// st_src/st_dst (optional): *st_dst = *st_src at kernel start (status hand-over between streams)
 size_t update_fused_smem(int R, bool pp, int RB);
 int update_fused_blocks(int64_t rows);
 cudaError_t launch_update_fused(int R, int64_t rows, const double* Ginv, const double* W, double* M, double* A,
                                 const double* base, double* dA, double* S, double* dS, double* part, double* gpart,
-                                double* o_dA2, double* o_A2, double* o_MA, cudaStream_t st);
+                                double* o_dA2, double* o_A2, double* o_MA, const int* st_src, int* st_dst,
+                                cudaStream_t st);
 
 }  // namespace cpd

@@ -38,9 +38,15 @@ struct MttvJobs {
   int64_t E;  // output elements (pre*C, same for every job)
 };
 
+__device__ __forceinline__ double* map_dst(const OutMap& m, double* out, int64_t e) {
+  if (m.nq == 0) return out + e;
+  const int64_t q = e / m.chunk;
+  return m.dst[q] + (e - q * m.chunk);
+}
+
 template <bool VEC2, bool VV>
 __global__ void __launch_bounds__(MT_THREADS)
-    mttv_kernel(MttvJobs jobs, int R, double* __restrict__ out, int beta, double* __restrict__ ws) {
+    mttv_kernel(MttvJobs jobs, int R, double* __restrict__ out, int beta, double* __restrict__ ws, OutMap om) {
   __shared__ double red[8][MT_COLS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int jj = 0;
@@ -119,8 +125,8 @@ __global__ void __launch_bounds__(MT_THREADS)
 #pragma unroll
       for (int w = 1; w < 8; w++) s += red[w][threadIdx.x];
       if (ws == nullptr) {
-        double* o = out + p * C + c;
-        *o = beta ? *o + s : s;
+        const int64_t e = p * C + c;
+        *map_dst(om, out, e) = beta ? out[e] + s : s;
       } else {
         ws[(jb.slot0 + split) * jobs.E + p * C + c] = s;
       }
@@ -130,11 +136,24 @@ __global__ void __launch_bounds__(MT_THREADS)
 
 // out[e] = (base ? base[e] : beta*out[e]) + Σ_slot ws[slot*n + e]   (slot order fixed)
 __global__ void mttv_reduce_kernel(const double* __restrict__ ws, int slots, int64_t n, const double* __restrict__ base,
-                                   double* __restrict__ out, int beta) {
+                                   double* __restrict__ out, int beta, OutMap om) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     double s = base ? base[e] : (beta ? out[e] : 0.0);
     for (int k = 0; k < slots; k++) s += ws[k * n + e];
-    out[e] = s;
+    *map_dst(om, out, e) = s;
+  }
+}
+
+__global__ void scatter_copy_kernel(const double* __restrict__ src, int64_t n, OutMap om) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    *map_dst(om, nullptr, e) = src[e];
+}
+
+__global__ void slot_sum_kernel(const double* __restrict__ src, int nq, int64_t n, double* __restrict__ dst) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    double s = src[e];
+    for (int q = 1; q < nq; q++) s += src[q * n + e];
+    dst[e] = s;
   }
 }
 
@@ -149,13 +168,21 @@ __device__ __forceinline__ double hash_u(uint64_t key, uint64_t idx, uint64_t la
   return (double)(splitmix64(key ^ (2ull * idx + lane)) >> 11) * 0x1.0p-53;
 }
 
-__global__ void noise_kernel(double* __restrict__ T, int64_t Q, int64_t w, int64_t sN, int64_t lo,
-                             int kind, double stdv, uint64_t key) {
-  const int64_t n = Q * w;
+// T block [lo_0:hi_0, ..., lo_{N-1}:hi_{N-1}] (row-major, local extents b.ext) of a tensor of
+// global shape b.shape: element li gets the hash of its GLOBAL row-major linear index
+__global__ void noise_kernel(double* __restrict__ T, BlockGeo b, int kind, double stdv, uint64_t key) {
+  int64_t n = 1;
+  for (int m = 0; m < b.N; m++) n *= b.ext[m];
   for (int64_t li = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; li < n;
        li += (int64_t)gridDim.x * blockDim.x) {
-    int64_t q = li / w, z = li - q * w;
-    uint64_t gidx = (uint64_t)(q * sN + lo + z);
+    int64_t rem = li, gidx_s = 0, stride = 1;
+    for (int m = b.N - 1; m >= 0; m--) {
+      const int64_t c = rem % b.ext[m];
+      rem /= b.ext[m];
+      gidx_s += (b.lo[m] + c) * stride;
+      stride *= b.shape[m];
+    }
+    const uint64_t gidx = (uint64_t)gidx_s;
     if (kind == 1) {
       T[li] = hash_u(key, gidx, 0);
     } else {
@@ -238,9 +265,20 @@ __global__ void sub_kernel(const double* __restrict__ x, const double* __restric
 
 }  // namespace
 
+cudaError_t launch_slot_sum(const double* src, int nq, int64_t n, double* dst, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  g_launches++;
+  slot_sum_kernel<<<(unsigned)blocks, 256, 0, st>>>(src, nq, n, dst);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_mttv_multi(const MttvSpec* specs, int J, int R, const double* base, double* out, int beta,
-                              double* ws, int64_t ws_elems, cudaStream_t st) {
+                              double* ws, int64_t ws_elems, cudaStream_t st, const OutMap* map) {
   if (J < 1 || J > 8) return cudaErrorInvalidValue;
+  OutMap om{};
+  if (map) om = *map;
   MttvJobs jobs{};
   jobs.J = J;
   jobs.E = specs[0].pre * specs[0].post * R;
@@ -290,29 +328,37 @@ cudaError_t launch_mttv_multi(const MttvSpec* specs, int J, int R, const double*
       one.j[0].slot0 = 0;
       int64_t grid = one.j[0].pre * one.j[0].nchunks;
       g_launches++;
+      const OutMap none{};
       if (vec2 && vv)
-        mttv_kernel<true, true><<<(unsigned)grid, MT_THREADS, 0, st>>>(one, R, out, q > 0 ? 1 : beta, nullptr);
+        mttv_kernel<true, true><<<(unsigned)grid, MT_THREADS, 0, st>>>(one, R, out, q > 0 ? 1 : beta, nullptr, none);
       else if (vec2)
-        mttv_kernel<true, false><<<(unsigned)grid, MT_THREADS, 0, st>>>(one, R, out, q > 0 ? 1 : beta, nullptr);
+        mttv_kernel<true, false><<<(unsigned)grid, MT_THREADS, 0, st>>>(one, R, out, q > 0 ? 1 : beta, nullptr, none);
       else
-        mttv_kernel<false, false><<<(unsigned)grid, MT_THREADS, 0, st>>>(one, R, out, q > 0 ? 1 : beta, nullptr);
+        mttv_kernel<false, false><<<(unsigned)grid, MT_THREADS, 0, st>>>(one, R, out, q > 0 ? 1 : beta, nullptr, none);
+    }
+    if (om.nq > 0) {  // the local result, then scattered to the owners' slots
+      int64_t blocks = (jobs.E + 255) / 256;
+      if (blocks > 148 * 8) blocks = 148 * 8;
+      g_launches++;
+      scatter_copy_kernel<<<(unsigned)blocks, 256, 0, st>>>(out, jobs.E, om);
     }
     return cudaGetLastError();
   }
   if (items > 0x7fffffff) return cudaErrorInvalidConfiguration;
   double* w = direct ? nullptr : ws;
   g_launches++;
+  const OutMap km = direct ? om : OutMap{};
   if (vec2 && vv)
-    mttv_kernel<true, true><<<(unsigned)items, MT_THREADS, 0, st>>>(jobs, R, out, beta, w);
+    mttv_kernel<true, true><<<(unsigned)items, MT_THREADS, 0, st>>>(jobs, R, out, beta, w, km);
   else if (vec2)
-    mttv_kernel<true, false><<<(unsigned)items, MT_THREADS, 0, st>>>(jobs, R, out, beta, w);
+    mttv_kernel<true, false><<<(unsigned)items, MT_THREADS, 0, st>>>(jobs, R, out, beta, w, km);
   else
-    mttv_kernel<false, false><<<(unsigned)items, MT_THREADS, 0, st>>>(jobs, R, out, beta, w);
+    mttv_kernel<false, false><<<(unsigned)items, MT_THREADS, 0, st>>>(jobs, R, out, beta, w, km);
   if (!direct) {
     g_launches++;
     int64_t blocks = (jobs.E + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
-    mttv_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(ws, (int)slots, jobs.E, base, out, beta);
+    mttv_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(ws, (int)slots, jobs.E, base, out, beta, om);
   }
   return cudaGetLastError();
 }
@@ -324,15 +370,14 @@ cudaError_t launch_mttv(const double* X, int64_t pre, int64_t K, int64_t post, i
   return launch_mttv_multi(&sp, 1, R, nullptr, out, beta, ws, ws_elems, st);
 }
 
-cudaError_t launch_noise(double* T, int64_t Q, int64_t w, int64_t sN, int64_t lo, int kind,
-                         double stdv, uint64_t seed, cudaStream_t st) {
+cudaError_t launch_noise(double* T, const BlockGeo& b, int kind, double stdv, uint64_t seed, cudaStream_t st) {
   // key = splitmix64(seed), computed on the host with the same mix
   uint64_t z = seed + 0x9E3779B97F4A7C15ull;
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
   uint64_t key = z ^ (z >> 31);
   g_launches++;
-  noise_kernel<<<148 * 8, 256, 0, st>>>(T, Q, w, sN, lo, kind, stdv, key);
+  noise_kernel<<<148 * 8, 256, 0, st>>>(T, b, kind, stdv, key);
   return cudaGetLastError();
 }
 

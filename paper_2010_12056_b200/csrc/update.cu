@@ -77,7 +77,8 @@ __global__ void __launch_bounds__(UPD_THREADS)
                         double* __restrict__ M, double* __restrict__ A, const double* __restrict__ base,
                         double* __restrict__ dA, double* __restrict__ S, double* __restrict__ dS,
                         double* __restrict__ part, double* __restrict__ gpart, int RB,
-                        double* __restrict__ o_dA2, double* __restrict__ o_A2, double* __restrict__ o_MA) {
+                        double* __restrict__ o_dA2, double* __restrict__ o_A2, double* __restrict__ o_MA,
+                        const int* __restrict__ st_src, int* __restrict__ st_dst) {
   extern __shared__ double sm[];
   double* G = sm;                 // R x R: Γ^{-1}
   double* Ws = sm + R * R;        // R x R (PP only)
@@ -85,6 +86,8 @@ __global__ void __launch_bounds__(UPD_THREADS)
   double* Ds = Xs + RB * R;           // RB x R: their dA
   __shared__ double red[3][UPD_THREADS / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // the side stream's SPD verdict for this Γ^{-1}, handed to the main stream's status slot
+  if (st_dst && blockIdx.x == 0 && tid == 0) *st_dst = *st_src;
   fill_smem(G, Gi, R * R, tid);
   if (W) fill_smem(Ws, W, R * R, tid);
   __syncthreads();
@@ -243,13 +246,14 @@ int update_fused_blocks(int64_t rows) { return (int)std::min<int64_t>(kUpdMaxBlo
 
 cudaError_t launch_update_fused(int R, int64_t rows, const double* Ginv, const double* W, double* M, double* A,
                                 const double* base, double* dA, double* S, double* dS, double* part, double* gpart,
-                                double* o_dA2, double* o_A2, double* o_MA, cudaStream_t st) {
+                                double* o_dA2, double* o_A2, double* o_MA, const int* st_src, int* st_dst,
+                                cudaStream_t st) {
   if (R > kUpdMaxR || rows <= 0) return cudaErrorInvalidValue;
   const int blocks = update_fused_blocks(rows);
   int RB = (int)((rows + blocks - 1) / blocks);
   const size_t smem = update_fused_smem(R, W != nullptr, RB);
   if (smem > 227 * 1024 - 2048) return cudaErrorInvalidValue;
-  void* args[] = {&R, &rows, &Ginv, &W, &M, &A, &base, &dA, &S, &dS, &part, &gpart, &RB, &o_dA2, &o_A2, &o_MA};
+  void* args[] = {&R, &rows, &Ginv, &W, &M, &A, &base, &dA, &S, &dS, &part, &gpart, &RB, &o_dA2, &o_A2, &o_MA, &st_src, &st_dst};
   switch ((R + 31) / 32) {
     case 1: return coop_launch<1>(blocks, smem, args, st);
     case 2: return coop_launch<2>(blocks, smem, args, st);

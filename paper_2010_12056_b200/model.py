@@ -16,14 +16,15 @@ from ._lib import check, dptr, dptr_array, load_library
 class CPDecomposition:
     """One rank's CP-ALS state on the device (a cpd_ctx).
 
-    T: torch CUDA float64 contiguous tensor = this rank's slab [s_1..s_{N-1}, s_N/world]
+    T: torch CUDA float64 contiguous tensor = this rank's block [s_1/I_1, ..., s_N/I_N] of the
+       processor grid (default 1 x .. x 1 x world: the slab [s_1..s_{N-1}, s_N/world])
        (borrowed: keep it alive as long as this object).
     shape: global mode sizes; R: rank; A0: N global s_n x R host arrays.
     """
 
     def __init__(self, T, shape, R, A0, *, device=0, rank=0, world=1, nccl_id=None, stream=None,
                  pp_eps=0.1, reuse_root_in_pp_init=True, profile_phases=False, local_group=None,
-                 ttm_impl=2):
+                 ttm_impl=2, grid=None, fused_rs=False):
         lib = load_library()
         self.N = len(shape)
         self.shape = tuple(int(s) for s in shape)
@@ -43,6 +44,11 @@ class CPDecomposition:
         o.profile_phases = int(profile_phases)
         o.local_group = local_group.value if local_group is not None else None
         o.ttm_impl = int(ttm_impl)
+        o.fused_rs = int(bool(fused_rs))
+        self.grid = tuple(grid) if grid is not None else (1,) * (self.N - 1) + (world,)
+        if grid is not None:
+            for n, g in enumerate(grid):
+                o.grid[n] = int(g)
         A0 = [np.ascontiguousarray(a, dtype=np.float64) for a in A0]
         shp = (C.c_int64 * self.N)(*self.shape)
         ctx = C.c_void_p()
@@ -114,9 +120,7 @@ class CPDecomposition:
         check(self._lib.cpd_reset_counters(self._ctx), self._ctx)
 
     def debug_pp_operator(self, a, b):
-        sb = self.shape[b] // (self.world if b == self.N - 1 else 1)
-        sa = self.shape[a]
-        out = np.empty((sa, sb, self.R))
+        out = np.empty((self.shape[a] // self.grid[a], self.shape[b] // self.grid[b], self.R))
         check(self._lib.cpd_debug_get_pp_operator(self._ctx, a, b, dptr(out)), self._ctx)
         return out
 

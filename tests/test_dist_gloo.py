@@ -117,3 +117,81 @@ def test_gloo_world2_parallel_als_equals_sequential():
         assert abs(got[("f", sweep)] - out["f"]) <= 1e-10
     for a, b in zip(got["A"], A):
         assert np.linalg.norm(a - b) <= 1e-10 * np.linalg.norm(b)
+
+
+# ------------------------- N-D processor grid, world 4 ------------------------------
+
+def _grid_worker(rank, world, port, q, grid):
+    """Alg. 3 on the grid `grid` with real collectives: block-local MTTKRP, reduce-scatter
+    within Proc-Slice(x_n) (the ranks sharing x_n; gloo: all_reduce on the slice group + own rows),
+    solve own rows, Gram of own rows all-reduced over all ranks, all-gather of the block in the slice
+    -- the same exchange pattern libcpd's exchange_mode / update_mode uses."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = synth.custom(3, 8, 3, noise_var=1e-3, seed=22)
+        N = cfg.N
+        procs = O.grid_procs(grid)
+        x = procs[rank]
+        # every rank creates every group (collective), keeps its own slice
+        slices = {}
+        for n in range(N):
+            for c in range(grid[n]):
+                g = dist.new_group([r for r, y in enumerate(procs) if y[n] == c])
+                if x[n] == c:
+                    slices[n] = (g, [r for r, y in enumerate(procs) if y[n] == c])
+        blk = [synth.slab_range(s, k, g) for s, k, g in zip(cfg.shape, x, grid)]
+        Tl = O.make_tensor_block(cfg, blk)
+        A0 = synth.init_factors(cfg)
+        Ab = [a[lo:hi].copy() for a, (lo, hi) in zip(A0, blk)]        # block rows of every factor
+        nt2 = float(_allreduce([O.norm2(Tl)])[0])
+        S = [O.gram(a) for a in A0]
+        for sweep in range(3):
+            for n in range(N):
+                G = O.gamma(S, n)
+                Mloc = O.mttkrp(Tl, Ab, n)                              # line 13
+                g, members = slices[n]
+                P = len(members)
+                t = torch.from_numpy(np.ascontiguousarray(Mloc))
+                dist.all_reduce(t, group=g)                               # line 14 (sum over the slice)
+                b = Mloc.shape[0] // P
+                me = members.index(rank)
+                Mown = t.numpy()[me * b:(me + 1) * b]
+                own = O.solve(G, Mown)                                    # line 15
+                S[n] = _allreduce(O.gram(own))                            # lines 16-17 (all ranks)
+                parts = [torch.empty_like(torch.from_numpy(own)) for _ in range(P)]
+                dist.all_gather(parts, torch.from_numpy(np.ascontiguousarray(own)), group=g)  # line 18
+                Ab[n] = np.concatenate([p.numpy() for p in parts])
+                if n == N - 1:
+                    ma = float(_allreduce([np.sum(Mown * own)])[0])
+                    gs = float(np.sum(G * S[n]))
+            r = np.sqrt(max(nt2 + gs - 2 * ma, 0.0)) / np.sqrt(nt2)
+            if rank == 0:
+                q.put(("f", sweep, 1 - r))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("grid", [(2, 2, 1), (1, 2, 2)])
+def test_gloo_world4_grid_als_equals_sequential(grid):
+    world = 4
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_grid_worker, args=(r, world, port, q, grid)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(180)
+    assert all(p.exitcode == 0 for p in procs)
+    got = {}
+    while not q.empty():
+        item = q.get()
+        got[item[1]] = item[2]
+    cfg = synth.custom(3, 8, 3, noise_var=1e-3, seed=22)
+    T = O.make_tensor(cfg)
+    A = synth.init_factors(cfg)
+    for sweep in range(3):
+        out = O.als_sweep(T, A)
+        A = out["A"]
+        assert abs(got[sweep] - out["f"]) <= 1e-10

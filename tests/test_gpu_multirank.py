@@ -51,16 +51,30 @@ def schedule(m, N):
     return rec
 
 
-def run_group(cpd, cfg, P):
+def block(cpd, cfg, rank, grid):
+    """Rank `rank`'s block of the N-D processor grid (row-major rank order, last mode fastest)."""
+    coord, rem = [0] * cfg.N, rank
+    for n in reversed(range(cfg.N)):
+        coord[n], rem = rem % grid[n], rem // grid[n]
+    lo = [c * (s // g) for c, s, g in zip(coord, cfg.shape, grid)]
+    hi = [l + s // g for l, s, g in zip(lo, cfg.shape, grid)]
+    T = torch.empty([h - l for l, h in zip(lo, hi)], dtype=torch.float64, device="cuda")
+    cpd.cpd_gen_tensor_block(T, cfg.shape, lo, hi, 0, synth.true_factors(cfg), np.sqrt(cfg.noise_var),
+                             cfg.seed_noise)
+    torch.cuda.synchronize()
+    return T
+
+
+def run_group(cpd, cfg, P, grid=None, fused_rs=False):
     group = cpd.cpd_local_group_create(P)
-    Ts = [slab(cpd, cfg, r, P) for r in range(P)]
+    Ts = [slab(cpd, cfg, r, P) if grid is None else block(cpd, cfg, r, grid) for r in range(P)]
     out, errs = [None] * P, []
 
     def worker(r):
         try:
             torch.cuda.set_device(0)
             m = cpd.cp_als_init(Ts[r], cfg.shape, cfg.R, synth.init_factors(cfg), rank=r, world=P,
-                                local_group=group, stream=torch.cuda.Stream())
+                                local_group=group, stream=torch.cuda.Stream(), grid=grid, fused_rs=fused_rs)
             out[r] = schedule(m, cfg.N)
             m.close()
         except Exception as e:  # pragma: no cover - reported below
@@ -108,3 +122,54 @@ def test_local_group_rejects_bad_world(cpd):
         cpd.cp_als_init(T, cfg.shape, cfg.R, synth.init_factors(cfg), rank=0, world=4, local_group=g)
     assert e.value.status == 1
     cpd.cpd_local_group_destroy(g)
+
+
+@pytest.mark.parametrize("cfg,grid", [(synth.custom(3, 16, 5, noise_var=1e-4, seed=34), (2, 2, 2)),
+                                      (synth.custom(3, 24, 4, noise_var=1e-4, seed=35), (2, 1, 3)),
+                                      (synth.custom(4, 8, 3, noise_var=1e-3, seed=36), (2, 2, 1, 2)),
+                                      (synth.custom(3, 16, 6, noise_var=1e-4, seed=37), (1, 4, 2))])
+def test_nd_grid_equals_single_rank_and_oracle(cpd, cfg, grid):
+    """Alg. 3 / Alg. 4 on an N-D processor grid: every rank holds
+    a cubical block, M^(n) reduce-scattered in Proc-Slice(x_n), A^(n) all-gathered there, Grams
+    all-reduced; same schedule as above, P ranks of a local group on one GPU, against P = 1 and the
+    oracle's grid simulation (oracle.par_als_sweep_grid_sim)."""
+    P = int(np.prod(grid))
+    ref = run_group(cpd, cfg, 1)[0]
+    got = run_group(cpd, cfg, P, grid=grid)
+    for r in range(P):
+        for a, b in zip(got[r]["f"], ref["f"]):
+            assert abs(a - b) <= TOL * abs(b)
+        for Ms, Mr in zip(got[r]["M"], ref["M"]):
+            for a, b in zip(Ms, Mr):
+                assert np.linalg.norm(a - b) <= TOL * np.linalg.norm(b)
+        for As, Ar in zip(got[r]["A"], ref["A"]):
+            for a, b in zip(As, Ar):
+                assert np.linalg.norm(a - b) <= TOL * np.linalg.norm(b)
+    T = O.make_tensor(cfg)
+    A = synth.init_factors(cfg)
+    for k in range(3):
+        o = O.par_als_sweep_grid_sim(T, A, grid)
+        A = o["A"]
+        assert abs(got[0]["f"][k] - o["f"]) <= TOL * abs(o["f"])
+
+
+@pytest.mark.parametrize("cfg,grid", [(synth.config(1), None), (synth.custom(3, 16, 5, noise_var=1e-4, seed=34), (2, 2, 2)),
+                                      (synth.custom(4, 8, 3, noise_var=1e-3, seed=36), (2, 2, 1, 2))])
+def test_fused_reduce_scatter_epilogue(cpd, cfg, grid):
+    """opts.fused_rs (Alg. 3 line 14, Alg. 4 line 9): the mTTV / PP-stream launch that
+    completes each rank's partial M^(n) stores the owners' rows straight into their receive slots,
+    then a stream-ordered barrier and a fixed-order slot sum replace the reduce-scatter collective.
+    Same schedule (MSDT, PP, DT sweeps) against the collective path and P = 1."""
+    P = 4 if grid is None else int(np.prod(grid))
+    ref = run_group(cpd, cfg, 1)[0]
+    plain = run_group(cpd, cfg, P, grid=grid)
+    fused = run_group(cpd, cfg, P, grid=grid, fused_rs=True)
+    for r in range(P):
+        for a, b, c in zip(fused[r]["f"], plain[r]["f"], ref["f"]):
+            assert abs(a - c) <= TOL * abs(c) and abs(a - b) <= TOL * abs(b)
+        for Ms, Mr in zip(fused[r]["M"], ref["M"]):
+            for a, b in zip(Ms, Mr):
+                assert np.linalg.norm(a - b) <= TOL * np.linalg.norm(b)
+        for As, Ar in zip(fused[r]["A"], ref["A"]):
+            for a, b in zip(As, Ar):
+                assert np.linalg.norm(a - b) <= TOL * np.linalg.norm(b)

@@ -303,9 +303,14 @@ def test_full_size_sampled_rows(cpd, c, ttm_impl):
     """BASELINE configs at full size: one msdt_sweep; sampled rows of every M^(n) against
     the oracle's slice-by-slice explicit-KRP rows with the GPU's input factors."""
     cfg = synth.config(c)
+    torch.cuda.empty_cache()
     free, total = torch.cuda.mem_get_info()
-    if free < 1.5 * 8 * cfg.numel + 16e9:
-        pytest.skip("not enough device memory")
+    # T (8 B/element) + the int8 engine's digit planes (7 B/element) + two live tree nodes of
+    # root size (8 B x numel/s x R) + workspaces; every ctx returns its memory at close
+    need = 8 * cfg.numel + (7 * cfg.numel if ttm_impl == 1 else 0) + 2 * 8 * cfg.numel // cfg.s * cfg.R + 4e9
+    assert need < total, "config does not fit one B200"
+    if free < need:
+        pytest.skip(f"not enough free device memory ({free / 1e9:.1f} GB < {need / 1e9:.1f} GB)")
     T = dev_tensor(cpd, cfg)
     m = _model(cpd, cfg, T, ttm_impl=ttm_impl)
     A0 = synth.init_factors(cfg)
@@ -495,9 +500,21 @@ def test_large_rank_sweeps(cpd, dims, R, ttm_impl):
         f = sweep()
         out = O.als_sweep(To, A, nt2)
         assert abs(f - out["f"]) <= TOL * abs(out["f"]), (f, out["f"])
+        A1 = [m.get_factor(n) for n in range(3)]
         for n in range(3):
-            assert rel(m.get_factor(n), out["A"][n]) <= 1e-8, (n, rel(m.get_factor(n), out["A"][n]))
-        A = [m.get_factor(n) for n in range(3)]   # state-synchronised
+            # the MTTKRP itself at 1e-10, against the oracle at the GPU's own input factors
+            cur = A1[:n] + A[n:]
+            ref = O.mttkrp(To, cur, n)
+            Mg = m.get_last_mttkrp(n)
+            assert rel(Mg, ref) <= TOL, (n, rel(Mg, ref))
+            # the factor: the oracle's Cholesky solve of the GPU's own M^(n); the forward error of
+            # an SPD solve is ~cond(Γ) u (DESIGN R19), and Γ here (random initial factors, s_n < R
+            # for some modes) has cond up to ~1e6
+            G = O.gamma([O.gram(a) for a in cur], n)
+            tol = max(TOL, 256 * np.finfo(float).eps * np.linalg.cond(G))
+            xr = O.solve(G, Mg)
+            assert rel(A1[n], xr) <= tol, (n, rel(A1[n], xr), tol)
+        A = A1   # state-synchronised
     m.pp_init()
     st = O.pp_init(To, A)
     f, _ = m.pp_approx_sweep()
@@ -532,3 +549,55 @@ def test_last_sweep_status_flags_inconsistent_eq3(cpd, seed, kind):
     m.msdt_sweep()
     assert not m.last_sweep_status()["radicand_negative"]
     m.close()
+
+
+@pytest.mark.parametrize("c,rows_per_mode", [(3, 3), (4, 2)])
+def test_full_size_pp_state_synchronised(cpd, c, rows_per_mode):
+    """C3 and C4 at full size: MSDT sweeps, pp_init, then 3 forced approximated sweeps (Alg. 2
+    lines 11-16, Eqs. 5-8), each state-synchronised: before every sweep the oracle takes
+    the GPU's factors.  Sampled rows of every M~^(n) against the oracle's row-restricted Eq. 5
+    (pp_init_rows / pp_approx_rows: operator rows from T's slices with explicit partial KRPs),
+    factor rows against the oracle's solve of those rows (cond(Γ)-scaled tolerance, R19), and
+    still_valid against the oracle's ε test on the GPU's factors.  A sweep whose Eq. 3 radicand is
+    flagged negative (R18) is checked the same way (M~ and factors, not the clamped f)."""
+    cfg = synth.config(c)
+    torch.cuda.empty_cache()
+    free, total = torch.cuda.mem_get_info()
+    need = 15 * cfg.numel + 6 * 8 * cfg.numel // cfg.s * cfg.R + 4e9
+    if free < need:
+        pytest.skip(f"not enough free device memory ({free / 1e9:.1f} GB)")
+    eps = 0.2 if c == 4 else 0.1
+    T = dev_tensor(cpd, cfg)
+    m = _model(cpd, cfg, T, pp_eps=eps)
+    for _ in range(3):
+        m.msdt_sweep()
+    Ap = [m.get_factor(n) for n in range(cfg.N)]
+    m.pp_init()
+    rng = np.random.default_rng(100 + c)
+    rows = [np.sort(rng.choice(cfg.s, rows_per_mode, replace=False)) for _ in range(cfg.N)]
+    cache = {}
+    st_rows = [O.pp_init_rows(cfg, Ap, n, rows[n], cache) for n in range(cfg.N)]
+    A = Ap
+    for sweep in range(3):
+        f, valid = m.pp_approx_sweep()
+        flagged = m.last_sweep_status()["radicand_negative"]
+        A1 = [m.get_factor(n) for n in range(cfg.N)]
+        for n in range(cfg.N):
+            cur = A1[:n] + A[n:]
+            ref = O.pp_approx_rows(st_rows[n], cur, n, rows[n])
+            got = m.get_last_mttkrp(n)[rows[n]]
+            assert rel(got, ref) <= TOL, (sweep, n, rel(got, ref))
+            G = O.gamma([O.gram(a) for a in cur], n)
+            tol = max(TOL, 256 * np.finfo(float).eps * np.linalg.cond(G))
+            xr = O.solve(G, got)   # the oracle's solve of the GPU's M~ rows (R19)
+            assert rel(A1[n][rows[n]], xr) <= tol, (sweep, n, rel(A1[n][rows[n]], xr), tol)
+        dA = [a - p for a, p in zip(A1, Ap)]
+        ratios = [np.linalg.norm(d) / np.linalg.norm(a) for d, a in zip(dA, A1)]
+        if all(abs(r - eps) > 1e-9 * eps for r in ratios):   # not at the ε boundary (Q17)
+            assert valid == O.pp_condition(dA, A1, eps)
+        if flagged:
+            assert f == 1.0
+        A = A1
+    m.close()
+    del T
+    torch.cuda.empty_cache()

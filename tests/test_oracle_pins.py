@@ -434,3 +434,59 @@ def test_parallel_sim_equals_sequential(P):
     for a, b in zip(s1["M"], s2["M"]):
         assert np.linalg.norm(a - b) <= 1e-10 * np.linalg.norm(a)
     del T, A
+
+
+@pytest.mark.parametrize("N", [3, 4, 5])
+def test_pp_rows_equal_full_operators(N):
+    """pp_init_rows / pp_approx_rows (row-restricted Eq. 4-8 for full-size checks) equal the rows
+    of the full oracle.pp_init / pp_approx_sweep operators and M~ (mode by mode of one sweep)."""
+    cfg = synth.custom(N, 5 if N > 3 else 7, 3, noise_var=1e-2, seed=20 + N)
+    T = O.make_tensor(cfg)
+    Ap = [rnd((cfg.s, 3), 900 + i) for i in range(N)]
+    st = O.pp_init(T, Ap)
+    A = [a + 0.1 * rnd(a.shape, 950 + i) for i, a in enumerate(Ap)]
+    out = O.pp_approx_sweep(st, A, O.norm2(T))
+    rows = [1, 3]
+    cache = {}
+    for n in range(N):
+        sr = O.pp_init_rows(cfg, Ap, n, rows, cache)
+        for (a, b), op in sr.ops.items():
+            full = st.ops[(a, b)]
+            ref = full[rows] if a == n else full[:, rows]
+            assert np.abs(op - ref).max() <= 1e-12 * np.abs(full).max()
+        assert np.abs(sr.Mp[n] - st.Mp[n][rows]).max() <= 1e-12 * np.abs(st.Mp[n]).max()
+        cur = out["A"][:n] + A[n:]
+        got = O.pp_approx_rows(sr, cur, n, rows)
+        assert np.abs(got - out["M"][n][rows]).max() <= 1e-12 * np.abs(out["M"][n]).max()
+
+
+@pytest.mark.parametrize("grid", [(2, 2, 2), (1, 1, 4), (1, 1, 2), (2, 1, 3), (4, 2, 1)])
+def test_grid_sim_equals_sequential(grid):
+    """Alg. 3 / Alg. 4 on an N-D processor grid equal the sequential sweep
+    up to reduction order; (1, 1, P) is the 1-D grid of par_als_sweep_sim."""
+    T = rnd((8, 6, 12), 14)
+    A = [rnd((s, 3), 710 + i) for i, s in enumerate(T.shape)]
+    seq = O.als_sweep(T, A)
+    par = O.par_als_sweep_grid_sim(T, A, grid)
+    for a, b in zip(seq["A"], par["A"]):
+        assert np.linalg.norm(a - b) <= 1e-10 * np.linalg.norm(a)
+    assert abs(seq["f"] - par["f"]) <= 1e-10
+    if grid[0] == grid[1] == 1 and all(d % grid[2] == 0 for d in T.shape):
+        p1 = O.par_als_sweep_sim(T, A, grid[2])
+        assert abs(p1["f"] - par["f"]) <= 1e-12
+    st = O.pp_init(T, A)
+    A2 = [a + 0.05 * rnd(a.shape, 810 + i) for i, a in enumerate(A)]
+    s1 = O.pp_approx_sweep(st, A2, O.norm2(T))
+    s2 = O.par_pp_approx_sweep_grid_sim(T, st, A2, grid, O.norm2(T))
+    for a, b in zip(s1["M"], s2["M"]):
+        assert np.linalg.norm(a - b) <= 1e-10 * np.linalg.norm(a)
+
+
+def test_grid_sim_order4():
+    T = rnd((4, 6, 4, 6), 15)
+    A = [rnd((s, 2), 720 + i) for i, s in enumerate(T.shape)]
+    seq = O.als_sweep(T, A)
+    par = O.par_als_sweep_grid_sim(T, A, (2, 3, 1, 2))
+    assert abs(seq["f"] - par["f"]) <= 1e-10
+    for a, b in zip(seq["A"], par["A"]):
+        assert np.linalg.norm(a - b) <= 1e-10 * np.linalg.norm(a)
