@@ -387,6 +387,7 @@ def main():
     parts = np.array([[a.elapsed_time(b) for a, b in zip(r[:-1], r[1:])] for r in recs])  # steps x 4
     ph = m.phase_ms()
     ctr = m.counters()
+    fill = m.filler_counters()
     launches = int(ctr["kernel_launches"] - launches0)
     part_means = parts.mean(axis=0)
     vals = np.array([total_ms, part_means[0] / (N - 1), part_means[1], part_means[2] / (N - 1), part_means[3]])
@@ -476,7 +477,11 @@ def main():
                                 "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
                                 "frac": (st_gbs / peaks["hbm_gbs"]) if st_gbs and peaks.get("hbm_gbs") else None,
                                 "traffic": ncu_traffic("mttv"), "bytes_per_launch": st_launch_bytes,
-                                "avg_launch_ms": st_ms, "launches": int(ctr["stream_launches"])},
+                                "avg_launch_ms": st_ms, "launches": int(ctr["stream_launches"]),
+                                "scope": "main-stream launches (timed); the PP filler-stream launches overlap "
+                                         "them and are ledgered separately (pp_filler_streams)"},
+            "pp_filler_streams": {"bytes_per_step": fill["bytes"] / args.steps,
+                                  "launches_per_step": fill["launches"] / args.steps},
             "gpu_launches": launches, "clocks": clk.summary(wall0, wall1), "e2e": e2e, "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

@@ -190,6 +190,12 @@ cpd_status cpd_get_phase_ms(cpd_ctx* ctx, double out[5]);
  * out[5]=kernels launched by libcpd.so in this process (all kernels, monotone; not reset). */
 cpd_status cpd_get_counters(cpd_ctx* ctx, double out[6]);
 
+/* Ledger of the PP operator streams (Eq. 6) issued on the low-priority filler stream (the ones whose
+ * dA is already final, and the next sweep's speculative ones): out[0] = bytes (8*(elements read +
+ * written)), out[1] = launches.  These overlap the main stream and are NOT in cpd_get_counters'
+ * out[2..3], which (with the mTTV timer of cpd_get_phase_ms) cover the main-stream launches only. */
+cpd_status cpd_get_filler_counters(cpd_ctx* ctx, double out[2]);
+
 /* Change the timer level of opts.profile_phases (0, 1, 2) between calls. */
 cpd_status cpd_set_profile_level(cpd_ctx* ctx, int level);
 

@@ -109,6 +109,8 @@ struct cpd_ctx {
   // (pp_spec); any call other than pp_approx_sweep first waits for that work and drops it
   int mt_par = 0;
   bool pp_spec = false;
+  bool pp_spec0 = false;  // the next sweep's mode-0 M~ (M_p + all U^(0,i)) is also speculated
+  bool pp_fresh = false;  // no approximated sweep since pp_init: dA = 0 exactly (Alg. 2 line 7)
   std::vector<double*> Mlast_src;  // non-null: the last M of mode n lives there (PP: Mt[n])
   double* S_all = nullptr;   // N x R x R
   double* dS_all = nullptr;  // N x R x R
@@ -158,6 +160,9 @@ struct cpd_ctx {
   std::string err;
   double phase_ms[5] = {0};
   double counters[5] = {0};
+  // PP operator streams on the low-priority filler stream (overlapped with the main stream, so not
+  // timed as launches of their own): bytes, launches (cpd_get_filler_counters)
+  double filler[2] = {0};
   std::vector<PhaseRec> pending;
   std::multimap<size_t, void*> node_cache;         // free device blocks by exact size
   std::unordered_map<void*, size_t> node_bytes;    // size of every block from dalloc
@@ -717,9 +722,10 @@ void free_pp(cpd_ctx* c) {
 // the speculative next-sweep PP streams (filler stream st3) read the operators, M_p and dA and
 // write the spare M~ set: the main stream waits for them before it writes any of those
 void drop_spec(cpd_ctx* c) {
-  if (c->pp_spec) {
-    cudaStreamWaitEvent(c->st, c->ev_pp_side[1], 0);
+  if (c->pp_spec || c->pp_spec0) {
+    cudaStreamWaitEvent(c->st, c->ev_pp_side[1], 0);  // recorded after every speculative launch on st3
     c->pp_spec = false;
+    c->pp_spec0 = false;
   }
 }
 
@@ -1443,6 +1449,7 @@ cpd_status pp_init(cpd_ctx* ctx) {
   drain_timers(ctx);
   ctx->pp_valid = true;
   ctx->pp_regime = true;
+  ctx->pp_fresh = true;
   for (int n = 0; n < N; n++) ctx->dA2[n] = 0.0;
   ctx->have_dA = true;
   return CPD_OK;
@@ -1472,7 +1479,19 @@ cpd_status pp_approx_sweep(cpd_ctx* ctx, double* fitness_out, int* still_valid) 
   double* const* Mcur = ctx->mt_par ? ctx->Mt2.data() : ctx->Mt.data();
   double* const* Mnxt = ctx->mt_par ? ctx->Mt.data() : ctx->Mt2.data();
   // the independent streams of mode nx (all i != nx, nx-1) on the filler stream into M[nx]
+  // first sweep after pp_init: dA = 0 for every mode not yet updated in this sweep (Alg. 2 line 7), so
+  // U^(n,i) = 0 exactly (Eq. 6) for those i and M~ starts as M_p: mode 0 entirely, mode 1's filler part
+  bool fresh = ctx->pp_fresh;  // cleared after the mode loop: the speculation for the NEXT sweep sees dA != 0
+  ctx->pp_fresh = false;
   auto side = [&](int nx, double* const* M) -> cpd_status {
+    if (fresh && nx == 1) {
+      CU(cudaEventRecord(ctx->ev_pp_a, ctx->st));
+      CU(cudaStreamWaitEvent(ctx->st3, ctx->ev_pp_a, 0));
+      CU(cudaMemcpyAsync(M[nx], ctx->Mp[nx], sizeof(double) * ext(ctx, nx) * ctx->R, cudaMemcpyDeviceToDevice,
+                         ctx->st3));
+      CU(cudaEventRecord(ctx->ev_pp_side[nx], ctx->st3));
+      return CPD_OK;
+    }
     cpd::MttvSpec sp[CPD_MAX_ORDER];
     int J = 0;
     double bytes = 0.0;
@@ -1480,20 +1499,33 @@ cpd_status pp_approx_sweep(cpd_ctx* ctx, double* fitness_out, int* still_valid) 
       if (i != nx && i != nx - 1) sp[J++] = spec(nx, i, &bytes);
     CU(cudaEventRecord(ctx->ev_pp_a, ctx->st));  // update nx-2 (and everything before) enqueued
     CU(cudaStreamWaitEvent(ctx->st3, ctx->ev_pp_a, 0));
-    {
-      PhaseScope ps(ctx, PH_MTTV, ctx->st3);
-      CU(cpd::launch_mttv_multi(sp, J, ctx->R, ctx->Mp[nx], M[nx], 0, ctx->ws_mttv3, kMttvWs, ctx->st3));
-    }
+    CU(cpd::launch_mttv_multi(sp, J, ctx->R, ctx->Mp[nx], M[nx], 0, ctx->ws_mttv3, kMttvWs, ctx->st3));
     CU(cudaEventRecord(ctx->ev_pp_side[nx], ctx->st3));
-    ctx->counters[2] += bytes + 8.0 * 2 * ext(ctx, nx) * ctx->R;
-    ctx->counters[3] += 1;
+    ctx->filler[0] += bytes + 8.0 * 2 * ext(ctx, nx) * ctx->R;
+    ctx->filler[1] += 1;
     return CPD_OK;
   };
+  static const bool no_spec = getenv("CPD_NO_PP_SPEC") != nullptr;
+  static const bool no_spec0 = getenv("CPD_NO_PP_SPEC0") != nullptr;
+  const bool spec0 = N > 2 && !no_spec && !no_spec0 && !rs_map_of(ctx, 0);
   for (int n = 0; n < N; n++) {
     const int nx = n + 1;
     if (nx < N && N > 2) {
       if (nx == 1 && ctx->pp_spec) ctx->pp_spec = false;  // started at the end of the last sweep
       else TRY(side(nx, Mcur));
+    }
+    if (n == N - 1 && spec0) {
+      // the next sweep's M~^(0) without its last term: M_p^(0) + Σ_{i<N-1} U^(0,i) (those dA are final
+      // once update N-2 is done), on the filler stream while mode N-1 streams
+      cpd::MttvSpec sp[CPD_MAX_ORDER];
+      int J = 0;
+      double bytes = 0.0;
+      for (int i = 1; i < N - 1; i++) sp[J++] = spec(0, i, &bytes);
+      CU(cudaEventRecord(ctx->ev_pp_a, ctx->st));
+      CU(cudaStreamWaitEvent(ctx->st3, ctx->ev_pp_a, 0));
+      CU(cpd::launch_mttv_multi(sp, J, ctx->R, ctx->Mp[0], Mnxt[0], 0, ctx->ws_mttv3, kMttvWs, ctx->st3));
+      ctx->filler[0] += bytes + 8.0 * 2 * ext(ctx, 0) * ctx->R;
+      ctx->filler[1] += 1;
     }
     double* Mt = Mcur[n];
     cpd::MttvSpec sp[CPD_MAX_ORDER];
@@ -1501,7 +1533,13 @@ cpd_status pp_approx_sweep(cpd_ctx* ctx, double* fitness_out, int* still_valid) 
     double bytes = 0.0;
     // the launch that completes M~_loc^(n) stores it into the owners' slots under the fused RS
     const cpd::OutMap* mp = rs_map_of(ctx, n);
-    if (n == 0 || N <= 2) {
+    if (n == 0 && ctx->pp_spec0) {
+      // M~^(0) was completed on the filler stream at the end of the last sweep (all its dA final)
+      CU(cudaStreamWaitEvent(ctx->st, ctx->ev_pp_side[0], 0));
+      ctx->pp_spec0 = false;
+    } else if (n == 0 && fresh && !mp) {
+      CU(cudaMemcpyAsync(Mt, ctx->Mp[0], sizeof(double) * ext(ctx, 0) * ctx->R, cudaMemcpyDeviceToDevice, ctx->st));
+    } else if (n == 0 || N <= 2) {
       for (int i = 0; i < N; i++)
         if (i != n) sp[J++] = spec(n, i, &bytes);
       PhaseScope ps(ctx, PH_MTTV);
@@ -1521,8 +1559,23 @@ cpd_status pp_approx_sweep(cpd_ctx* ctx, double* fitness_out, int* still_valid) 
   // speculation: the next sweep's mode-1 independent streams need only this sweep's final dA,
   // so they start now and overlap the end of this sweep and the host round trip; this sweep's
   // M~ (readable through cpd_get_last_mttkrp) stays intact in the other buffer set
-  static const bool no_spec = getenv("CPD_NO_PP_SPEC") != nullptr;
+  fresh = false;
+  // Mode 0 of the next sweep needs only this sweep's final dA as well: its last term U^(0,N-1) completes
+  // the M~^(0) started during mode N-1, first on the filler stream, so the next sweep starts with its
+  // first update (not with the fused reduce-scatter, whose slots must be written by the consuming sweep)
   if (N > 2 && !no_spec) {
+    if (spec0) {
+      cpd::MttvSpec sp[1];
+      double bytes = 0.0;
+      sp[0] = spec(0, N - 1, &bytes);
+      CU(cudaEventRecord(ctx->ev_pp_a, ctx->st));
+      CU(cudaStreamWaitEvent(ctx->st3, ctx->ev_pp_a, 0));
+      CU(cpd::launch_mttv_multi(sp, 1, ctx->R, nullptr, Mnxt[0], 1, ctx->ws_mttv3, kMttvWs, ctx->st3));
+      CU(cudaEventRecord(ctx->ev_pp_side[0], ctx->st3));
+      ctx->filler[0] += bytes + 8.0 * 2 * ext(ctx, 0) * ctx->R;
+      ctx->filler[1] += 1;
+      ctx->pp_spec0 = true;
+    }
     TRY(side(1, Mnxt));
     ctx->pp_spec = true;
   }
@@ -1617,6 +1670,13 @@ cpd_status cpd_get_counters(cpd_ctx* ctx, double out[6]) {
   return CPD_OK;
 }
 
+cpd_status cpd_get_filler_counters(cpd_ctx* ctx, double out[2]) {
+  if (!ctx || !out) return CPD_ERR_INVALID_ARG;
+  out[0] = ctx->filler[0];
+  out[1] = ctx->filler[1];
+  return CPD_OK;
+}
+
 cpd_status cpd_set_profile_level(cpd_ctx* ctx, int level) {
   if (!ctx || level < 0 || level > 2) return CPD_ERR_INVALID_ARG;
   cudaStreamSynchronize(ctx->st);
@@ -1632,6 +1692,7 @@ cpd_status cpd_reset_counters(cpd_ctx* ctx) {
   cudaStreamSynchronize(ctx->st3);
   drain_timers(ctx, true);
   for (int i = 0; i < 5; i++) ctx->phase_ms[i] = ctx->counters[i] = 0.0;
+  ctx->filler[0] = ctx->filler[1] = 0.0;
   return CPD_OK;
 }
 

@@ -11,6 +11,8 @@
 // warp load is a contiguous 512-byte row segment (double2 per lane).  A CTA owns one
 // p and 64 columns; its 8 warps split the K rows (fixed interleave) and reduce through
 // shared memory in a fixed order (deterministic, no atomics).
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace cpd {
@@ -300,7 +302,8 @@ cudaError_t launch_mttv_multi(const MttvSpec* specs, int J, int R, const double*
     // split K so the whole grid is >= ~8 waves of 4 resident CTAs per SM (tail <= 1/8 wave)
     int64_t ks = (148 * 4 * 8 / J + items0 - 1) / items0;
     if (ks > jb.K / 64) ks = jb.K / 64;
-    if (ks > 16) ks = 16;
+    static const int ks_max = getenv("CPD_MTTV_MAXKS") ? atoi(getenv("CPD_MTTV_MAXKS")) : 16;  // experiment switch
+    if (ks > ks_max) ks = ks_max;
     if (ks < 1) ks = 1;
     jb.ks = (int)ks;
     jb.rps = (jb.K + ks - 1) / ks;

@@ -704,9 +704,10 @@ __device__ __forceinline__ uint64_t sdesc_sw(uint32_t addr, uint32_t lbo, uint32
 }
 
 // DRAIN epilogue of one warp: rows r (TMEM lane quarter base tq), columns c_lo .. c_lo + CQ.
-// Per tile: the 7 diagonals -> exact int64 partial sums in registers (tcgen05.ld, two diagonals
-// per wait), release the accumulator (tempty), then the FP64 recombination and the global stores
-// overlap the next tile's MMAs.
+// Per tile and 8-column chunk: the 7 diagonals in one batch of tcgen05.ld (one wait per chunk: the
+// TMEM load latency is paid CQ/8 times per tile, not once per diagonal pair), exact int64 partial
+// sums, the FP64 value; then release the accumulator (tempty), and the global stores overlap the
+// next tile's MMAs.
 template <int L, int Rp, int CQ>
 __device__ __forceinline__ void epilogue_drain(const Geo& g, uint32_t tq, int c_lo, int r, int64_t my_tiles,
                                                double* __restrict__ out, int beta, const double* colscale,
@@ -729,34 +730,29 @@ __device__ __forceinline__ void epilogue_drain(const Geo& g, uint32_t tq, int c_
     const int n0 = nt * g.Rn;
     mbar_wait_sleep(tfull0, (uint32_t)tt & 1);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    long long l0[CQ], l1[CQ];  // diagonals 0-2; diagonals 3-6 (|l1| < 2^56)
+    double v[NCH][8];
     if (active) {
 #pragma unroll
-      for (int d0 = 0; d0 < kND; d0 += 2) {
-        uint32_t D[2][CQ];
+      for (int ch = 0; ch < NCH; ch++) {
+        uint32_t D[kND][8];
 #pragma unroll
-        for (int dd = 0; dd < 2; dd++)
-#pragma unroll
-          for (int ch = 0; ch < NCH; ch++)
-            if (d0 + dd < kND)
-              asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                           : "=r"(D[dd][8 * ch]), "=r"(D[dd][8 * ch + 1]), "=r"(D[dd][8 * ch + 2]),
-                             "=r"(D[dd][8 * ch + 3]), "=r"(D[dd][8 * ch + 4]), "=r"(D[dd][8 * ch + 5]),
-                             "=r"(D[dd][8 * ch + 6]), "=r"(D[dd][8 * ch + 7])
-                           : "r"(tq + (d0 + dd) * Rp + c_lo + 8 * ch));
+        for (int d = 0; d < kND; d++)
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                       : "=r"(D[d][0]), "=r"(D[d][1]), "=r"(D[d][2]), "=r"(D[d][3]), "=r"(D[d][4]), "=r"(D[d][5]),
+                         "=r"(D[d][6]), "=r"(D[d][7])
+                       : "r"(tq + d * Rp + c_lo + 8 * ch));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const int c0 = c_lo + 8 * ch;
+        const int cmax = max(1, min(8, min(g.Rn - c0, g.ncols - n0 - c0)));
 #pragma unroll
-        for (int dd = 0; dd < 2; dd++) {
-          const int d = d0 + dd;
-          if (d >= kND) break;
-#pragma unroll
-          for (int j = 0; j < CQ; j++) {
-            const long long v = (long long)(int)D[dd][j];
-            if (d == 0) l0[j] = v;
-            else if (d < 3) l0[j] += v << (8 * d);
-            else if (d == 3) l1[j] = v;
-            else l1[j] += v << (8 * (d - 3));
-          }
+        for (int j = 0; j < 8; j++) {
+          // Σ_d D_d 256^d: exact int64 partial sums of diagonals 0-2 and 3-6 (|l1| < 2^56), one rounding
+          // of l1, then the FP64 value (the same arithmetic as the ping-pong epilogue)
+          const long long l0 = (long long)(int)D[0][j] + ((long long)(int)D[1][j] << 8) +
+                               ((long long)(int)D[2][j] << 16);
+          const long long l1 = (long long)(int)D[3][j] + ((long long)(int)D[4][j] << 8) +
+                               ((long long)(int)D[5][j] << 16) + ((long long)(int)D[6][j] << 24);
+          v[ch][j] = fma((double)l1, 16777216.0 /* 2^24 */, (double)l0) * colscale[n0 + c0 + min(j, cmax - 1)];
         }
       }
     }
@@ -768,28 +764,21 @@ __device__ __forceinline__ void epilogue_drain(const Geo& g, uint32_t tq, int c_
       const int c0 = c_lo + 8 * ch;
       const int cmax = min(8, min(g.Rn - c0, g.ncols - n0 - c0));
       if (!row_ok || cmax <= 0) continue;
-      double v[8];
-#pragma unroll
-      for (int j = 0; j < 8; j++) {
-        const int jj = 8 * ch + j;
-        // (double)l1 rounds once: the same value as fma(D6, 2^48, l1_{3-5} 2^24) in the ping-pong path
-        v[j] = fma((double)l1[jj], 16777216.0 /* 2^24 */, (double)l0[jj]) * colscale[n0 + c0 + min(j, cmax - 1)];
-      }
       double* orow = out + i * g.ncols + n0 + c0;
       const uintptr_t al = reinterpret_cast<uintptr_t>(orow) & 31;
       if (cmax == 8 && !beta && al == 0) {
-        asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(orow), "d"(v[0]), "d"(v[1]), "d"(v[2]),
-                     "d"(v[3]) : "memory");
-        asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(orow + 4), "d"(v[4]), "d"(v[5]), "d"(v[6]),
-                     "d"(v[7]) : "memory");
+        asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(orow), "d"(v[ch][0]), "d"(v[ch][1]),
+                     "d"(v[ch][2]), "d"(v[ch][3]) : "memory");
+        asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(orow + 4), "d"(v[ch][4]), "d"(v[ch][5]),
+                     "d"(v[ch][6]), "d"(v[ch][7]) : "memory");
       } else if (cmax == 8 && !beta && (al & 15) == 0) {
 #pragma unroll
         for (int j = 0; j < 8; j += 2)
-          asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(orow + j), "d"(v[j]), "d"(v[j + 1]) : "memory");
+          asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(orow + j), "d"(v[ch][j]), "d"(v[ch][j + 1]) : "memory");
       } else {
 #pragma unroll
         for (int j = 0; j < 8; j++)
-          if (j < cmax) orow[j] = beta ? orow[j] + v[j] : v[j];
+          if (j < cmax) orow[j] = beta ? orow[j] + v[ch][j] : v[ch][j];
       }
     }
   }
@@ -844,7 +833,6 @@ __global__ void __launch_bounds__(kThreadsD, 1)
   const uint32_t tmem = *tslot;
   const int64_t my_tiles = tiles_of_cta(g);
   const uint16_t cmask = (uint16_t)((1u << g.cl) - 1);
-  const bool a_issuer = (blockIdx.x % g.cl) == 0;  // the cluster's rank 0 loads (multicasts) A
 
   if (warp == 0) {
     // ===================== TMA producer =====================
@@ -882,8 +870,9 @@ __global__ void __launch_bounds__(kThreadsD, 1)
           mbar_arrive_expect_tx(bar, ((dbg & 8) ? 0 : kAStage) + ((dbg & 4) ? 0 : Bbytes));
           if (dbg & 8) {  // profiling: no A loads
           } else if (g.cl > 1) {
-            // A box multicast to every CTA of the cluster (same smem offset, each CTA's full[s])
-            if (a_issuer) {
+            // A box multicast to every CTA of the cluster (same smem offset, each CTA's full[s]) by the
+            // cluster's rank 0 (rotating the issuer with the K step measured slower: C3 loads 4.2 -> 5.1 ms)
+            if (blockIdx.x % g.cl == 0) {
               if constexpr (L == D_KC) {
                 asm volatile(
                     "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster "

@@ -15,6 +15,8 @@
 //   statistics partials in CTA order.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace cpd {
@@ -242,7 +244,13 @@ size_t update_fused_smem(int R, bool pp, int RB) {
   return sizeof(double) * ((size_t)R * R + (pp ? (size_t)R * R : 0) + 2 * (size_t)RB * R);
 }
 
-int update_fused_blocks(int64_t rows) { return (int)std::min<int64_t>(kUpdMaxBlocks, (rows + 7) / 8); }
+int update_fused_blocks(int64_t rows) {
+  // experiment switch CPD_UPD_BLOCKS: cap on the cooperative grid (fewer CTAs: less Γ^-1 / W staging
+  // and fewer Gram partials, and fewer SMs to wait for while filler-stream kernels occupy the GPU)
+  static const int cap = getenv("CPD_UPD_BLOCKS") ? std::max(1, std::min(kUpdMaxBlocks, atoi(getenv("CPD_UPD_BLOCKS"))))
+                                                  : kUpdMaxBlocks;
+  return (int)std::min<int64_t>(cap, (rows + 7) / 8);
+}
 
 cudaError_t launch_update_fused(int R, int64_t rows, const double* Ginv, const double* W, double* M, double* A,
                                 const double* base, double* dA, double* S, double* dS, double* part, double* gpart,

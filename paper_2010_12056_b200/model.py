@@ -113,6 +113,12 @@ class CPDecomposition:
                          "kernel_launches"],
                         out.tolist()))
 
+    def filler_counters(self):
+        """cpd_get_filler_counters: PP operator streams on the filler stream (bytes, launches)."""
+        out = np.zeros(2)
+        check(self._lib.cpd_get_filler_counters(self._ctx, dptr(out)), self._ctx)
+        return {"bytes": float(out[0]), "launches": int(out[1])}
+
     def set_profile_level(self, level):
         check(self._lib.cpd_set_profile_level(self._ctx, int(level)), self._ctx)
 

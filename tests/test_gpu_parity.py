@@ -601,3 +601,32 @@ def test_full_size_pp_state_synchronised(cpd, c, rows_per_mode):
     m.close()
     del T
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("N,s,R", [(3, 48, 6), (4, 12, 4), (5, 8, 3)])
+def test_pp_back_to_back_speculation(cpd, N, s, R):
+    """Approximated sweeps called back to back with no other call in between, so every speculative
+    filler-stream launch (the next sweep's mode-1 streams and its mode-0 M~, started during and at
+    the end of a sweep) is consumed: the fitness trace and the final factors against the oracle's
+    pp_approx_sweep chain (Eqs. 5-8) from the same state.  Also covers the first sweep after
+    pp_init, whose dA = 0 terms are taken as M_p directly."""
+    cfg = synth.custom(N, s, R, noise_var=1e-4, seed=60 + N)
+    T = dev_tensor(cpd, cfg)
+    To = O.make_tensor(cfg)
+    nt2 = O.norm2(To)
+    m = _model(cpd, cfg, T)
+    A = synth.init_factors(cfg)
+    for _ in range(4):
+        m.msdt_sweep()
+        A = O.als_sweep(To, A, nt2)["A"]
+    A = [m.get_factor(n) for n in range(N)]
+    m.pp_init()
+    st = O.pp_init(To, A)
+    fs = [m.pp_approx_sweep()[0] for _ in range(4)]
+    for k in range(4):
+        out = O.pp_approx_sweep(st, A, nt2)
+        A = out["A"]
+        assert abs(fs[k] - out["f"]) <= TOL * abs(out["f"]), (k, fs[k], out["f"])
+    for n in range(N):
+        assert rel(m.get_factor(n), A[n]) <= 1e-9, (n, rel(m.get_factor(n), A[n]))
+    m.close()
