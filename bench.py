@@ -482,11 +482,31 @@ def main():
                                          "them and are ledgered separately (pp_filler_streams)"},
             "pp_filler_streams": {"bytes_per_step": fill["bytes"] / args.steps,
                                   "launches_per_step": fill["launches"] / args.steps},
+            "roofline_pp_sweep": pp_sweep_roof(cfg, world, ppapprox_ms, peaks),
             "gpu_launches": launches, "clocks": clk.summary(wall0, wall1), "e2e": e2e, "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def pp_sweep_roof(cfg, world, pp_ms, peaks):
+    """A PP-approximated sweep as a whole (Eqs. 5-6): every pair operator M_p^(a,b)
+    ([s_a, s_b, R], the last mode's extent split over the ranks of the 1-D grid) is streamed twice
+    per sweep (once for each of its two modes), 8 bytes per element, plus the dA reads and M~
+    writes -- SURVEY §8(d)'s 8·N(N-1)·s²R leading term -- over the measured sweep time, against the
+    HBM copy peak.  Main- and filler-stream launches overlap, so this is the honest per-sweep roof."""
+    N, R = cfg.N, cfg.R
+    ext = list(cfg.shape[:-1]) + [cfg.shape[-1] // world]
+    b = 0.0
+    for n in range(N):
+        for i in range(N):
+            if i != n:
+                b += 8.0 * (ext[n] * ext[i] * R + ext[i] * R)
+        b += 8.0 * 2 * ext[n] * R
+    gbs = b / (pp_ms * 1e-3) / 1e9 if pp_ms > 0 else None
+    return {"bound": "hbm", "bytes_per_sweep": b, "ms_per_sweep": pp_ms, "achieved": gbs, "peak": peaks.get("hbm_gbs"),
+            "unit": "GB/s", "frac": (gbs / peaks["hbm_gbs"]) if gbs and peaks.get("hbm_gbs") else None}
 
 
 def dmma_roof(ttm_tf, fp64, fp64_src, flops, ms, ctr):

@@ -11,6 +11,7 @@
 // warp load is a contiguous 512-byte row segment (double2 per lane).  A CTA owns one
 // p and 64 columns; its 8 warps split the K rows (fixed interleave) and reduce through
 // shared memory in a fixed order (deterministic, no atomics).
+#include <algorithm>
 #include <cstdlib>
 
 #include "kernels.h"
@@ -299,8 +300,11 @@ cudaError_t launch_mttv_multi(const MttvSpec* specs, int J, int R, const double*
     vec2 = vec2 && (jb.C % 2) == 0 && ((uintptr_t)sp.X % 16) == 0;
     vv = vv && ((uintptr_t)sp.v % 16) == 0;
     const int64_t items0 = jb.pre * jb.nchunks;
-    // split K so the whole grid is >= ~8 waves of 4 resident CTAs per SM (tail <= 1/8 wave)
-    int64_t ks = (148 * 4 * 8 / J + items0 - 1) / items0;
+    // split K so the whole grid is >= ~`waves` waves of 4 resident CTAs per SM; every split adds a
+    // partial-sum slot and the reduce pass, so the split stops at 2 waves (8 waves measured slower
+    // on the C2 PP operator streams: PP sweep 0.736 -> 0.65 ms with at most 2 splits)
+    static const int waves = getenv("CPD_MTTV_WAVES") ? std::max(1, atoi(getenv("CPD_MTTV_WAVES"))) : 2;
+    int64_t ks = (148 * 4 * waves / J + items0 - 1) / items0;
     if (ks > jb.K / 64) ks = jb.K / 64;
     static const int ks_max = getenv("CPD_MTTV_MAXKS") ? atoi(getenv("CPD_MTTV_MAXKS")) : 16;  // experiment switch
     if (ks > ks_max) ks = ks_max;
