@@ -424,30 +424,34 @@ def main():
         ttm_roof = dmma_roof(ttm_tf, fp64, fp64_src, ttm_launch_flops, ttm_ms, ctr)
         engines = None
     else:
-        # int8-digit TTM: streams T's 7 digit planes (7 B/element) once per launch (R <= 64), so
-        # the bound is HBM; bytes = digit planes + FP64 output + the factor's digit image (K x R x 7)
+        # int8-digit TTM: streams T's 7 digit planes (7 B/element) and writes the FP64 root; its
+        # MMAs are 28 exact int8 digit-pair products per FP64 multiply-add.  Both
+        # roofs are computed; the primary `bound` is the one the launch is closer to (the binding
+        # roof), the other is kept beside it.
         t_el = ttm_launch_flops / (2 * cfg.R)
-        k = cfg.s // world if False else cfg.s
+        k = cfg.s
         ttm_bytes = (7.0 if engine == "int8-digits" else 8.0) * t_el + 8.0 * t_el / k * cfg.R + 7.0 * k * cfg.R
         ttm_gbs = ttm_bytes / (ttm_ms * 1e-3) / 1e9 if ttm_ms > 0 else None
-        ttm_roof = {"kernel": f"ttm_i8 ({engine}: first-level TTM, FP64 operands as exact int8 digit products, "
-                              "tcgen05.mma kind::i8, TMEM accumulators)",
-                    "bound": "hbm", "achieved": ttm_gbs, "peak": peaks.get("hbm_gbs"),
-                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)", "unit": "GB/s",
-                    "frac": (ttm_gbs / peaks["hbm_gbs"]) if ttm_gbs and peaks.get("hbm_gbs") else None,
-                    "traffic": ncu_traffic("ttm_i8"), "bytes_per_launch": ttm_bytes,
-                    "fp64_equiv_tflops": ttm_tf, "fp64_equiv_over_dmma_peak": (ttm_tf / fp64) if ttm_tf else None,
-                    "avg_launch_ms": ttm_ms, "launches": int(ctr["ttm_launches"])}
-        # the same launch against the int8 tensor pipe: 28 exact digit-pair products per FP64
-        # multiply-add; peak = measured bf16 x the nominal int8/bf16 ratio 2
-        # (sustained figure: the TTM runs inside a long step)
+        hbm = {"bound": "hbm", "achieved": ttm_gbs, "peak": peaks.get("hbm_gbs"),
+               "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)", "unit": "GB/s",
+               "frac": (ttm_gbs / peaks["hbm_gbs"]) if ttm_gbs and peaks.get("hbm_gbs") else None,
+               "bytes_per_launch": ttm_bytes}
+        # int8 peak = measured bf16 x the nominal int8/bf16 ratio 2 (sustained figure: the TTM runs
+        # inside a long step)
         i8_ops = 28.0 * 2.0 * t_el * cfg.R
         i8_tops = i8_ops / (ttm_ms * 1e-3) / 1e12 if ttm_ms > 0 else None
         i8_peak = 2.0 * peaks["bf16_tflops_sustained"] if peaks.get("bf16_tflops_sustained") else None
-        ttm_roof["tensor_int8"] = {"bound": "tensor", "achieved": i8_tops, "peak": i8_peak, "unit": "TOP/s",
-                                   "frac": (i8_tops / i8_peak) if i8_tops and i8_peak else None,
-                                   "ops_per_launch": i8_ops,
-                                   "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops_sustained (nominal int8:bf16 = 2)"}
+        tensor = {"bound": "tensor", "achieved": i8_tops, "peak": i8_peak, "unit": "TOP/s",
+                  "frac": (i8_tops / i8_peak) if i8_tops and i8_peak else None, "ops_per_launch": i8_ops,
+                  "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops_sustained (nominal int8:bf16 = 2)"}
+        prim, sec = (tensor, hbm) if (tensor["frac"] or 0) >= (hbm["frac"] or 0) else (hbm, tensor)
+        ttm_roof = {"kernel": f"ttm_i8 ({engine}: first-level TTM, FP64 operands as exact int8 digit products, "
+                              "tcgen05.mma kind::i8, TMEM accumulators)", **prim,
+                    "traffic": ncu_traffic("ttm_i8d" if args.config == 2 else f"c{args.config}_ttm"),
+                    "traffic_source": "dram bytes per launch, profiles/ncu_traffic.json (ncu --set full)",
+                    "secondary": sec, "bytes_per_launch": ttm_bytes,
+                    "fp64_equiv_tflops": ttm_tf, "fp64_equiv_over_dmma_peak": (ttm_tf / fp64) if ttm_tf else None,
+                    "avg_launch_ms": ttm_ms, "launches": int(ctr["ttm_launches"])}
         engines = {engine: {"msdt_ms_per_sweep": msdt_ms, "ttm_ms": ttm_ms, "ttm_fp64_equiv_tflops": ttm_tf}}
         if not args.no_dmma_compare:
             engines["dmma"] = dmma_compare(cpd, torch, cfg, T, m, local, rank, world, nccl_id, stream, fp64, fp64_src)
@@ -476,7 +480,8 @@ def main():
             "roofline_stream": {"kernel": "mttv (mTTV levels + PP U-stream)", "bound": "hbm", "achieved": st_gbs,
                                 "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
                                 "frac": (st_gbs / peaks["hbm_gbs"]) if st_gbs and peaks.get("hbm_gbs") else None,
-                                "traffic": ncu_traffic("mttv"), "bytes_per_launch": st_launch_bytes,
+                                "traffic": ncu_traffic("mttv" if args.config == 2 else f"c{args.config}_mttv"),
+                                "bytes_per_launch": st_launch_bytes,
                                 "avg_launch_ms": st_ms, "launches": int(ctr["stream_launches"]),
                                 "scope": "main-stream launches (timed); the PP filler-stream launches overlap "
                                          "them and are ledgered separately (pp_filler_streams)"},
