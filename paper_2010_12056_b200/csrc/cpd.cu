@@ -816,33 +816,96 @@ cpd_status regular_sweep(cpd_ctx* ctx, bool msdt, double* f_out) {
 
 // produce all pair operators in `targets` (subsets of node.kept) from `node` (greedy
 // shared descent); node buffer is not freed here
-cpd_status pp_descend(cpd_ctx* ctx, const Node& node, std::vector<std::pair<int, int>> targets) {
-  if (node.kept.size() == 2) {
-    // the node is itself the operator (copy unless the caller hands over ownership)
-    return fail(ctx, CPD_ERR_INTERNAL, "pp_descend on a pair");
-  }
-  while (!targets.empty()) {
-    // choose the mode m whose removal keeps the most targets
-    int best = -1, bestc = -1;
-    for (int m : node.kept) {
-      int cnt = 0;
-      for (auto& pr : targets)
-        if (pr.first != m && pr.second != m) cnt++;
-      if (cnt > bestc) {
-        bestc = cnt;
-        best = m;
-      }
+// the mode of `node` whose contraction keeps the most of `targets`
+int pp_best_mode(const Node& node, const std::vector<std::pair<int, int>>& targets) {
+  int best = -1, bestc = -1;
+  for (int m : node.kept) {
+    int cnt = 0;
+    for (auto& pr : targets)
+      if (pr.first != m && pr.second != m) cnt++;
+    if (cnt > bestc) {
+      bestc = cnt;
+      best = m;
     }
-    std::vector<std::pair<int, int>> sub, rest;
-    for (auto& pr : targets) (pr.first != best && pr.second != best ? sub : rest).push_back(pr);
-    Node child;
-    TRY(contract_modes(ctx, node, {best}, {best}, &child));
+  }
+  return best;
+}
+
+// two children of `node` (contract mode ma, resp. mb) from ONE read of the node (mTTV dual kernel)
+cpd_status contract_dual(cpd_ctx* ctx, const Node& node, int ma, int mb, Node* ca, Node* cb) {
+  const auto& kp = node.kept;
+  int qa = (int)(std::find(kp.begin(), kp.end(), ma) - kp.begin());
+  int qb = (int)(std::find(kp.begin(), kp.end(), mb) - kp.begin());
+  const bool swap = qa > qb;
+  if (swap) std::swap(qa, qb);
+  int64_t P = 1, Q = 1, C = ctx->R;
+  for (int i = 0; i < qa; i++) P *= ext(ctx, kp[i]);
+  for (int i = qa + 1; i < qb; i++) Q *= ext(ctx, kp[i]);
+  for (int i = qb + 1; i < (int)kp.size(); i++) C *= ext(ctx, kp[i]);
+  const int m1 = kp[qa], m2 = kp[qb];  // out1 contracts m1, out2 contracts m2
+  Node c1, c2;
+  for (int k : kp) {
+    if (k != m1) c1.kept.push_back(k);
+    if (k != m2) c2.kept.push_back(k);
+  }
+  TRY(dalloc(ctx, &c1.buf, node_elems(ctx, c1.kept)));
+  TRY(dalloc(ctx, &c2.buf, node_elems(ctx, c2.kept)));
+  const int64_t K1 = ext(ctx, m1), K2 = ext(ctx, m2);
+  const int64_t nkb = (K1 + 31) / 32;
+  const int64_t E1 = node_elems(ctx, c1.kept);
+  double* ws = nullptr;
+  if (nkb > 1) TRY(dalloc(ctx, &ws, nkb * E1));
+  {
+    PhaseScope ps(ctx, PH_MTTV);
+    CU(cpd::launch_mttv_dual(node.buf, P, K1, Q, K2, C, ctx->R, ctx->A[m1], ctx->A[m2], c1.buf, c2.buf, ws,
+                             nkb * E1, ctx->st));
+  }
+  if (ws) dfree(ctx, ws);
+  ctx->counters[2] += 8.0 * ((double)node_elems(ctx, kp) + E1 + node_elems(ctx, c2.kept) + (K1 + K2) * ctx->R);
+  ctx->counters[3] += 1;
+  *ca = swap ? c2 : c1;
+  *cb = swap ? c1 : c2;
+  return CPD_OK;
+}
+
+// produce all pair operators in `targets` (subsets of node.kept) from `node` (greedy shared
+// descent: the child keeping the most targets first; the next child, for the targets the first
+// one cannot give, is built in the same read of the node by the dual mTTV); the node buffer is
+// not freed here
+cpd_status pp_descend(cpd_ctx* ctx, const Node& node, std::vector<std::pair<int, int>> targets) {
+  if (node.kept.size() == 2) return fail(ctx, CPD_ERR_INTERNAL, "pp_descend on a pair");
+  static const bool no_dual = getenv("CPD_PP_NO_DUAL") != nullptr;
+  auto take = [&](Node& child, std::vector<std::pair<int, int>>& sub) -> cpd_status {
     if (child.kept.size() == 2) {
       ctx->ops[{child.kept[0], child.kept[1]}] = child.buf;
     } else {
       TRY(pp_descend(ctx, child, sub));
       dfree(ctx, child.buf);
     }
+    return CPD_OK;
+  };
+  auto split = [](const std::vector<std::pair<int, int>>& t, int m, std::vector<std::pair<int, int>>& sub,
+                  std::vector<std::pair<int, int>>& rest) {
+    for (auto& pr : t) (pr.first != m && pr.second != m ? sub : rest).push_back(pr);
+  };
+  while (!targets.empty()) {
+    const int best = pp_best_mode(node, targets);
+    std::vector<std::pair<int, int>> sub, rest;
+    split(targets, best, sub, rest);
+    if (!rest.empty() && !no_dual) {
+      const int best2 = pp_best_mode(node, rest);
+      std::vector<std::pair<int, int>> sub2, rest2;
+      split(rest, best2, sub2, rest2);
+      Node c1, c2;
+      TRY(contract_dual(ctx, node, best, best2, &c1, &c2));
+      TRY(take(c1, sub));
+      TRY(take(c2, sub2));
+      targets = rest2;
+      continue;
+    }
+    Node child;
+    TRY(contract_modes(ctx, node, {best}, {best}, &child));
+    TRY(take(child, sub));
     targets = rest;
   }
   return CPD_OK;

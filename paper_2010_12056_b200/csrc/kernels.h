@@ -76,6 +76,12 @@ struct OutMap {
 };
 cudaError_t launch_mttv_multi(const MttvSpec* specs, int J, int R, const double* base, double* out, int beta,
                               double* ws, int64_t ws_elems, cudaStream_t st, const OutMap* map = nullptr);
+// Two single-mode contractions of one node in one read (PP-init multi-output descent):
+// X viewed as [P][K1][Q][K2][C] (C = trailing extents x R), out1 = contract K1 -> [P][Q][K2][C],
+// out2 = contract K2 -> [P][K1][Q][C]; ws: ceil(K1/32) x |out1| doubles of partials when K1 > 32.
+cudaError_t launch_mttv_dual(const double* X, int64_t P, int64_t K1, int64_t Q, int64_t K2, int64_t C, int R,
+                             const double* v1, const double* v2, double* out1, double* out2, double* ws,
+                             int64_t ws_elems, cudaStream_t st);
 // dst[e] = Σ_{q < nq} src[q * n + e], q in fixed order (the owner's sum of the received slots)
 cudaError_t launch_slot_sum(const double* src, int nq, int64_t n, double* dst, cudaStream_t st);
 

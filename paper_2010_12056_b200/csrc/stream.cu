@@ -147,6 +147,108 @@ __global__ void mttv_reduce_kernel(const double* __restrict__ ws, int slots, int
   }
 }
 
+// Two contractions of one node in one read (PP-init's multi-output descent, SURVEY a9 "deeper levels
+// from each parent in one multi-output pass"): X viewed as [P][K1][Q][K2][C],
+//   out1[p][q][k2][c] = Σ_{k1} X[p][k1][q][k2][c] v1[k1][c % R]   (contract K1)
+//   out2[p][k1][q][c] = Σ_{k2} X[p][k1][q][k2][c] v2[k2][c % R]   (contract K2).
+// A CTA owns (p, q, a block of 32 k1 rows, 64 columns) and walks all k2: out2 of its rows completes
+// in registers; out1 gets the block's partial (8 warps x 4 rows, fixed-order shared-memory sum per
+// group of 4 k2), written to ws[k1 block] (or straight to out1 when K1 <= 32) and summed over the
+// blocks in block order by mttv_reduce_kernel (deterministic).
+constexpr int DU_ROWS = 32;   // k1 rows per CTA (8 warps x 4)
+constexpr int DU_K2B = 4;     // k2 values per shared-memory reduction
+template <bool VEC2>
+__global__ void __launch_bounds__(MT_THREADS)
+    mttv_dual_kernel(const double* __restrict__ X, int64_t P, int64_t K1, int64_t Q, int64_t K2, int64_t C, int R,
+                     const double* __restrict__ v1, const double* __restrict__ v2, double* __restrict__ out1,
+                     double* __restrict__ out2, double* __restrict__ ws, int nkb) {
+  __shared__ double red[DU_K2B][8][MT_COLS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nch = (int)((C + MT_COLS - 1) / MT_COLS);
+  int64_t b = blockIdx.x;
+  const int ch = (int)(b % nch);
+  b /= nch;
+  const int kb = (int)(b % nkb);
+  b /= nkb;
+  const int64_t q = b % Q, p = b / Q;
+  const int64_t cA = (int64_t)ch * MT_COLS + (VEC2 ? 2 * lane : lane);
+  const int64_t cB = VEC2 ? cA + 1 : cA + 32;
+  const bool okA = cA < C, okB = cB < C;
+  const int rA = okA ? (int)(cA % R) : 0, rB = okB ? (int)(cB % R) : 0;
+  int64_t y[4];
+  bool yok[4];
+  const double* xr[4];
+#pragma unroll
+  for (int u = 0; u < 4; u++) {
+    y[u] = (int64_t)kb * DU_ROWS + warp + 8 * u;
+    yok[u] = y[u] < K1;
+    xr[u] = X + ((p * K1 + (yok[u] ? y[u] : 0)) * Q + q) * K2 * C;
+  }
+  double w1a[4], w1b[4];
+#pragma unroll
+  for (int u = 0; u < 4; u++) {
+    w1a[u] = (yok[u] && okA) ? v1[y[u] * R + rA] : 0.0;
+    w1b[u] = (yok[u] && okB) ? v1[y[u] * R + rB] : 0.0;
+  }
+  double a2[4] = {0, 0, 0, 0}, b2[4] = {0, 0, 0, 0};
+  const int64_t E1 = P * Q * K2 * C;
+  for (int64_t k0 = 0; k0 < K2; k0 += DU_K2B) {
+#pragma unroll
+    for (int j = 0; j < DU_K2B; j++) {
+      const int64_t k2 = k0 + j;
+      double pa = 0.0, pb = 0.0;
+      if (k2 < K2 && okA) {
+        const double v2a = v2[k2 * R + rA], v2b = okB ? v2[k2 * R + rB] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          if (!yok[u]) continue;
+          double xa, xb;
+          if (VEC2) {
+            const double2 x2 = __ldcs(reinterpret_cast<const double2*>(xr[u] + k2 * C + cA));
+            xa = x2.x;
+            xb = x2.y;
+          } else {
+            xa = __ldcs(xr[u] + k2 * C + cA);
+            xb = okB ? __ldcs(xr[u] + k2 * C + cB) : 0.0;
+          }
+          a2[u] = fma(xa, v2a, a2[u]);
+          b2[u] = fma(xb, v2b, b2[u]);
+          pa = fma(xa, w1a[u], pa);
+          pb = fma(xb, w1b[u], pb);
+        }
+      }
+      if (VEC2) {
+        red[j][warp][2 * lane] = pa;
+        red[j][warp][2 * lane + 1] = pb;
+      } else {
+        red[j][warp][lane] = pa;
+        red[j][warp][lane + 32] = pb;
+      }
+    }
+    __syncthreads();
+    {
+      const int j = threadIdx.x / MT_COLS, col = threadIdx.x % MT_COLS;  // 4 x 64 outputs, one per thread
+      const int64_t k2 = k0 + j, c = (int64_t)ch * MT_COLS + col;
+      if (k2 < K2 && c < C) {
+        double s = red[j][0][col];
+#pragma unroll
+        for (int w = 1; w < 8; w++) s += red[j][w][col];
+        const int64_t e = ((p * Q + q) * K2 + k2) * C + c;
+        if (ws) ws[(int64_t)kb * E1 + e] = s;
+        else out1[e] = s;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < 4; u++) {
+    if (!yok[u]) continue;
+    double* o = out2 + ((p * K1 + y[u]) * Q + q) * C;
+    if (okA) o[cA] = a2[u];
+    if (okB) o[cB] = b2[u];
+  }
+}
+
 __global__ void scatter_copy_kernel(const double* __restrict__ src, int64_t n, OutMap om) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
     *map_dst(om, nullptr, e) = src[e];
@@ -366,6 +468,33 @@ cudaError_t launch_mttv_multi(const MttvSpec* specs, int J, int R, const double*
     int64_t blocks = (jobs.E + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
     mttv_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(ws, (int)slots, jobs.E, base, out, beta, om);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mttv_dual(const double* X, int64_t P, int64_t K1, int64_t Q, int64_t K2, int64_t C, int R,
+                             const double* v1, const double* v2, double* out1, double* out2, double* ws,
+                             int64_t ws_elems, cudaStream_t st) {
+  if (P <= 0 || Q <= 0 || C <= 0 || K1 <= 0 || K2 <= 0) return cudaSuccess;
+  static_assert(MT_THREADS == DU_K2B * MT_COLS, "one reduction output per thread");
+  const int nkb = (int)((K1 + DU_ROWS - 1) / DU_ROWS);
+  const int64_t E1 = P * Q * K2 * C;
+  if (nkb > 1 && (ws == nullptr || (int64_t)nkb * E1 > ws_elems)) return cudaErrorInvalidValue;
+  const int64_t nch = (C + MT_COLS - 1) / MT_COLS;
+  const int64_t grid = P * Q * nkb * nch;
+  if (grid > 0x7fffffff) return cudaErrorInvalidConfiguration;
+  const bool vec2 = (C % 2) == 0 && ((uintptr_t)X % 16) == 0;
+  double* w = nkb > 1 ? ws : nullptr;
+  g_launches++;
+  if (vec2)
+    mttv_dual_kernel<true><<<(unsigned)grid, MT_THREADS, 0, st>>>(X, P, K1, Q, K2, C, R, v1, v2, out1, out2, w, nkb);
+  else
+    mttv_dual_kernel<false><<<(unsigned)grid, MT_THREADS, 0, st>>>(X, P, K1, Q, K2, C, R, v1, v2, out1, out2, w, nkb);
+  if (nkb > 1) {
+    int64_t blocks = (E1 + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    g_launches++;
+    mttv_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(ws, nkb, E1, nullptr, out1, 0, OutMap{});
   }
   return cudaGetLastError();
 }

@@ -73,7 +73,64 @@ __device__ __forceinline__ void rowvec_mat(const double (&v)[U], const double* _
   for (int u = 0; u < U; u++) out[u] = e[u] + o[u];
 }
 
-template <int U>
+// phase 2b: S, dS = Σ over the nparts CTA partials in CTA order (deterministic; S exactly symmetric);
+// gt / nthr: this thread's index in, and the size of, the grid doing the reduction; t0 >= 0 for the
+// threads 0..2 of one CTA (the scalar sums)
+__device__ __forceinline__ void reduce_partials(const double* __restrict__ gpart, const double* __restrict__ part,
+                                                unsigned nparts, int64_t nout, int64_t RR, int64_t gt, int64_t nthr,
+                                                int t0, double* __restrict__ S, double* __restrict__ dS,
+                                                double* __restrict__ o_dA2, double* __restrict__ o_A2,
+                                                double* __restrict__ o_MA) {
+  // 4 lanes per output when the grid has the threads (lane q sums the CTA partials c = q mod 4 in
+  // ascending c, then ((s0 + s1) + (s2 + s3))): a fixed order either way
+  if (nout * 4 <= nthr) {
+    const int64_t e = gt >> 2;
+    const int q = (int)(gt & 3);
+    double acc = 0.0;
+    if (e < nout) {
+      unsigned c = q;
+      for (; c + 12 < nparts; c += 16) {
+        double v[4];
+#pragma unroll
+        for (int t = 0; t < 4; t++) v[t] = gpart[(int64_t)(c + 4 * t) * nout + e];
+#pragma unroll
+        for (int t = 0; t < 4; t++) acc += v[t];
+      }
+      for (; c < nparts; c += 4) acc += gpart[(int64_t)c * nout + e];
+    }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    if (e < nout && q == 0) {
+      if (e < RR) S[e] = acc;
+      else dS[e - RR] = acc;
+    }
+  } else {
+    for (int64_t e = gt; e < nout; e += nthr) {
+      // CTA partials in CTA order; 16 independent loads in flight per batch
+      double acc = gpart[e];
+      unsigned c = 1;
+      for (; c + 16 <= nparts; c += 16) {
+        double v[16];
+#pragma unroll
+        for (int q = 0; q < 16; q++) v[q] = gpart[(int64_t)(c + q) * nout + e];
+#pragma unroll
+        for (int q = 0; q < 16; q++) acc += v[q];
+      }
+      for (; c < nparts; c++) acc += gpart[(int64_t)c * nout + e];
+      if (e < RR) S[e] = acc;
+      else dS[e - RR] = acc;
+    }
+  }
+  if (t0 >= 0 && t0 < 3) {
+    double s = part[t0];
+    for (unsigned b = 1; b < nparts; b++) s += part[b * 3 + t0];
+    if (t0 == 0) *o_dA2 = s;
+    if (t0 == 1) *o_A2 = s;
+    if (t0 == 2 && o_MA) *o_MA = s;
+  }
+}
+
+template <int U, bool SPLIT>
 __global__ void __launch_bounds__(UPD_THREADS)
     update_fused_kernel(int R, int64_t rows, const double* __restrict__ Gi, const double* __restrict__ W,
                         double* __restrict__ M, double* __restrict__ A, const double* __restrict__ base,
@@ -171,70 +228,43 @@ __global__ void __launch_bounds__(UPD_THREADS)
     for (int r = 0; r < nrows; r++) acc = fma(Xs[r * R + a], Y[r * R + b], acc);
     gpart[(int64_t)blockIdx.x * nout + e] = acc;
   }
+  if constexpr (SPLIT) return;  // phase 2b in update_reduce_kernel (a second, ordinary launch)
   cg::this_grid().sync();
-  // phase 2b: S, dS = Σ over CTAs in CTA order (deterministic; S exactly symmetric)
-  // 4 lanes per output when the grid has the threads (lane q sums the CTA partials c = q mod 4 in
-  // ascending c, then ((s0 + s1) + (s2 + s3))): a fixed order either way
-  const int64_t nthr = (int64_t)gridDim.x * UPD_THREADS;
-  const int64_t gt = (int64_t)blockIdx.x * UPD_THREADS + tid;
-  if (nout * 4 <= nthr) {
-    const int64_t e = gt >> 2;
-    const int q = (int)(gt & 3);
-    double acc = 0.0;
-    if (e < nout) {
-      unsigned c = q;
-      for (; c + 12 < gridDim.x; c += 16) {
-        double v[4];
-#pragma unroll
-        for (int t = 0; t < 4; t++) v[t] = gpart[(int64_t)(c + 4 * t) * nout + e];
-#pragma unroll
-        for (int t = 0; t < 4; t++) acc += v[t];
-      }
-      for (; c < gridDim.x; c += 4) acc += gpart[(int64_t)c * nout + e];
-    }
-    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-    if (e < nout && q == 0) {
-      if (e < RR) S[e] = acc;
-      else dS[e - RR] = acc;
-    }
-  } else {
-    for (int64_t e = gt; e < nout; e += nthr) {
-      // CTA partials in CTA order; 16 independent loads in flight per batch
-      double acc = gpart[e];
-      unsigned c = 1;
-      for (; c + 16 <= gridDim.x; c += 16) {
-        double v[16];
-#pragma unroll
-        for (int q = 0; q < 16; q++) v[q] = gpart[(int64_t)(c + q) * nout + e];
-#pragma unroll
-        for (int q = 0; q < 16; q++) acc += v[q];
-      }
-      for (; c < gridDim.x; c++) acc += gpart[(int64_t)c * nout + e];
-      if (e < RR) S[e] = acc;
-      else dS[e - RR] = acc;
-    }
-  }
-  if (blockIdx.x == 0 && tid < 3) {
-    double s = part[tid];
-    for (unsigned b = 1; b < gridDim.x; b++) s += part[b * 3 + tid];
-    if (tid == 0) *o_dA2 = s;
-    if (tid == 1) *o_A2 = s;
-    if (tid == 2 && o_MA) *o_MA = s;
-  }
+  reduce_partials(gpart, part, gridDim.x, nout, RR, (int64_t)blockIdx.x * UPD_THREADS + tid,
+                  (int64_t)gridDim.x * UPD_THREADS, blockIdx.x == 0 ? tid : -1, S, dS, o_dA2, o_A2, o_MA);
 }
 
+__global__ void __launch_bounds__(UPD_THREADS)
+    update_reduce_kernel(const double* __restrict__ gpart, const double* __restrict__ part, unsigned nparts,
+                         int64_t nout, int64_t RR, double* __restrict__ S, double* __restrict__ dS,
+                         double* __restrict__ o_dA2, double* __restrict__ o_A2, double* __restrict__ o_MA) {
+  reduce_partials(gpart, part, nparts, nout, RR, (int64_t)blockIdx.x * UPD_THREADS + threadIdx.x,
+                  (int64_t)gridDim.x * UPD_THREADS, blockIdx.x == 0 ? (int)threadIdx.x : -1, S, dS, o_dA2, o_A2,
+                  o_MA);
+}
+
+
+// SPLIT (experiment switch CPD_UPD_SPLIT): the row phase as an ordinary launch (its CTAs start as SMs
+// free up, no co-residency, no grid barrier) and the partial-sum reduction as a second launch
 template <int U>
-cudaError_t coop_launch(int blocks, size_t smem, void** args, cudaStream_t st) {
-  static bool attr = false;  // per instantiation
+cudaError_t coop_launch(int blocks, size_t smem, void** args, cudaStream_t st, bool split) {
+  static bool attr = false, attr_s = false;  // per instantiation
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(update_fused_kernel<U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(update_fused_kernel<U, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          227 * 1024 - 2048);
     if (e != cudaSuccess) return e;
     attr = true;
   }
+  if (!attr_s) {
+    cudaError_t e = cudaFuncSetAttribute(update_fused_kernel<U, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         227 * 1024 - 2048);
+    if (e != cudaSuccess) return e;
+    attr_s = true;
+  }
   g_launches++;
-  return cudaLaunchCooperativeKernel((void*)update_fused_kernel<U>, blocks, UPD_THREADS, args, smem, st);
+  if (!split)
+    return cudaLaunchCooperativeKernel((void*)update_fused_kernel<U, false>, blocks, UPD_THREADS, args, smem, st);
+  return cudaLaunchKernel((void*)update_fused_kernel<U, true>, blocks, UPD_THREADS, args, smem, st);
 }
 
 }  // namespace
@@ -262,14 +292,25 @@ cudaError_t launch_update_fused(int R, int64_t rows, const double* Ginv, const d
   const size_t smem = update_fused_smem(R, W != nullptr, RB);
   if (smem > 227 * 1024 - 2048) return cudaErrorInvalidValue;
   void* args[] = {&R, &rows, &Ginv, &W, &M, &A, &base, &dA, &S, &dS, &part, &gpart, &RB, &o_dA2, &o_A2, &o_MA, &st_src, &st_dst};
+  static const bool split = getenv("CPD_UPD_SPLIT") != nullptr;
+  cudaError_t e = cudaErrorInvalidValue;
   switch ((R + 31) / 32) {
-    case 1: return coop_launch<1>(blocks, smem, args, st);
-    case 2: return coop_launch<2>(blocks, smem, args, st);
-    case 3: return coop_launch<3>(blocks, smem, args, st);
-    case 4: return coop_launch<4>(blocks, smem, args, st);
-    case 5: return coop_launch<5>(blocks, smem, args, st);
+    case 1: e = coop_launch<1>(blocks, smem, args, st, split); break;
+    case 2: e = coop_launch<2>(blocks, smem, args, st, split); break;
+    case 3: e = coop_launch<3>(blocks, smem, args, st, split); break;
+    case 4: e = coop_launch<4>(blocks, smem, args, st, split); break;
+    case 5: e = coop_launch<5>(blocks, smem, args, st, split); break;
   }
-  return cudaErrorInvalidValue;
+  if (e != cudaSuccess || !split) return e;
+  const int64_t RR = (int64_t)R * R;
+  const int64_t nout = S ? (dS ? 2 * RR : RR) : 0;
+  int64_t rb = (4 * nout + UPD_THREADS - 1) / UPD_THREADS;
+  if (rb < 1) rb = 1;
+  if (rb > 4 * kUpdMaxBlocks) rb = 4 * kUpdMaxBlocks;
+  g_launches++;
+  update_reduce_kernel<<<(unsigned)rb, UPD_THREADS, 0, st>>>(gpart, part, (unsigned)blocks, nout, RR, S, dS, o_dA2,
+                                                             o_A2, o_MA);
+  return cudaGetLastError();
 }
 
 }  // namespace cpd

@@ -300,8 +300,8 @@ def test_set_factors_restarts_cycle(cpd):
 @pytest.mark.parametrize("ttm_impl", [0, 1])
 @pytest.mark.parametrize("c", [2, 3, 4, 5])
 def test_full_size_sampled_rows(cpd, c, ttm_impl):
-    """BASELINE configs at full size: one msdt_sweep; sampled rows of every M^(n) against
-    the oracle's slice-by-slice explicit-KRP rows with the GPU's input factors."""
+    """BASELINE configs at full size: one msdt_sweep and one dt_sweep; sampled rows of every M^(n)
+    against the oracle's slice-by-slice explicit-KRP rows with the GPU's input factors."""
     cfg = synth.config(c)
     torch.cuda.empty_cache()
     free, total = torch.cuda.mem_get_info()
@@ -314,15 +314,18 @@ def test_full_size_sampled_rows(cpd, c, ttm_impl):
     T = dev_tensor(cpd, cfg)
     m = _model(cpd, cfg, T, ttm_impl=ttm_impl)
     A0 = synth.init_factors(cfg)
-    m.msdt_sweep()
-    A1 = [m.get_factor(n) for n in range(cfg.N)]
     rng = np.random.default_rng(c)
-    for n in range(cfg.N):
-        Ause = A1[:n] + A0[n:]   # modes < n already updated in this sweep
-        rows = rng.choice(cfg.s, 2 if c == 5 else 3, replace=False)
-        ref = O.mttkrp_rows(cfg, Ause, n, rows)
-        got = m.get_last_mttkrp(n)[rows]
-        assert rel(got, ref) <= TOL, (n, rel(got, ref))
+    # one MSDT sweep, then one standard-DT sweep (Fig. 1a) from the MSDT sweep's factors
+    for sweep in (m.msdt_sweep, m.dt_sweep):
+        sweep()
+        A1 = [m.get_factor(n) for n in range(cfg.N)]
+        for n in range(cfg.N):
+            Ause = A1[:n] + A0[n:]   # modes < n already updated in this sweep
+            rows = rng.choice(cfg.s, 2 if c == 5 else 3, replace=False)
+            ref = O.mttkrp_rows(cfg, Ause, n, rows)
+            got = m.get_last_mttkrp(n)[rows]
+            assert rel(got, ref) <= TOL, (sweep.__name__, n, rel(got, ref))
+        A0 = A1
     m.close()
     del T
     torch.cuda.empty_cache()
