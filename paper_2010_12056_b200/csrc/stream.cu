@@ -34,6 +34,7 @@ struct MttvJob {
   const double* v;
   int64_t pre, K, C, rps, item0, slot0;
   int nchunks, ks;
+  int ppc;  // p values per CTA: 64 / C when the row is narrower than a CTA's 64 columns (C4: C = R = 32)
 };
 struct MttvJobs {
   MttvJob j[8];
@@ -44,31 +45,62 @@ struct MttvJobs {
 __device__ __forceinline__ double* map_dst(const OutMap& m, double* out, int64_t e) {
   if (m.nq == 0) return out + e;
   const int64_t q = e / m.chunk;
-  return m.dst[q] + (e - q * m.chunk);
+  double* d = m.dst[0];
+#pragma unroll
+  for (int k = 1; k < 8; k++) d = (q == k) ? m.dst[k] : d;  // static indices: no local copy of the map
+  return d + (e - q * m.chunk);
 }
 
-template <bool VEC2, bool VV>
-__global__ void __launch_bounds__(MT_THREADS)
+// 4 CTAs (32 warps, 128 loads of 512 bytes) resident per SM: at 80 registers only 3 fit, and the
+// stream was latency-bound at ~4.6-5.6 TB/s on the large-node contractions (C3/C4 roots)
+template <bool VEC2, bool VV, bool PACK>
+__global__ void __launch_bounds__(MT_THREADS, PACK ? 3 : 4)
     mttv_kernel(MttvJobs jobs, int R, double* __restrict__ out, int beta, double* __restrict__ ws, OutMap om) {
   __shared__ double red[8][MT_COLS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int jj = 0;
-  while (jj + 1 < jobs.J && (int64_t)blockIdx.x >= jobs.j[jj + 1].item0) jj++;
-  const MttvJob& jb = jobs.j[jj];
+  // this CTA's job, read from the parameter space with static indices only (a dynamically indexed
+  // copy of the job table went to the local stack)
+  struct {
+    const double* X;
+    const double* v;
+    int64_t pre, K, C, rps, item0, slot0;
+    int nchunks, ks, ppc;
+  } jb = {jobs.j[0].X, jobs.j[0].v, jobs.j[0].pre, jobs.j[0].K, jobs.j[0].C, jobs.j[0].rps, jobs.j[0].item0,
+          jobs.j[0].slot0, jobs.j[0].nchunks, jobs.j[0].ks, jobs.j[0].ppc};
+#pragma unroll
+  for (int q = 1; q < 8; q++) {
+    const bool sel = q < jobs.J && (int64_t)blockIdx.x >= jobs.j[q].item0;
+    jb.X = sel ? jobs.j[q].X : jb.X;
+    jb.v = sel ? jobs.j[q].v : jb.v;
+    jb.K = sel ? jobs.j[q].K : jb.K;
+    jb.C = sel ? jobs.j[q].C : jb.C;
+    jb.rps = sel ? jobs.j[q].rps : jb.rps;
+    jb.item0 = sel ? jobs.j[q].item0 : jb.item0;
+    jb.slot0 = sel ? jobs.j[q].slot0 : jb.slot0;
+    jb.nchunks = sel ? jobs.j[q].nchunks : jb.nchunks;
+    jb.ks = sel ? jobs.j[q].ks : jb.ks;
+    jb.pre = sel ? jobs.j[q].pre : jb.pre;
+    jb.ppc = sel ? jobs.j[q].ppc : jb.ppc;
+  }
   const int64_t local = (int64_t)blockIdx.x - jb.item0;
   const int split = (int)(local % jb.ks);
   const int64_t rest = local / jb.ks;
-  const int64_t p = rest / jb.nchunks;
+  const int ppc = PACK ? jb.ppc : 1;
+  const int64_t p = (rest / jb.nchunks) * ppc;  // first p of this CTA
   const int chunk = (int)(rest % jb.nchunks);
   const int64_t K = jb.K, C = jb.C;
   const double* __restrict__ v = jb.v;
   const int64_t k0 = split * jb.rps;
   const int64_t k1 = min(K, k0 + jb.rps);
-  const int64_t cA = (int64_t)chunk * MT_COLS + (VEC2 ? 2 * lane : lane);
-  const int64_t cB = VEC2 ? cA + 1 : cA + 32;
-  const bool okA = cA < C, okB = cB < C;
+  // virtual column cv in [0, 64) of the chunk; with ppc > 1 it spans ppc consecutive rows p of width C
+  const int64_t cvA = (int64_t)chunk * MT_COLS + (VEC2 ? 2 * lane : lane);
+  const int64_t cvB = VEC2 ? cvA + 1 : cvA + 32;
+  const int64_t pA = ppc > 1 ? p + cvA / C : p, pB = ppc > 1 ? p + cvB / C : p;
+  const int64_t cA = ppc > 1 ? cvA % C : cvA, cB = ppc > 1 ? cvB % C : cvB;
+  const bool okA = ppc > 1 ? pA < jb.pre : cA < C, okB = ppc > 1 ? pB < jb.pre : cB < C;
   const int rA = okA ? (int)(cA % R) : 0, rB = okB ? (int)(cB % R) : 0;
-  const double* Xp = jb.X + p * K * C;
+  const double* Xp = jb.X + pA * K * C;    // VEC2: cB = cA + 1 lies in the same row (C even)
+  const double* XpB = jb.X + pB * K * C;
   double sA = 0.0, sB = 0.0;
   if (okA) {
     int64_t y = k0 + warp;
@@ -85,7 +117,7 @@ __global__ void __launch_bounds__(MT_THREADS)
 #pragma unroll
         for (int u = 0; u < 4; u++) {
           a[u] = __ldcs(Xp + (y + 8 * u) * C + cA);
-          b[u] = okB ? __ldcs(Xp + (y + 8 * u) * C + cB) : 0.0;
+          b[u] = okB ? __ldcs(XpB + (y + 8 * u) * C + cB) : 0.0;
         }
       }
       if (VV) {
@@ -110,7 +142,7 @@ __global__ void __launch_bounds__(MT_THREADS)
     }
     for (; y < k1; y += 8) {
       sA = fma(Xp[y * C + cA], v[y * R + rA], sA);
-      if (okB) sB = fma(Xp[y * C + cB], v[y * R + rB], sB);
+      if (okB) sB = fma(XpB[y * C + cB], v[y * R + rB], sB);
     }
   }
   if (VEC2) {
@@ -122,16 +154,16 @@ __global__ void __launch_bounds__(MT_THREADS)
   }
   __syncthreads();
   if (threadIdx.x < MT_COLS) {
-    int64_t c = (int64_t)chunk * MT_COLS + threadIdx.x;
-    if (c < C) {
+    const int64_t cv = (int64_t)chunk * MT_COLS + threadIdx.x;
+    if (ppc > 1 ? p + cv / C < jb.pre : cv < C) {
       double s = red[0][threadIdx.x];
 #pragma unroll
       for (int w = 1; w < 8; w++) s += red[w][threadIdx.x];
+      const int64_t e = p * C + cv;  // rows p.. of width C are contiguous in the output
       if (ws == nullptr) {
-        const int64_t e = p * C + c;
         *map_dst(om, out, e) = beta ? out[e] + s : s;
       } else {
-        ws[(jb.slot0 + split) * jobs.E + p * C + c] = s;
+        ws[(jb.slot0 + split) * jobs.E + e] = s;
       }
     }
   }
@@ -370,6 +402,21 @@ __global__ void sub_kernel(const double* __restrict__ x, const double* __restric
 
 }  // namespace
 
+void launch_mttv_variant(bool vec2, bool vv, bool pack, unsigned grid, const MttvJobs& jobs, int R, double* out,
+                         int beta, double* ws, const OutMap& om, cudaStream_t st) {
+#define CPD_MTTV_V(V2, VV_, PK) mttv_kernel<V2, VV_, PK><<<grid, MT_THREADS, 0, st>>>(jobs, R, out, beta, ws, om)
+  if (pack) {
+    if (vec2 && vv) CPD_MTTV_V(true, true, true);
+    else if (vec2) CPD_MTTV_V(true, false, true);
+    else CPD_MTTV_V(false, false, true);
+  } else {
+    if (vec2 && vv) CPD_MTTV_V(true, true, false);
+    else if (vec2) CPD_MTTV_V(true, false, false);
+    else CPD_MTTV_V(false, false, false);
+  }
+#undef CPD_MTTV_V
+}
+
 cudaError_t launch_slot_sum(const double* src, int nq, int64_t n, double* dst, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   int64_t blocks = (n + 255) / 256;
@@ -399,9 +446,15 @@ cudaError_t launch_mttv_multi(const MttvSpec* specs, int J, int R, const double*
     jb.C = sp.post * R;
     if (jb.pre * jb.C != jobs.E || jb.K <= 0) return cudaErrorInvalidValue;
     jb.nchunks = (int)((jb.C + MT_COLS - 1) / MT_COLS);
+    jb.ppc = 1;
+    static const bool no_pack = getenv("CPD_MTTV_NO_PACK") != nullptr;  // experiment switch
+    if (!no_pack && jb.C < MT_COLS && MT_COLS % jb.C == 0) {  // several narrow rows per CTA
+      jb.ppc = (int)(MT_COLS / jb.C);
+      jb.nchunks = 1;
+    }
     vec2 = vec2 && (jb.C % 2) == 0 && ((uintptr_t)sp.X % 16) == 0;
     vv = vv && ((uintptr_t)sp.v % 16) == 0;
-    const int64_t items0 = jb.pre * jb.nchunks;
+    const int64_t items0 = (jb.pre + jb.ppc - 1) / jb.ppc * jb.nchunks;
     // split K so the whole grid is >= ~`waves` waves of 4 resident CTAs per SM; every split adds a
     // partial-sum slot and the reduce pass, so the split stops at 2 waves (8 waves measured slower
     // on the C2 PP operator streams: PP sweep 0.736 -> 0.65 ms with at most 2 splits)
@@ -435,15 +488,10 @@ cudaError_t launch_mttv_multi(const MttvSpec* specs, int J, int R, const double*
       one.j[0].rps = one.j[0].K;
       one.j[0].item0 = 0;
       one.j[0].slot0 = 0;
-      int64_t grid = one.j[0].pre * one.j[0].nchunks;
+      int64_t grid = (one.j[0].pre + one.j[0].ppc - 1) / one.j[0].ppc * one.j[0].nchunks;
       g_launches++;
       const OutMap none{};
-      if (vec2 && vv)
-        mttv_kernel<true, true><<<(unsigned)grid, MT_THREADS, 0, st>>>(one, R, out, q > 0 ? 1 : beta, nullptr, none);
-      else if (vec2)
-        mttv_kernel<true, false><<<(unsigned)grid, MT_THREADS, 0, st>>>(one, R, out, q > 0 ? 1 : beta, nullptr, none);
-      else
-        mttv_kernel<false, false><<<(unsigned)grid, MT_THREADS, 0, st>>>(one, R, out, q > 0 ? 1 : beta, nullptr, none);
+      launch_mttv_variant(vec2, vv, one.j[0].ppc > 1, (unsigned)grid, one, R, out, q > 0 ? 1 : beta, nullptr, none, st);
     }
     if (om.nq > 0) {  // the local result, then scattered to the owners' slots
       int64_t blocks = (jobs.E + 255) / 256;
@@ -457,12 +505,9 @@ cudaError_t launch_mttv_multi(const MttvSpec* specs, int J, int R, const double*
   double* w = direct ? nullptr : ws;
   g_launches++;
   const OutMap km = direct ? om : OutMap{};
-  if (vec2 && vv)
-    mttv_kernel<true, true><<<(unsigned)items, MT_THREADS, 0, st>>>(jobs, R, out, beta, w, km);
-  else if (vec2)
-    mttv_kernel<true, false><<<(unsigned)items, MT_THREADS, 0, st>>>(jobs, R, out, beta, w, km);
-  else
-    mttv_kernel<false, false><<<(unsigned)items, MT_THREADS, 0, st>>>(jobs, R, out, beta, w, km);
+  bool pack = false;  // jobs of one launch share the output size, not C: any packed job selects the variant
+  for (int q = 0; q < J; q++) pack = pack || jobs.j[q].ppc > 1;
+  launch_mttv_variant(vec2, vv, pack, (unsigned)items, jobs, R, out, beta, w, km, st);
   if (!direct) {
     g_launches++;
     int64_t blocks = (jobs.E + 255) / 256;
