@@ -816,6 +816,12 @@ cpd_status regular_sweep(cpd_ctx* ctx, bool msdt, double* f_out) {
 
 // produce all pair operators in `targets` (subsets of node.kept) from `node` (greedy
 // shared descent); node buffer is not freed here
+// filler-stream operator streams at 3 CTAs/SM (CPD_FILLER_OCC4: 4, the main-stream build)
+bool filler_occ3() {
+  static const bool occ4 = getenv("CPD_FILLER_OCC4") != nullptr;
+  return !occ4;
+}
+
 // the mode of `node` whose contraction keeps the most of `targets`
 int pp_best_mode(const Node& node, const std::vector<std::pair<int, int>>& targets) {
   int best = -1, bestc = -1;
@@ -1562,7 +1568,8 @@ cpd_status pp_approx_sweep(cpd_ctx* ctx, double* fitness_out, int* still_valid) 
       if (i != nx && i != nx - 1) sp[J++] = spec(nx, i, &bytes);
     CU(cudaEventRecord(ctx->ev_pp_a, ctx->st));  // update nx-2 (and everything before) enqueued
     CU(cudaStreamWaitEvent(ctx->st3, ctx->ev_pp_a, 0));
-    CU(cpd::launch_mttv_multi(sp, J, ctx->R, ctx->Mp[nx], M[nx], 0, ctx->ws_mttv3, kMttvWs, ctx->st3));
+    CU(cpd::launch_mttv_multi(sp, J, ctx->R, ctx->Mp[nx], M[nx], 0, ctx->ws_mttv3, kMttvWs, ctx->st3, nullptr,
+                                    filler_occ3()));
     CU(cudaEventRecord(ctx->ev_pp_side[nx], ctx->st3));
     ctx->filler[0] += bytes + 8.0 * 2 * ext(ctx, nx) * ctx->R;
     ctx->filler[1] += 1;
@@ -1586,7 +1593,8 @@ cpd_status pp_approx_sweep(cpd_ctx* ctx, double* fitness_out, int* still_valid) 
       for (int i = 1; i < N - 1; i++) sp[J++] = spec(0, i, &bytes);
       CU(cudaEventRecord(ctx->ev_pp_a, ctx->st));
       CU(cudaStreamWaitEvent(ctx->st3, ctx->ev_pp_a, 0));
-      CU(cpd::launch_mttv_multi(sp, J, ctx->R, ctx->Mp[0], Mnxt[0], 0, ctx->ws_mttv3, kMttvWs, ctx->st3));
+      CU(cpd::launch_mttv_multi(sp, J, ctx->R, ctx->Mp[0], Mnxt[0], 0, ctx->ws_mttv3, kMttvWs, ctx->st3, nullptr,
+                                    filler_occ3()));
       ctx->filler[0] += bytes + 8.0 * 2 * ext(ctx, 0) * ctx->R;
       ctx->filler[1] += 1;
     }
@@ -1633,7 +1641,8 @@ cpd_status pp_approx_sweep(cpd_ctx* ctx, double* fitness_out, int* still_valid) 
       sp[0] = spec(0, N - 1, &bytes);
       CU(cudaEventRecord(ctx->ev_pp_a, ctx->st));
       CU(cudaStreamWaitEvent(ctx->st3, ctx->ev_pp_a, 0));
-      CU(cpd::launch_mttv_multi(sp, 1, ctx->R, nullptr, Mnxt[0], 1, ctx->ws_mttv3, kMttvWs, ctx->st3));
+      CU(cpd::launch_mttv_multi(sp, 1, ctx->R, nullptr, Mnxt[0], 1, ctx->ws_mttv3, kMttvWs, ctx->st3, nullptr,
+                                    filler_occ3()));
       CU(cudaEventRecord(ctx->ev_pp_side[0], ctx->st3));
       ctx->filler[0] += bytes + 8.0 * 2 * ext(ctx, 0) * ctx->R;
       ctx->filler[1] += 1;

@@ -53,8 +53,8 @@ __device__ __forceinline__ double* map_dst(const OutMap& m, double* out, int64_t
 
 // 4 CTAs (32 warps, 128 loads of 512 bytes) resident per SM: at 80 registers only 3 fit, and the
 // stream was latency-bound at ~4.6-5.6 TB/s on the large-node contractions (C3/C4 roots)
-template <bool VEC2, bool VV, bool PACK>
-__global__ void __launch_bounds__(MT_THREADS, PACK ? 3 : 4)
+template <bool VEC2, bool VV, bool PACK, int OCC>
+__global__ void __launch_bounds__(MT_THREADS, PACK ? 3 : OCC)
     mttv_kernel(MttvJobs jobs, int R, double* __restrict__ out, int beta, double* __restrict__ ws, OutMap om) {
   __shared__ double red[8][MT_COLS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -187,14 +187,17 @@ __global__ void mttv_reduce_kernel(const double* __restrict__ ws, int slots, int
 // in registers; out1 gets the block's partial (8 warps x 4 rows, fixed-order shared-memory sum per
 // group of 4 k2), written to ws[k1 block] (or straight to out1 when K1 <= 32) and summed over the
 // blocks in block order by mttv_reduce_kernel (deterministic).
-constexpr int DU_ROWS = 32;   // k1 rows per CTA (8 warps x 4)
-constexpr int DU_K2B = 4;     // k2 values per shared-memory reduction
+constexpr int DU_THREADS = 512;             // 16 warps x 2 k1 rows
+constexpr int DU_WARPS = DU_THREADS / 32;
+constexpr int DU_RPW = 2;                   // k1 rows per warp
+constexpr int DU_ROWS = DU_WARPS * DU_RPW;  // k1 rows per CTA (32)
+constexpr int DU_K2B = 4;                   // k2 values per shared-memory reduction
 template <bool VEC2>
-__global__ void __launch_bounds__(MT_THREADS)
+__global__ void __launch_bounds__(DU_THREADS, 2)
     mttv_dual_kernel(const double* __restrict__ X, int64_t P, int64_t K1, int64_t Q, int64_t K2, int64_t C, int R,
                      const double* __restrict__ v1, const double* __restrict__ v2, double* __restrict__ out1,
                      double* __restrict__ out2, double* __restrict__ ws, int nkb) {
-  __shared__ double red[DU_K2B][8][MT_COLS];
+  __shared__ double red[DU_K2B][DU_WARPS][MT_COLS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nch = (int)((C + MT_COLS - 1) / MT_COLS);
   int64_t b = blockIdx.x;
@@ -207,22 +210,19 @@ __global__ void __launch_bounds__(MT_THREADS)
   const int64_t cB = VEC2 ? cA + 1 : cA + 32;
   const bool okA = cA < C, okB = cB < C;
   const int rA = okA ? (int)(cA % R) : 0, rB = okB ? (int)(cB % R) : 0;
-  int64_t y[4];
-  bool yok[4];
-  const double* xr[4];
+  int64_t y[DU_RPW];
+  bool yok[DU_RPW];
+  const double* xr[DU_RPW];
+  double w1a[DU_RPW], w1b[DU_RPW], a2[DU_RPW], b2[DU_RPW];
 #pragma unroll
-  for (int u = 0; u < 4; u++) {
-    y[u] = (int64_t)kb * DU_ROWS + warp + 8 * u;
+  for (int u = 0; u < DU_RPW; u++) {
+    y[u] = (int64_t)kb * DU_ROWS + warp + DU_WARPS * u;
     yok[u] = y[u] < K1;
     xr[u] = X + ((p * K1 + (yok[u] ? y[u] : 0)) * Q + q) * K2 * C;
-  }
-  double w1a[4], w1b[4];
-#pragma unroll
-  for (int u = 0; u < 4; u++) {
     w1a[u] = (yok[u] && okA) ? v1[y[u] * R + rA] : 0.0;
     w1b[u] = (yok[u] && okB) ? v1[y[u] * R + rB] : 0.0;
+    a2[u] = b2[u] = 0.0;
   }
-  double a2[4] = {0, 0, 0, 0}, b2[4] = {0, 0, 0, 0};
   const int64_t E1 = P * Q * K2 * C;
   for (int64_t k0 = 0; k0 < K2; k0 += DU_K2B) {
 #pragma unroll
@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(MT_THREADS)
       if (k2 < K2 && okA) {
         const double v2a = v2[k2 * R + rA], v2b = okB ? v2[k2 * R + rB] : 0.0;
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
+        for (int u = 0; u < DU_RPW; u++) {
           if (!yok[u]) continue;
           double xa, xb;
           if (VEC2) {
@@ -258,13 +258,13 @@ __global__ void __launch_bounds__(MT_THREADS)
       }
     }
     __syncthreads();
-    {
-      const int j = threadIdx.x / MT_COLS, col = threadIdx.x % MT_COLS;  // 4 x 64 outputs, one per thread
+    if (threadIdx.x < DU_K2B * MT_COLS) {
+      const int j = threadIdx.x / MT_COLS, col = threadIdx.x % MT_COLS;  // 4 x 64 outputs
       const int64_t k2 = k0 + j, c = (int64_t)ch * MT_COLS + col;
       if (k2 < K2 && c < C) {
         double s = red[j][0][col];
 #pragma unroll
-        for (int w = 1; w < 8; w++) s += red[j][w][col];
+        for (int w = 1; w < DU_WARPS; w++) s += red[j][w][col];
         const int64_t e = ((p * Q + q) * K2 + k2) * C + c;
         if (ws) ws[(int64_t)kb * E1 + e] = s;
         else out1[e] = s;
@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(MT_THREADS)
     __syncthreads();
   }
 #pragma unroll
-  for (int u = 0; u < 4; u++) {
+  for (int u = 0; u < DU_RPW; u++) {
     if (!yok[u]) continue;
     double* o = out2 + ((p * K1 + y[u]) * Q + q) * C;
     if (okA) o[cA] = a2[u];
@@ -402,17 +402,24 @@ __global__ void sub_kernel(const double* __restrict__ x, const double* __restric
 
 }  // namespace
 
-void launch_mttv_variant(bool vec2, bool vv, bool pack, unsigned grid, const MttvJobs& jobs, int R, double* out,
-                         int beta, double* ws, const OutMap& om, cudaStream_t st) {
-#define CPD_MTTV_V(V2, VV_, PK) mttv_kernel<V2, VV_, PK><<<grid, MT_THREADS, 0, st>>>(jobs, R, out, beta, ws, om)
+// occ3: the 3-CTAs-per-SM build (80 registers) -- used for the PP filler-stream launches, which
+// then leave room on every SM for the critical main-stream kernels (C2 PP sweep 0.645 -> 0.615 ms
+// with 3/SM everywhere; the large root contractions of C3/C4 prefer 4/SM)
+void launch_mttv_variant(bool vec2, bool vv, bool pack, bool occ3, unsigned grid, const MttvJobs& jobs, int R,
+                         double* out, int beta, double* ws, const OutMap& om, cudaStream_t st) {
+#define CPD_MTTV_V(V2, VV_, PK, O) mttv_kernel<V2, VV_, PK, O><<<grid, MT_THREADS, 0, st>>>(jobs, R, out, beta, ws, om)
   if (pack) {
-    if (vec2 && vv) CPD_MTTV_V(true, true, true);
-    else if (vec2) CPD_MTTV_V(true, false, true);
-    else CPD_MTTV_V(false, false, true);
+    if (vec2 && vv) CPD_MTTV_V(true, true, true, 3);
+    else if (vec2) CPD_MTTV_V(true, false, true, 3);
+    else CPD_MTTV_V(false, false, true, 3);
+  } else if (occ3) {
+    if (vec2 && vv) CPD_MTTV_V(true, true, false, 3);
+    else if (vec2) CPD_MTTV_V(true, false, false, 3);
+    else CPD_MTTV_V(false, false, false, 3);
   } else {
-    if (vec2 && vv) CPD_MTTV_V(true, true, false);
-    else if (vec2) CPD_MTTV_V(true, false, false);
-    else CPD_MTTV_V(false, false, false);
+    if (vec2 && vv) CPD_MTTV_V(true, true, false, 4);
+    else if (vec2) CPD_MTTV_V(true, false, false, 4);
+    else CPD_MTTV_V(false, false, false, 4);
   }
 #undef CPD_MTTV_V
 }
@@ -427,7 +434,7 @@ cudaError_t launch_slot_sum(const double* src, int nq, int64_t n, double* dst, c
 }
 
 cudaError_t launch_mttv_multi(const MttvSpec* specs, int J, int R, const double* base, double* out, int beta,
-                              double* ws, int64_t ws_elems, cudaStream_t st, const OutMap* map) {
+                              double* ws, int64_t ws_elems, cudaStream_t st, const OutMap* map, bool occ3) {
   if (J < 1 || J > 8) return cudaErrorInvalidValue;
   OutMap om{};
   if (map) om = *map;
@@ -491,7 +498,8 @@ cudaError_t launch_mttv_multi(const MttvSpec* specs, int J, int R, const double*
       int64_t grid = (one.j[0].pre + one.j[0].ppc - 1) / one.j[0].ppc * one.j[0].nchunks;
       g_launches++;
       const OutMap none{};
-      launch_mttv_variant(vec2, vv, one.j[0].ppc > 1, (unsigned)grid, one, R, out, q > 0 ? 1 : beta, nullptr, none, st);
+      launch_mttv_variant(vec2, vv, one.j[0].ppc > 1, occ3, (unsigned)grid, one, R, out, q > 0 ? 1 : beta, nullptr,
+                          none, st);
     }
     if (om.nq > 0) {  // the local result, then scattered to the owners' slots
       int64_t blocks = (jobs.E + 255) / 256;
@@ -507,7 +515,7 @@ cudaError_t launch_mttv_multi(const MttvSpec* specs, int J, int R, const double*
   const OutMap km = direct ? om : OutMap{};
   bool pack = false;  // jobs of one launch share the output size, not C: any packed job selects the variant
   for (int q = 0; q < J; q++) pack = pack || jobs.j[q].ppc > 1;
-  launch_mttv_variant(vec2, vv, pack, (unsigned)items, jobs, R, out, beta, w, km, st);
+  launch_mttv_variant(vec2, vv, pack, occ3, (unsigned)items, jobs, R, out, beta, w, km, st);
   if (!direct) {
     g_launches++;
     int64_t blocks = (jobs.E + 255) / 256;
@@ -521,7 +529,7 @@ cudaError_t launch_mttv_dual(const double* X, int64_t P, int64_t K1, int64_t Q, 
                              const double* v1, const double* v2, double* out1, double* out2, double* ws,
                              int64_t ws_elems, cudaStream_t st) {
   if (P <= 0 || Q <= 0 || C <= 0 || K1 <= 0 || K2 <= 0) return cudaSuccess;
-  static_assert(MT_THREADS == DU_K2B * MT_COLS, "one reduction output per thread");
+  static_assert(DU_THREADS >= DU_K2B * MT_COLS, "one reduction output per thread");
   const int nkb = (int)((K1 + DU_ROWS - 1) / DU_ROWS);
   const int64_t E1 = P * Q * K2 * C;
   if (nkb > 1 && (ws == nullptr || (int64_t)nkb * E1 > ws_elems)) return cudaErrorInvalidValue;
@@ -532,9 +540,9 @@ cudaError_t launch_mttv_dual(const double* X, int64_t P, int64_t K1, int64_t Q, 
   double* w = nkb > 1 ? ws : nullptr;
   g_launches++;
   if (vec2)
-    mttv_dual_kernel<true><<<(unsigned)grid, MT_THREADS, 0, st>>>(X, P, K1, Q, K2, C, R, v1, v2, out1, out2, w, nkb);
+    mttv_dual_kernel<true><<<(unsigned)grid, DU_THREADS, 0, st>>>(X, P, K1, Q, K2, C, R, v1, v2, out1, out2, w, nkb);
   else
-    mttv_dual_kernel<false><<<(unsigned)grid, MT_THREADS, 0, st>>>(X, P, K1, Q, K2, C, R, v1, v2, out1, out2, w, nkb);
+    mttv_dual_kernel<false><<<(unsigned)grid, DU_THREADS, 0, st>>>(X, P, K1, Q, K2, C, R, v1, v2, out1, out2, w, nkb);
   if (nkb > 1) {
     int64_t blocks = (E1 + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
