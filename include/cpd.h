@@ -185,9 +185,10 @@ cpd_status cpd_set_factors(cpd_ctx* ctx, const double* const* A_host);
 cpd_status cpd_get_phase_ms(cpd_ctx* ctx, double out[5]);
 
 /* Algorithmic-work ledger since init: out[0]=TTM flops (2*rows*K*R per launch),
- * out[1]=TTM launches, out[2]=mTTV/PP-stream bytes (8*(elements read+written)),
- * out[3]=mTTV/PP-stream launches, out[4]=first-level TTMs (roots) built,
- * out[5]=kernels launched by libcpd.so in this process (all kernels, monotone; not reset). */
+ * out[1]=TTM launches, out[2]=mTTV/PP-stream bytes (8*(elements read+written)) of the launches on
+ * the library's main stream (the ones the mTTV timer brackets; see cpd_get_filler_counters for the
+ * overlapped PP filler-stream launches), out[3]=those launches, out[4]=first-level TTMs (roots)
+ * built, out[5]=kernels launched by libcpd.so in this process (all kernels, monotone; not reset). */
 cpd_status cpd_get_counters(cpd_ctx* ctx, double out[6]);
 
 /* Ledger of the PP operator streams (Eq. 6) issued on the low-priority filler stream (the ones whose
