@@ -534,6 +534,8 @@ __global__ void gamma_dot_kernel(const double* __restrict__ S_all, int N, int R,
 
 // whether mode n's update runs as the single fused cooperative kernel (update.cu)
 bool use_fused(const cpd_ctx* ctx, int n, bool pp) {
+  static const bool off = getenv("CPD_NO_FUSED_UPDATE") != nullptr;  // experiment switch: Cholesky path
+  if (off) return false;
   const int64_t ro = rows_own(ctx, n);
   const int blocks = cpd::update_fused_blocks(ro);
   return ctx->R <= cpd::kUpdMaxR && ctx->Gi[0] &&
