@@ -558,14 +558,16 @@ cpd_status prefetch_solve(cpd_ctx* ctx, int m, bool pp) {
   int* pst = ctx->pf_status + b;
   if (fz) {
     // the fused update multiplies by Γ^{-1}: form it directly (Gauss-Jordan, SPD check)
-    CU(cpd::launch_gamma_inverse(ctx->S_all, ctx->N, m, ctx->R, ctx->Gi[b], pst, ctx->st2));
+    // with W of Eq. 7 in the same launch for PP sweeps
+    CU(cpd::launch_gamma_inverse(ctx->S_all, ctx->N, m, ctx->R, ctx->Gi[b], pst, ctx->st2, pp ? ctx->dS_all : nullptr,
+                                 pp ? ctx->Wb[b] : nullptr));
   } else if (ctx->R > kCholMaxR) {
     // beyond the single-CTA packed Cholesky: Γ^{-1} by the grid-wide blocked Gauss-Jordan
     CU(cpd::launch_gamma_inverse_big(ctx->S_all, ctx->N, m, ctx->R, ctx->ws_gj, ctx->Gi[b], pst, ctx->st2));
   } else {
     CU(cpd::launch_gamma_chol(ctx->S_all, ctx->N, m, ctx->R, ctx->Lp[b], pst, ctx->st2));
   }
-  if (pp) CU(cpd::launch_pp_w(ctx->S_all, ctx->dS_all, ctx->N, m, ctx->R, ctx->Wb[b], ctx->st2));
+  if (pp && !fz) CU(cpd::launch_pp_w(ctx->S_all, ctx->dS_all, ctx->N, m, ctx->R, ctx->Wb[b], ctx->st2));
   CU(cudaEventRecord(ctx->ev_pf, ctx->st2));
   ctx->pf_buf = b;
   ctx->pf_mode = m;

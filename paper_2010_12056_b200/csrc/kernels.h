@@ -118,13 +118,14 @@ cudaError_t launch_gamma_chol(const double* S_all, int N, int n, int R, double* 
                               cudaStream_t st);
 // Γ^(n) (Eq. 1) and Ginv = Γ^{-1} (dense R x R) by Gauss-Jordan without pivoting (SPD);
 // status[0] = 1 if a pivot is not positive (Γ not SPD).  One CTA, R^2 doubles of shared memory.
+// W (optional): also the PP second-order sum W^(n) of Eq. 7 (as launch_pp_w) from S_all, dS_all.
 // R beyond one CTA's shared memory: the blocked Gauss-Jordan over a cooperative grid with Γ in
 // global memory; ws holds gamma_inverse_big_ws(R) doubles
 size_t gamma_inverse_big_ws(int R);
 cudaError_t launch_gamma_inverse_big(const double* S_all, int N, int n, int R, double* ws, double* Ginv,
                                      int* status, cudaStream_t st);
 cudaError_t launch_gamma_inverse(const double* S_all, int N, int n, int R, double* Ginv, int* status,
-                                 cudaStream_t st);
+                                 cudaStream_t st, const double* dS_all = nullptr, double* W = nullptr);
 // Ginv = Γ^{-1} = L^{-T} L^{-1} (dense R x R, exactly symmetric) from the packed factor; one CTA,
 // R(R+1)/2 + R + R^2 doubles of shared memory (R <= kUpdMaxR)
 cudaError_t launch_chol_inverse(const double* Lp, int R, double* Ginv, cudaStream_t st);

@@ -407,7 +407,7 @@ constexpr int kGjB = 16;
 
 __global__ void __launch_bounds__(kGjThreads)
     gamma_inverse_kernel(const double* __restrict__ S_all, int N, int n, int R, double* __restrict__ Ginv,
-                         int* status, int dbg) {
+                         int* status, int dbg, const double* __restrict__ dS_all, double* __restrict__ W) {
   extern __shared__ double gsm[];
   const int Rp = (R + kGjB - 1) / kGjB * kGjB;
   const int LDA = Rp + 1;
@@ -420,6 +420,23 @@ __global__ void __launch_bounds__(kGjThreads)
   const int tid = threadIdx.x;
   const int64_t RR = (int64_t)R * R;
   if (tid == 0) bad = 0;
+  // PP: the second-order Hadamard sum W^(n) of Eq. 7 (pp_w_kernel's arithmetic) in the same launch
+  if (W) {
+    for (int64_t e = tid; e < RR; e += kGjThreads) {
+      double w = 0.0;
+      for (int i = 0; i < N; i++) {
+        if (i == n) continue;
+        for (int j = i + 1; j < N; j++) {
+          if (j == n) continue;
+          double term = dS_all[i * RR + e] * dS_all[j * RR + e];
+          for (int k = 0; k < N; k++)
+            if (k != i && k != j && k != n) term *= S_all[k * RR + e];
+          w += term;
+        }
+      }
+      W[e] = w;
+    }
+  }
 #pragma unroll 4
   for (int e = tid; e < Rp * Rp; e += kGjThreads) {
     const int i = e / Rp, j = e - i * Rp;
@@ -705,7 +722,7 @@ cudaError_t launch_gamma_chol(const double* S_all, int N, int n, int R, double* 
 }
 
 cudaError_t launch_gamma_inverse(const double* S_all, int N, int n, int R, double* Ginv, int* status,
-                                 cudaStream_t st) {
+                                 cudaStream_t st, const double* dS_all, double* W) {
   if (R < 1 || R > 128) return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
@@ -715,7 +732,7 @@ cudaError_t launch_gamma_inverse(const double* S_all, int N, int n, int R, doubl
   }
   g_launches++;
   static const int dbg = getenv("CPD_GJ_DBG") ? atoi(getenv("CPD_GJ_DBG")) : 0;  // profiling switches
-  gamma_inverse_kernel<<<1, kGjThreads, gamma_inverse_smem(R), st>>>(S_all, N, n, R, Ginv, status, dbg);
+  gamma_inverse_kernel<<<1, kGjThreads, gamma_inverse_smem(R), st>>>(S_all, N, n, R, Ginv, status, dbg, dS_all, W);
   return cudaGetLastError();
 }
 
