@@ -405,9 +405,26 @@ __global__ void sub_kernel(const double* __restrict__ x, const double* __restric
 // occ3: the 3-CTAs-per-SM build (80 registers) -- used for the PP filler-stream launches, which
 // then leave room on every SM for the critical main-stream kernels (C2 PP sweep 0.645 -> 0.615 ms
 // with 3/SM everywhere; the large root contractions of C3/C4 prefer 4/SM)
+// experiment switch CPD_MTTV_CARVEOUT: the mTTV kernels prefer the maximum shared-memory carveout, so an
+// SM running them never has to drain to host the large-smem update / Γ^-1 kernels of the other streams
+// (measured: C2 PP sweep 0.62 -> 0.93 ms -- the smaller L1 costs the streams more; off by default)
+template <typename K>
+void carveout(K kern) {
+  static const bool on = getenv("CPD_MTTV_CARVEOUT") != nullptr;
+  if (on) cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+}
+
 void launch_mttv_variant(bool vec2, bool vv, bool pack, bool occ3, unsigned grid, const MttvJobs& jobs, int R,
                          double* out, int beta, double* ws, const OutMap& om, cudaStream_t st) {
-#define CPD_MTTV_V(V2, VV_, PK, O) mttv_kernel<V2, VV_, PK, O><<<grid, MT_THREADS, 0, st>>>(jobs, R, out, beta, ws, om)
+#define CPD_MTTV_V(V2, VV_, PK, O)                                                             \
+  do {                                                                                         \
+    static bool set_ = false;                                                                  \
+    if (!set_) {                                                                               \
+      carveout(mttv_kernel<V2, VV_, PK, O>);                                                   \
+      set_ = true;                                                                             \
+    }                                                                                          \
+    mttv_kernel<V2, VV_, PK, O><<<grid, MT_THREADS, 0, st>>>(jobs, R, out, beta, ws, om);     \
+  } while (0)
   if (pack) {
     if (vec2 && vv) CPD_MTTV_V(true, true, true, 3);
     else if (vec2) CPD_MTTV_V(true, false, true, 3);
