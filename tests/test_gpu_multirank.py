@@ -173,3 +173,22 @@ def test_fused_reduce_scatter_epilogue(cpd, cfg, grid):
         for As, Ar in zip(fused[r]["A"], ref["A"]):
             for a, b in zip(As, Ar):
                 assert np.linalg.norm(a - b) <= TOL * np.linalg.norm(b)
+
+
+def test_grid_validation(cpd):
+    """cpd_opts.grid errors (include/cpd.h): prod(grid) != world, s_n % I_n != 0, or a block not
+    divisible over its slice -> CPD_ERR_INVALID_ARG at cp_als_init (every rank; checked on rank 0 of
+    a local group of 4, where the call fails before any collective)."""
+    g = cpd.cpd_local_group_create(4)
+    cfg = synth.custom(3, 8, 2, seed=38)
+    T = torch.empty(4, 4, 4, dtype=torch.float64, device="cuda")
+    for grid in [(2, 2, 2), (3, 1, 1), (2, 1, 1)]:
+        with pytest.raises(cpd.CPDError) as e:
+            cpd.cp_als_init(T, cfg.shape, cfg.R, synth.init_factors(cfg), rank=0, world=4, local_group=g, grid=grid)
+        assert e.value.status == 1
+    cfg6 = synth.custom(3, 6, 2, seed=39)   # 6 % 4 != 0 for a 1x1x4 grid
+    with pytest.raises(cpd.CPDError) as e:
+        cpd.cp_als_init(T, cfg6.shape, cfg6.R, synth.init_factors(cfg6), rank=0, world=4, local_group=g,
+                        grid=(1, 1, 4))
+    assert e.value.status == 1
+    cpd.cpd_local_group_destroy(g)
