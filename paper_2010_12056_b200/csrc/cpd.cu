@@ -542,6 +542,13 @@ bool use_fused(const cpd_ctx* ctx, int n, bool pp) {
          cpd::update_fused_smem(ctx->R, pp, (int)((ro + blocks - 1) / blocks)) <= 225 * 1024;
 }
 
+// R <= 32 on the fused path: Γ^{-1} (and W) are formed inside the update launch itself by one warp
+// (update.cu gj32_warp), so the side stream does nothing for these modes (CPD_NO_LOCAL_INV: off)
+bool local_inv(const cpd_ctx* ctx) {
+  static const bool off = getenv("CPD_NO_LOCAL_INV") != nullptr;
+  return !off && ctx->R <= 32;
+}
+
 // Γ^(m) = ∗_{k≠m} S^(k) depends only on the Grams, so its Cholesky factorisation (and the
 // PP Hadamard sum W^(m) of Eq. 7) can run on a side stream as soon as the previous update
 // has produced its S, overlapping the latency-bound single-CTA factorisation with the
@@ -556,7 +563,9 @@ cpd_status prefetch_solve(cpd_ctx* ctx, int m, bool pp) {
   // ordered on the main stream and a prefetch for the next sweep never touches this sweep's
   const bool fz = use_fused(ctx, m, pp);
   int* pst = ctx->pf_status + b;
-  if (fz) {
+  if (fz && local_inv(ctx)) {
+    // nothing to prepare: the update launch forms Γ^{-1} (and W) itself
+  } else if (fz) {
     // the fused update multiplies by Γ^{-1}: form it directly (Gauss-Jordan, SPD check)
     // with W of Eq. 7 in the same launch for PP sweeps
     CU(cpd::launch_gamma_inverse(ctx->S_all, ctx->N, m, ctx->R, ctx->Gi[b], pst, ctx->st2, pp ? ctx->dS_all : nullptr,
@@ -628,11 +637,14 @@ cpd_status update_mode(cpd_ctx* ctx, int n, double* Mloc, bool pp, bool scattere
   if (fused) {
     // fused: V term, row solve, dA, statistics, S (and dS) of the own rows in one cooperative launch
     PhaseScope ps(ctx, PH_SOLVE);
+    const bool loc = local_inv(ctx);
     CU(cpd::launch_update_fused(R, ro, ctx->Gi[b], pp ? ctx->Wb[b] : nullptr, Mown, ctx->A[n] + off * R,
                                 pp ? ctx->Ap[n] + off * R : nullptr, ctx->dA[n] + off * R, ctx->S_all + n * RR,
                                 pp ? ctx->dS_all + n * RR : nullptr, ctx->upd_part, ctx->upd_gpart,
                                 ctx->scal + SC_DA2 + n, ctx->scal + SC_A2 + n, last ? ctx->scal + SC_MA : nullptr,
-                                ctx->pf_status + b, ctx->status + n, ctx->st));
+                                loc ? nullptr : ctx->pf_status + b, loc ? nullptr : ctx->status + n, ctx->st,
+                                loc ? ctx->S_all : nullptr, loc ? ctx->dS_all : nullptr, ctx->N, n,
+                                loc ? ctx->status + n : nullptr));
   } else {
     if (pp) {
       // V^(n) = A^(n) W^(n) with the current (pre-update) A^(n): Eq. 7; M~ += V (Eq. 5)

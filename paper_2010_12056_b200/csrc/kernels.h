@@ -153,12 +153,15 @@ cudaError_t launch_update_stats(const double* A, const double* base, double* dA,
 constexpr int kUpdMaxR = 128;  // Γ^{-1} + the packed factor fit one CTA's shared memory
 constexpr int kUpdMaxBlocks = 148;
 // part: 3 * kUpdMaxBlocks doubles; gpart: kUpdMaxBlocks * 2 * R * R doubles (per-CTA Gram partials).
-// st_src/st_dst (optional): *st_dst = *st_src at kernel start (status hand-over between streams)
+// st_src/st_dst (optional): *st_dst = *st_src at kernel start (status hand-over between streams).
+// S_all (R <= 32): Γ^{-1} (and W from S_all, dS_all when W != null -- W then only selects PP) are
+// formed inside the launch from the Grams of mode != nmode; SPD verdict to *st_local.
 size_t update_fused_smem(int R, bool pp, int RB);
 int update_fused_blocks(int64_t rows);
 cudaError_t launch_update_fused(int R, int64_t rows, const double* Ginv, const double* W, double* M, double* A,
                                 const double* base, double* dA, double* S, double* dS, double* part, double* gpart,
                                 double* o_dA2, double* o_A2, double* o_MA, const int* st_src, int* st_dst,
-                                cudaStream_t st);
+                                cudaStream_t st, const double* S_all = nullptr, const double* dS_all = nullptr,
+                                int N = 0, int nmode = 0, int* st_local = nullptr);
 
 }  // namespace cpd

@@ -162,6 +162,7 @@ __global__ void __launch_bounds__(MT_THREADS, PACK ? 3 : OCC)
       const int64_t e = p * C + cv;  // rows p.. of width C are contiguous in the output
       if (ws == nullptr) {
         *map_dst(om, out, e) = beta ? out[e] + s : s;
+        if (om.nq) __threadfence_system();  // fused RS: the store may target a peer GPU (NVLink)
       } else {
         ws[(jb.slot0 + split) * jobs.E + e] = s;
       }
@@ -177,6 +178,7 @@ __global__ void mttv_reduce_kernel(const double* __restrict__ ws, int slots, int
     for (int k = 0; k < slots; k++) s += ws[k * n + e];
     *map_dst(om, out, e) = s;
   }
+  if (om.nq) __threadfence_system();  // fused RS: stores to peers complete before the barrier collective
 }
 
 // Two contractions of one node in one read (PP-init's multi-output descent, SURVEY a9 "deeper levels
@@ -284,6 +286,7 @@ __global__ void __launch_bounds__(DU_THREADS, 2)
 __global__ void scatter_copy_kernel(const double* __restrict__ src, int64_t n, OutMap om) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
     *map_dst(om, nullptr, e) = src[e];
+  __threadfence_system();
 }
 
 __global__ void slot_sum_kernel(const double* __restrict__ src, int nq, int64_t n, double* __restrict__ dst) {

@@ -40,6 +40,27 @@ __device__ __forceinline__ void fill_smem(double* dst, const double* __restrict_
   for (; e < n; e += UPD_THREADS) dst[e] = __ldg(src + e);
 }
 
+// Γ^{-1} of a 32 x 32 SPD matrix held by ONE warp, lane j holding column j (col[i] = Γ[i][j]):
+// Gauss-Jordan without pivoting (every pivot is a Schur-complement diagonal of an SPD matrix,
+// > 0 iff Γ is SPD -> bad), the pivot column broadcast by shuffles; fully unrolled, so the column
+// stays in registers.  Rows / columns beyond R are padded with the identity (pivots 1, untouched).
+__device__ __forceinline__ void gj32_warp(double (&col)[32], int lane, bool& bad) {
+#pragma unroll
+  for (int p = 0; p < 32; p++) {
+    const double piv = __shfl_sync(0xffffffffu, col[p], p);
+    const double inv = __drcp_rn(piv);  // IEEE reciprocal (= 1.0 / piv)
+    if (!(piv > 0.0) || !isfinite(piv)) bad = true;
+    const double r = col[p] * inv;      // new row p, column lane (j != p)
+#pragma unroll
+    for (int i = 0; i < 32; i++) {
+      if (i == p) continue;
+      const double c = __shfl_sync(0xffffffffu, col[i], p);  // old Γ[i][p]
+      col[i] = (lane == p) ? -c * inv : fma(-c, r, col[i]);
+    }
+    col[p] = (lane == p) ? inv : r;
+  }
+}
+
 // out[c] = Σ_k v[k] Mat[k, c] for the row v held by a warp (lane owns v[lane + 32 u]) and the
 // columns c = lane + 32 u: v_k broadcast by one shuffle per k (block u of k is static), two
 // independent FMA chains (even / odd k) summed at the end -- a fixed order
@@ -137,7 +158,9 @@ __global__ void __launch_bounds__(UPD_THREADS)
                         double* __restrict__ dA, double* __restrict__ S, double* __restrict__ dS,
                         double* __restrict__ part, double* __restrict__ gpart, int RB,
                         double* __restrict__ o_dA2, double* __restrict__ o_A2, double* __restrict__ o_MA,
-                        const int* __restrict__ st_src, int* __restrict__ st_dst) {
+                        const int* __restrict__ st_src, int* __restrict__ st_dst,
+                        const double* __restrict__ S_all, const double* __restrict__ dS_all, int N, int nmode,
+                        int* __restrict__ st_local) {
   extern __shared__ double sm[];
   double* G = sm;                 // R x R: Γ^{-1}
   double* Ws = sm + R * R;        // R x R (PP only)
@@ -147,8 +170,56 @@ __global__ void __launch_bounds__(UPD_THREADS)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // the side stream's SPD verdict for this Γ^{-1}, handed to the main stream's status slot
   if (st_dst && blockIdx.x == 0 && tid == 0) *st_dst = *st_src;
-  fill_smem(G, Gi, R * R, tid);
-  if (W) fill_smem(Ws, W, R * R, tid);
+  if constexpr (U != 1) {
+    fill_smem(G, Gi, R * R, tid);
+    if (W) fill_smem(Ws, W, R * R, tid);
+  } else if (S_all) {
+    // R <= 32: Γ^{(n)} = ∗_{k≠n} S^(k) (Eq. 1) and its inverse formed here by warp 0 (gj32_warp),
+    // and for PP W^(n) of Eq. 7 by the other warps -- no side-stream launches on the chain
+    const int64_t RR = (int64_t)R * R;
+    if (warp == 0) {
+      double col[32];
+      bool bad = false;
+#pragma unroll
+      for (int i = 0; i < 32; i++) {
+        double g = (i == lane) ? 1.0 : 0.0;
+        if (i < R && lane < R) {
+          bool first = true;
+          for (int k = 0; k < N; k++) {
+            if (k == nmode) continue;
+            const double sv = S_all[k * RR + i * R + lane];
+            g = first ? sv : g * sv;
+            first = false;
+          }
+        }
+        col[i] = g;
+      }
+      gj32_warp(col, lane, bad);
+#pragma unroll
+      for (int i = 0; i < 32; i++)
+        if (i < R && lane < R) G[i * R + lane] = col[i];
+      const unsigned any_bad = __ballot_sync(0xffffffffu, bad);
+      if (st_local && blockIdx.x == 0 && lane == 0) *st_local = any_bad ? 1 : 0;
+    } else if (W) {
+      for (int64_t e = tid - 32; e < RR; e += UPD_THREADS - 32) {  // pp_w_kernel's arithmetic
+        double w = 0.0;
+        for (int i = 0; i < N; i++) {
+          if (i == nmode) continue;
+          for (int j = i + 1; j < N; j++) {
+            if (j == nmode) continue;
+            double term = dS_all[i * RR + e] * dS_all[j * RR + e];
+            for (int k = 0; k < N; k++)
+              if (k != i && k != j && k != nmode) term *= S_all[k * RR + e];
+            w += term;
+          }
+        }
+        Ws[e] = w;
+      }
+    }
+  } else {
+    fill_smem(G, Gi, R * R, tid);
+    if (W) fill_smem(Ws, W, R * R, tid);
+  }
   __syncthreads();
 
   double s0 = 0.0, s1 = 0.0, s2 = 0.0;
@@ -285,13 +356,17 @@ int update_fused_blocks(int64_t rows) {
 cudaError_t launch_update_fused(int R, int64_t rows, const double* Ginv, const double* W, double* M, double* A,
                                 const double* base, double* dA, double* S, double* dS, double* part, double* gpart,
                                 double* o_dA2, double* o_A2, double* o_MA, const int* st_src, int* st_dst,
-                                cudaStream_t st) {
+                                cudaStream_t st, const double* S_all, const double* dS_all, int N, int nmode,
+                                int* st_local) {
+  if (S_all && R > 32) return cudaErrorInvalidValue;
   if (R > kUpdMaxR || rows <= 0) return cudaErrorInvalidValue;
   const int blocks = update_fused_blocks(rows);
   int RB = (int)((rows + blocks - 1) / blocks);
   const size_t smem = update_fused_smem(R, W != nullptr, RB);
   if (smem > 227 * 1024 - 2048) return cudaErrorInvalidValue;
-  void* args[] = {&R, &rows, &Ginv, &W, &M, &A, &base, &dA, &S, &dS, &part, &gpart, &RB, &o_dA2, &o_A2, &o_MA, &st_src, &st_dst};
+  void* args[] = {&R,     &rows,   &Ginv,   &W,      &M,      &A,    &base,  &dA,    &S,       &dS,
+                  &part,  &gpart,  &RB,     &o_dA2,  &o_A2,   &o_MA, &st_src, &st_dst, &S_all, &dS_all,
+                  &N,     &nmode,  &st_local};
   static const bool split = getenv("CPD_UPD_SPLIT") != nullptr;
   cudaError_t e = cudaErrorInvalidValue;
   switch ((R + 31) / 32) {

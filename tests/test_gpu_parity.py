@@ -634,3 +634,35 @@ def test_pp_back_to_back_speculation(cpd, N, s, R):
     for n in range(N):
         assert rel(m.get_factor(n), A[n]) <= 1e-9, (n, rel(m.get_factor(n), A[n]))
     m.close()
+
+
+def test_c2_full_trajectory(cpd):
+    """C2 (1024^3, R = 64) full-trajectory parity (SURVEY §8(d) run schedule): 4 msdt_sweep on the GPU
+    from the seeded initial factors against 4 exact oracle ALS sweeps (explicit unfolding + explicit
+    KRP + Cholesky) from the same factors on the host copy of the tensor (synth recipe, generated in
+    parallel blocks by bench.host_tensor; ~1e-16 from oracle.make_tensor): fitness at 1e-10 and
+    factors at 1e-9 every sweep (no state synchronisation)."""
+    import bench
+    cfg = synth.config(2)
+    torch.cuda.empty_cache()
+    if torch.cuda.mem_get_info()[0] < 8 * cfg.numel * 2.2:
+        pytest.skip("not enough device memory")
+    T = dev_tensor(cpd, cfg)
+    A0 = synth.init_factors(cfg)
+    m = _model(cpd, cfg, T)
+    f_gpu, A_gpu = [], []
+    for _ in range(4):
+        f_gpu.append(m.msdt_sweep())
+        A_gpu.append([m.get_factor(n) for n in range(cfg.N)])
+    m.close()
+    del T
+    torch.cuda.empty_cache()
+    To = bench.host_tensor(cfg)
+    nt2 = O.norm2(To)
+    A = A0
+    for k in range(4):
+        out = O.als_sweep(To, A, nt2)
+        A = out["A"]
+        assert abs(f_gpu[k] - out["f"]) <= TOL * abs(out["f"]), (k, f_gpu[k], out["f"])
+        for n in range(cfg.N):
+            assert rel(A_gpu[k][n], A[n]) <= 1e-9, (k, n, rel(A_gpu[k][n], A[n]))
