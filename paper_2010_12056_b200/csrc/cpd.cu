@@ -542,11 +542,13 @@ bool use_fused(const cpd_ctx* ctx, int n, bool pp) {
          cpd::update_fused_smem(ctx->R, pp, (int)((ro + blocks - 1) / blocks)) <= 225 * 1024;
 }
 
-// R <= 32 on the fused path: Γ^{-1} (and W) are formed inside the update launch itself by one warp
-// (update.cu gj32_warp), so the side stream does nothing for these modes (CPD_NO_LOCAL_INV: off)
+// experiment switch CPD_LOCAL_INV (R <= 32 on the fused path): Γ^{-1} (and W) formed inside the update
+// launch by one warp of every CTA (update.cu gj32_warp) instead of on the side stream.  Measured slower
+// (C4 PP sweep 0.25 -> 0.46 ms, C1 0.125 -> 0.21 ms: ~1000 dependent shuffles per CTA before any row
+// work), so off by default
 bool local_inv(const cpd_ctx* ctx) {
-  static const bool off = getenv("CPD_NO_LOCAL_INV") != nullptr;
-  return !off && ctx->R <= 32;
+  static const bool on = getenv("CPD_LOCAL_INV") != nullptr;
+  return on && ctx->R <= 32;
 }
 
 // Γ^(m) = ∗_{k≠m} S^(k) depends only on the Grams, so its Cholesky factorisation (and the
