@@ -152,6 +152,9 @@ struct Geo {
   // padded-digit MC tiling (D_MCP): rows (p, mo, m), m < w in blocks of 128
   int64_t w = 0, Mo = 0, ipad = 0;
   int wb = 0;
+  // flattened padded MC tiling (D_MCF): the (Mo, ipad) rows of one prefix are contiguous, so tiles run
+  // over postF = Mo * ipad in steps of 128 (pad positions m >= w are skipped in the epilogue)
+  int64_t postF = 0;
   // digit kernel: CTAs per cluster (1, or 2: a pair takes two N tiles of one M tile and the A box
   // is TMA-multicast to both -- T's digits leave HBM/L2 once per pair)
   int cl = 1;
@@ -690,7 +693,10 @@ cudaError_t dispatch_i8(int L, int grid, const double* X, const Geo& g, const ui
 // (post % 128 == 0, or post == 64 / 32 with 2 / 4 consecutive prefix indices per tile), or
 // D_MCP: MC over padded digit rows (innermost extent w not a multiple of 16, or post % 128 != 0):
 // tiles (p, mo, 128-block of the innermost mode), 5-D map {w, Mo, K, pre, 7}
-enum { D_KC = 0, D_MC128 = 1, D_MC64 = 2, D_MC32 = 3, D_MCP = 4 };
+// D_MCF: MC over padded digit rows with Mo = post / w > 1 and Mo * ipad % 128 == 0: the same boxes as
+// D_MC128 over the flattened (Mo, ipad) extent -- 4 % of pad rows instead of D_MCP's per-row 128-blocks
+// (C3, w = 200, ipad = 208: 208 MMA rows per 200 instead of 256)
+enum { D_KC = 0, D_MC128 = 1, D_MC64 = 2, D_MC32 = 3, D_MCP = 4, D_MCF = 5 };
 constexpr int kStagesD = 5;
 constexpr int kEpiWarps = 16;                        // 4 per TMEM lane quarter
 constexpr int kThreadsD = 32 * (2 + kEpiWarps);
@@ -726,12 +732,18 @@ __device__ __forceinline__ void epilogue_drain(const Geo& g, uint32_t tq, int c_
       const int64_t m = min(mb0, g.ipad - kBM) + r;
       i = pm * g.w + m;
       row_ok = m >= mb0 && m < g.w;
+    } else if constexpr (L == D_MCF) {
+      const int64_t f = mt * kBM + r, p = f / g.postF, fm = f - p * g.postF;
+      const int64_t mo = fm / g.ipad, m = fm - mo * g.ipad;
+      i = p * g.post + mo * g.w + m;
+      row_ok = m < g.w;
     }
     const int n0 = nt * g.Rn;
-    mbar_wait_sleep(tfull0, (uint32_t)tt & 1);
+    if (dbg & 128) mbar_wait(tfull0, (uint32_t)tt & 1);  // profiling switch 128: spin instead of suspend
+    else mbar_wait_sleep(tfull0, (uint32_t)tt & 1);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     double v[NCH][8];
-    if (active) {
+    if (active && !(dbg & 256)) {  // profiling switch 256: release the accumulator without draining it
 #pragma unroll
       for (int ch = 0; ch < NCH; ch++) {
         uint32_t D[kND][8];
@@ -758,7 +770,7 @@ __device__ __forceinline__ void epilogue_drain(const Geo& g, uint32_t tq, int c_
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     mbar_arrive(tempty0);
-    if (!active || (dbg & 32)) continue;
+    if (!active || (dbg & (32 | 256))) continue;
 #pragma unroll
     for (int ch = 0; ch < NCH; ch++) {
       const int c0 = c_lo + 8 * ch;
@@ -794,7 +806,7 @@ __global__ void __launch_bounds__(kThreadsD, 1)
   constexpr int NDS = kStagesD;
   // TMEM accumulator buffers: 7 diagonals x Rp columns each; two (ping-pong) when they fit
   constexpr int NACC = (2 * kND * Rp <= 512 && kND * Rp <= 256) ? 2 : 1;
-  constexpr int MCW = (L == D_MC128 || L == D_MCP) ? 128 : L == D_MC64 ? 64 : 32;  // MN atom bytes
+  constexpr int MCW = (L == D_MC128 || L == D_MCP || L == D_MCF) ? 128 : L == D_MC64 ? 64 : 32;  // MN atom bytes
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NDS * kDStage);
   const uint32_t full0 = su32(bars), empty0 = su32(bars + NDS);
@@ -852,6 +864,9 @@ __global__ void __launch_bounds__(kThreadsD, 1)
           m0 = (int)min((mt - pm * g.wb) * kBM, g.ipad - kBM);  // 16-byte aligned start
           p = (int)(pm / g.Mo);
           mo = (int)(pm - (int64_t)p * g.Mo);
+        } else if constexpr (L == D_MCF) {
+          p = (int)(i0 / g.postF);
+          m0 = (int)(i0 - (int64_t)p * g.postF);
         } else if constexpr (L != D_KC) {
           p = (int)(i0 / g.post);
           m0 = (int)(i0 - (int64_t)p * g.post);
@@ -957,7 +972,8 @@ __global__ void __launch_bounds__(kThreadsD, 1)
       for (int64_t tt = 0; tt < my_tiles; tt++) {
         const int ab = NACC == 2 ? (int)(tt & 1) : 0;
         const uint32_t use = NACC == 2 ? (uint32_t)(tt >> 1) : (uint32_t)tt;  // uses of this buffer so far
-        mbar_wait_sleep(tempty0 + 8 * ab, (use & 1) ^ 1);
+        if (dbg & 128) mbar_wait(tempty0 + 8 * ab, (use & 1) ^ 1);
+        else mbar_wait_sleep(tempty0 + 8 * ab, (use & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t dcol = tmem + ab * 256;
         for (int kc = 0; kc < g.nkc; kc++) {
@@ -1011,11 +1027,17 @@ __global__ void __launch_bounds__(kThreadsD, 1)
         const int64_t m = min(mb0, g.ipad - kBM) + r;    // row held in TMEM lane r
         i = pm * g.w + m;
         row_ok = m >= mb0 && m < g.w;                     // overlap rows belong to the previous block
+      } else if constexpr (L == D_MCF) {
+        const int64_t f = mt * kBM + r, p = f / g.postF, fm = f - p * g.postF;
+        const int64_t mo = fm / g.ipad, m = fm - mo * g.ipad;
+        i = p * g.post + mo * g.w + m;
+        row_ok = m < g.w;                                 // pad positions of the innermost mode
       }
       const int n0 = nt * g.Rn;
       const int ab = NACC == 2 ? (int)(tt & 1) : 0;
       const uint32_t use = NACC == 2 ? (uint32_t)(tt >> 1) : (uint32_t)tt;
-      mbar_wait_sleep(tfull0 + 8 * ab, use & 1);
+      if (dbg & 128) mbar_wait(tfull0 + 8 * ab, use & 1);
+      else mbar_wait_sleep(tfull0 + 8 * ab, use & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t tbase = tmem + ab * 256 + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
@@ -1151,10 +1173,11 @@ bool make_tmap_digits(int L, const DigitView& dv, const Geo& g, CUtensorMap* tm)
       r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
               CU_TENSOR_MAP_SWIZZLE_128B, promo_mc, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     }
-  } else {  // unpadded: post contiguous
-    const int mcw = L == D_MC128 ? 128 : L == D_MC64 ? 64 : 32;
-    cuuint64_t dims[4] = {(cuuint64_t)g.post, (cuuint64_t)g.K, (cuuint64_t)g.pre, (cuuint64_t)kND};
-    cuuint64_t strides[3] = {(cuuint64_t)g.post, (cuuint64_t)g.K * g.post, ps};
+  } else {  // unpadded: post contiguous (D_MCF: the flattened padded extent postF)
+    const int mcw = (L == D_MC128 || L == D_MCF) ? 128 : L == D_MC64 ? 64 : 32;
+    const cuuint64_t pe = (cuuint64_t)(L == D_MCF ? g.postF : g.post);
+    cuuint64_t dims[4] = {pe, (cuuint64_t)g.K, (cuuint64_t)g.pre, (cuuint64_t)kND};
+    cuuint64_t strides[3] = {pe, (cuuint64_t)g.K * pe, ps};
     cuuint32_t box[4] = {(cuuint32_t)mcw, 32, (cuuint32_t)(kBM / mcw), (cuuint32_t)kND}, es[4] = {1, 1, 1, 1};
     const CUtensorMapSwizzle sw =
         mcw == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : mcw == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
@@ -1232,6 +1255,8 @@ int digit_layout(int64_t pre, int64_t K, int64_t post, int64_t w, int64_t ipad) 
     if (post == 64 && pre % 2 == 0) return D_MC64;
     if (post == 32 && pre % 4 == 0) return D_MC32;
   }
+  static const bool no_mcf = getenv("CPD_I8_NO_MCF") != nullptr;  // experiment switch
+  if (!no_mcf && ipad != w && post / w > 1 && ((post / w) * ipad) % kBM == 0) return D_MCF;
   return ipad >= kBM ? D_MCP : -1;  // tiles of 128 rows over the innermost mode (no box overhang)
 }
 
@@ -1264,6 +1289,13 @@ cudaError_t launch_ttm_i8(const double* X, int64_t pre, int64_t K, int64_t post,
       gd.wb = (int)((dv->w + kBM - 1) / kBM);
       gd.nmt = pre * gd.Mo * gd.wb;
       gd.ntiles = gd.nmt * gd.ntn;
+    } else if (Ld == D_MCF) {
+      gd.w = dv->w;
+      gd.ipad = dv->ipad;
+      gd.Mo = post / dv->w;
+      gd.postF = gd.Mo * dv->ipad;
+      gd.nmt = pre * gd.postF / kBM;
+      gd.ntiles = gd.nmt * gd.ntn;
     }
     // N tiles of one M tile on one cluster with the A box multicast (2 or 4 N tiles)
     static const bool no_mc = getenv("CPD_I8_NO_MULTICAST") != nullptr;
@@ -1284,6 +1316,7 @@ cudaError_t launch_ttm_i8(const double* X, int64_t pre, int64_t K, int64_t post,
       case D_MC128: return run_i8d<D_MC128, RP_>(gridd, gd, Bimg, F, Xexp, out, beta, tmd, st);   \
       case D_MC64: return run_i8d<D_MC64, RP_>(gridd, gd, Bimg, F, Xexp, out, beta, tmd, st);     \
       case D_MC32: return run_i8d<D_MC32, RP_>(gridd, gd, Bimg, F, Xexp, out, beta, tmd, st);     \
+      case D_MCF: return run_i8d<D_MCF, RP_>(gridd, gd, Bimg, F, Xexp, out, beta, tmd, st);       \
       default: return run_i8d<D_MCP, RP_>(gridd, gd, Bimg, F, Xexp, out, beta, tmd, st);         \
     }
         CPD_I8D_CASE(16)

@@ -338,7 +338,8 @@ def test_full_size_sampled_rows(cpd, c, ttm_impl):
                                      ((11, 7, 13), 200), ((6, 5, 3), 1), ((200, 3, 130), 33), ((5, 300, 4), 17),
                                      ((64, 64, 64), 64), ((40, 33, 257), 32), ((3, 256, 128), 48), ((130, 48, 256), 64),
                                      ((64, 64, 64), 32), ((12, 48, 32), 16), ((6, 8, 64, 64), 24),
-                                     ((9, 30, 200), 64), ((5, 7, 6, 100), 40), ((3, 130, 72), 20)])
+                                     ((9, 30, 200), 64), ((5, 7, 6, 100), 40), ((3, 130, 72), 20),
+                                     ((4, 8, 200), 20), ((3, 16, 24), 12), ((2, 16, 8, 200), 100)])
 def test_ttm_i8_all_positions(cpd, shape, R, digits):
     """cpd_ttm_i8 (int8 digit slicing on tcgen05) against the oracle's T x_j A at every
     contraction position: ragged M tiles, K tails (odd K, K % 32 != 0), 1-4 N tiles."""
