@@ -38,6 +38,17 @@ def test_sass_uses_fp64_tensor_cores():
     assert "DMMA.8x8x4" in r.stdout
 
 
+def test_sass_uses_tcgen05_and_tma():
+    """The default first-level TTM is Blackwell-native: tcgen05.mma kind::i8 (UTCIMMA), TMEM loads
+    (LDTM), TMA tensor loads (UTMALDG) with cluster multicast, bulk copies (UBLKCP)."""
+    from paper_2010_12056_b200 import build
+    lib = build.build()
+    r = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", lib], capture_output=True, text=True)
+    for ins in ("UTCIMMA", "LDTM", "UTMALDG", "UBLKCP"):
+        assert ins in r.stdout, ins
+    assert re.search(r"UTMALDG\.\w+(\.\w+)*\.MULTICAST", r.stdout) or "MULTICAST" in r.stdout
+
+
 def test_product_never_imports_oracle():
     pkg = os.path.join(ROOT, "paper_2010_12056_b200")
     for dirpath, _, files in os.walk(pkg):
