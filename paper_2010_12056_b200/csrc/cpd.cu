@@ -839,6 +839,11 @@ bool filler_occ3() {
   static const bool occ4 = getenv("CPD_FILLER_OCC4") != nullptr;
   return !occ4;
 }
+// K-split target of the filler-stream launches (experiment switch CPD_FILLER_WAVES; 0 = the default)
+int filler_waves() {
+  static const int w = getenv("CPD_FILLER_WAVES") ? atoi(getenv("CPD_FILLER_WAVES")) : 0;
+  return w;
+}
 
 // the mode of `node` whose contraction keeps the most of `targets`
 int pp_best_mode(const Node& node, const std::vector<std::pair<int, int>>& targets) {
@@ -1587,7 +1592,7 @@ cpd_status pp_approx_sweep(cpd_ctx* ctx, double* fitness_out, int* still_valid) 
     CU(cudaEventRecord(ctx->ev_pp_a, ctx->st));  // update nx-2 (and everything before) enqueued
     CU(cudaStreamWaitEvent(ctx->st3, ctx->ev_pp_a, 0));
     CU(cpd::launch_mttv_multi(sp, J, ctx->R, ctx->Mp[nx], M[nx], 0, ctx->ws_mttv3, kMttvWs, ctx->st3, nullptr,
-                                    filler_occ3()));
+                                    filler_occ3(), filler_waves()));
     CU(cudaEventRecord(ctx->ev_pp_side[nx], ctx->st3));
     ctx->filler[0] += bytes + 8.0 * 2 * ext(ctx, nx) * ctx->R;
     ctx->filler[1] += 1;
@@ -1612,7 +1617,7 @@ cpd_status pp_approx_sweep(cpd_ctx* ctx, double* fitness_out, int* still_valid) 
       CU(cudaEventRecord(ctx->ev_pp_a, ctx->st));
       CU(cudaStreamWaitEvent(ctx->st3, ctx->ev_pp_a, 0));
       CU(cpd::launch_mttv_multi(sp, J, ctx->R, ctx->Mp[0], Mnxt[0], 0, ctx->ws_mttv3, kMttvWs, ctx->st3, nullptr,
-                                    filler_occ3()));
+                                    filler_occ3(), filler_waves()));
       ctx->filler[0] += bytes + 8.0 * 2 * ext(ctx, 0) * ctx->R;
       ctx->filler[1] += 1;
     }
@@ -1660,7 +1665,7 @@ cpd_status pp_approx_sweep(cpd_ctx* ctx, double* fitness_out, int* still_valid) 
       CU(cudaEventRecord(ctx->ev_pp_a, ctx->st));
       CU(cudaStreamWaitEvent(ctx->st3, ctx->ev_pp_a, 0));
       CU(cpd::launch_mttv_multi(sp, 1, ctx->R, nullptr, Mnxt[0], 1, ctx->ws_mttv3, kMttvWs, ctx->st3, nullptr,
-                                    filler_occ3()));
+                                    filler_occ3(), filler_waves()));
       CU(cudaEventRecord(ctx->ev_pp_side[0], ctx->st3));
       ctx->filler[0] += bytes + 8.0 * 2 * ext(ctx, 0) * ctx->R;
       ctx->filler[1] += 1;

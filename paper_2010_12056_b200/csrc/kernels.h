@@ -77,7 +77,7 @@ struct OutMap {
 // occ3: at most 3 resident CTAs per SM (for launches that overlap latency-critical kernels)
 cudaError_t launch_mttv_multi(const MttvSpec* specs, int J, int R, const double* base, double* out, int beta,
                               double* ws, int64_t ws_elems, cudaStream_t st, const OutMap* map = nullptr,
-                              bool occ3 = false);
+                              bool occ3 = false, int waves_override = 0);
 // Two single-mode contractions of one node in one read (PP-init multi-output descent):
 // X viewed as [P][K1][Q][K2][C] (C = trailing extents x R), out1 = contract K1 -> [P][Q][K2][C],
 // out2 = contract K2 -> [P][K1][Q][C]; ws: ceil(K1/32) x |out1| doubles of partials when K1 > 32.

@@ -454,7 +454,8 @@ cudaError_t launch_slot_sum(const double* src, int nq, int64_t n, double* dst, c
 }
 
 cudaError_t launch_mttv_multi(const MttvSpec* specs, int J, int R, const double* base, double* out, int beta,
-                              double* ws, int64_t ws_elems, cudaStream_t st, const OutMap* map, bool occ3) {
+                              double* ws, int64_t ws_elems, cudaStream_t st, const OutMap* map, bool occ3,
+                              int waves_override) {
   if (J < 1 || J > 8) return cudaErrorInvalidValue;
   OutMap om{};
   if (map) om = *map;
@@ -485,7 +486,8 @@ cudaError_t launch_mttv_multi(const MttvSpec* specs, int J, int R, const double*
     // split K so the whole grid is >= ~`waves` waves of 4 resident CTAs per SM; every split adds a
     // partial-sum slot and the reduce pass, so the split stops at 2 waves (8 waves measured slower
     // on the C2 PP operator streams: PP sweep 0.736 -> 0.65 ms with at most 2 splits)
-    static const int waves = getenv("CPD_MTTV_WAVES") ? std::max(1, atoi(getenv("CPD_MTTV_WAVES"))) : 2;
+    static const int waves_env = getenv("CPD_MTTV_WAVES") ? std::max(1, atoi(getenv("CPD_MTTV_WAVES"))) : 2;
+    const int waves = waves_override > 0 ? waves_override : waves_env;
     int64_t ks = (148 * 4 * waves / J + items0 - 1) / items0;
     if (ks > jb.K / 64) ks = jb.K / 64;
     static const int ks_max = getenv("CPD_MTTV_MAXKS") ? atoi(getenv("CPD_MTTV_MAXKS")) : 16;  // experiment switch
