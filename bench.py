@@ -292,6 +292,8 @@ def main():
     ap.add_argument("--ttm-impl", default="auto", choices=["dmma", "int8", "auto"],
                     help="first-level TTM engine: FP64 DMMA, FP64 operands as int8 digits on tcgen05, or the "
                          "library's choice (int8 when its error bound is FP64-class)")
+    ap.add_argument("--msdt-levels", type=int, default=1,
+                    help="upper-level fusion (P:700-702): modes each MSDT root contracts at once (1 = MSDT)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(self_launch(args.gpus))
@@ -329,7 +331,7 @@ def main():
     A0 = synth.init_factors(cfg)
     m = cpd.cp_als_init(T, cfg.shape, cfg.R, A0, device=local, rank=rank, world=world, nccl_id=nccl_id,
                         stream=stream, pp_eps=0.2 if args.config == 4 else 0.1, profile_phases=1,
-                        ttm_impl=TTM_IMPL[args.ttm_impl])
+                        ttm_impl=TTM_IMPL[args.ttm_impl], msdt_levels=args.msdt_levels)
     # untimed: converge until the PP entry condition holds (Alg. 2 line 5), so the forced
     # PP sweeps of each step run in their regime of validity
     pre = 0
@@ -388,6 +390,7 @@ def main():
     ph = m.phase_ms()
     ctr = m.counters()
     fill = m.filler_counters()
+    aux_mem = m.get_memory()
     launches = int(ctr["kernel_launches"] - launches0)
     part_means = parts.mean(axis=0)
     vals = np.array([total_ms, part_means[0] / (N - 1), part_means[1], part_means[2] / (N - 1), part_means[3]])
@@ -472,7 +475,8 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(cfg, world),
             "state": {"presweeps": pre, "pp_condition_held": pp_ok, "fitness_before_steps": f,
-                      "ttm_impl": args.ttm_impl},
+                      "ttm_impl": args.ttm_impl, "msdt_levels": args.msdt_levels,
+                      "aux_memory_bytes": aux_mem},
             "sweeps_ms": {"msdt": msdt_ms, "pp_approx": ppapprox_ms, "pp_init": ppinit_ms, "dt": dt_ms,
                           "dt_over_msdt": dt_ms / msdt_ms, "dt_over_pp_approx": dt_ms / ppapprox_ms},
             "phase_ms_per_step": {k: v / 2 for k, v in ph_all.items()},

@@ -102,6 +102,12 @@ typedef struct {
                                  addressed through ncclGetPeerPointer over NVLink; local group: the
                                  same device), then a stream-ordered barrier and a fixed-order sum of
                                  the received slots.  Needs <= 8 ranks per slice. */
+  int msdt_levels;            /* upper-level fusion: l in [1, N-2] (0 = 1).  Each MSDT
+                                 root contracts a cyclic block of l modes of T at once (one pass over T with
+                                 the Khatri-Rao product of their factors) and serves the next N-l updates, so
+                                 the largest tree node holds s^(N-l) R instead of s^(N-1) R elements, for N/(N-l)
+                                 instead of N/(N-1) passes over T per sweep.  l = 1 is the paper's MSDT.  Affects
+                                 msdt_sweep only (DT and pp_init keep first-level TTMs). */
 } cpd_opts;
 
 #define CPD_TTM_DMMA 0
@@ -190,6 +196,12 @@ cpd_status cpd_get_phase_ms(cpd_ctx* ctx, double out[5]);
  * overlapped PP filler-stream launches), out[3]=those launches, out[4]=first-level TTMs (roots)
  * built, out[5]=kernels launched by libcpd.so in this process (all kernels, monotone; not reset). */
 cpd_status cpd_get_counters(cpd_ctx* ctx, double out[6]);
+
+/* Auxiliary-memory ledger (Table 1's aux-memory column; the upper-level-fusion trade-off,
+ * P:700-702): out[0] = high-water mark of the library's intermediate device buffers (dimension-tree
+ * nodes, PP operators, block Khatri-Rao products) since init or the last cpd_reset_counters, in bytes;
+ * out[1] = bytes live now; out[2] = bytes of T's int8 digit planes (0 unless the digit engine is used). */
+cpd_status cpd_get_memory(cpd_ctx* ctx, double out[3]);
 
 /* Ledger of the PP operator streams (Eq. 6) issued on the low-priority filler stream (the ones whose
  * dA is already final, and the next sweep's speculative ones): out[0] = bytes (8*(elements read +

@@ -26,7 +26,7 @@ __all__ = [
     "unfold", "khatri_rao", "mttkrp", "gram", "gamma", "solve", "norm2", "fitness_eq3",
     "residual_eq2", "kruskal", "make_tensor", "make_tensor_block", "make_tensor_slice", "mttkrp_rows",
     "als_sweep", "PPState", "pp_init", "pp_approx_sweep", "pp_condition", "pp_controller_run",
-    "ttm", "mttv", "MSDTModel", "DTModel", "msdt_roots", "par_als_sweep_sim",
+    "ttm", "block_contract", "mttv", "MSDTModel", "DTModel", "msdt_roots", "par_als_sweep_sim",
     "par_pp_approx_sweep_sim", "dS_of", "pp_first_order", "pp_second_order", "eq3_radicand",
     "RADICAND_TOL", "pp_init_rows", "pp_approx_rows", "grid_procs", "par_als_sweep_grid_sim",
     "par_pp_approx_sweep_grid_sim",
@@ -444,6 +444,20 @@ def ttm(T, A, j):
     return out
 
 
+def block_contract(T, A, C):
+    """Upper-level fusion ("combining several upper level contractions"): T contracted
+    over all modes in C in ONE step, as the generalized unfolding T_(kept, C) (kept modes ascending,
+    then C ascending, last fastest) times the explicit Khatri-Rao product of the factors of C in
+    ascending mode order (first operand slowest, the convention of ``unfold``/``khatri_rao``).
+    Output modes = the kept ones (ascending) + R."""
+    C = sorted(C)
+    kept = [m for m in range(T.ndim) if m not in C]
+    Tm = np.ascontiguousarray(np.transpose(T, kept + C)).reshape(
+        int(np.prod([T.shape[m] for m in kept], dtype=np.int64)), -1)
+    K = khatri_rao([A[c] for c in C])
+    return (Tm @ K).reshape([T.shape[m] for m in kept] + [K.shape[1]])
+
+
 def mttv(X, v, axis):
     """Batched TTV: out[..., r] = Σ_y X[..., y, ..., r] v[y, r]."""
     Xm = np.moveaxis(X, axis, -2)                    # [..., y, r]
@@ -493,27 +507,41 @@ class MSDTModel:
     j = N, N-1, ..., 1 cyclically (1-based; "root of ith subtree is T×_{N-i+1}"),
     serving the N-1 modes (j+1, ..., j+N-1) mod N (0≡N, reading Q4).  In a continuous
     stream of updates t = 0,1,..., mode(t) = t mod N and root k serves t in
-    [k(N-1), (k+1)(N-1)).  Counts first-level TTMs (pin: N per N-1 sweeps)."""
+    [k(N-1), (k+1)(N-1)).  Counts first-level TTMs (pin: N per N-1 sweeps).
 
-    def __init__(self, T):
+    ``levels`` = l (upper-level fusion, P:700-702, 1 <= l <= N-2): root k contracts the l modes
+    that follow its served block cyclically in ONE step (``block_contract``) and serves the
+    N-l updates [k(N-l), (k+1)(N-l)), modes f, .., f+N-l-1 (mod N) with f = k(N-l) mod N;
+    l = 1 is the schedule above (f + N-1 = j).  N roots per N-l sweeps."""
+
+    def __init__(self, T, levels=1):
         self.T = T
         self.N = T.ndim
+        if not 1 <= levels <= max(1, self.N - 2):
+            raise ValueError("levels must be in [1, N-2]")
+        self.l = levels
         self.t = 0
         self.runner = None
         self.n_ttm = 0
-        self.trace = []      # (root contracted mode j (0-based), served list)
+        self.trace = []      # (root contracted mode j (0-based) or the block C, served list)
 
     def next_mttkrp(self, A):
-        N = self.N
-        k, q = divmod(self.t, N - 1)
+        N, l = self.N, self.l
+        k, q = divmod(self.t, N - l)
         if q == 0:
-            j = ((k + 1) * (N - 1)) % N                   # 0-based contracted mode of root k
-            served = [(j + d) % N for d in range(1, N)]
-            root = ttm(self.T, A[j], j)
+            f = (k * (N - l)) % N
+            served = [(f + d) % N for d in range(N - l)]
+            C = [(f + d) % N for d in range(N - l, N)]
+            if l == 1:
+                j = C[0]                                  # = ((k + 1)(N - 1)) mod N
+                root = ttm(self.T, A[j], j)
+                self.trace.append((j, served))
+            else:
+                root = block_contract(self.T, A, C)
+                self.trace.append((tuple(C), served))
             self.n_ttm += 1
-            kept = [m for m in range(N) if m != j]
+            kept = [m for m in range(N) if m not in C]
             self.runner = _SubtreeRunner(root, kept, served)
-            self.trace.append((j, served))
         n = self.t % N
         node, kept = self.runner.leaf(q, A)
         assert kept == [n] and self.runner.served[q] == n

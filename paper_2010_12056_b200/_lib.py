@@ -21,7 +21,7 @@ EXPORTED_SYMBOLS = [
     "cpd_set_factors", "cpd_get_phase_ms", "cpd_get_counters", "cpd_reset_counters",
     "cpd_debug_get_pp_operator", "cpd_last_error", "cpd_destroy", "cpd_gen_tensor", "cpd_ttm", "cpd_ttm_i8", "cpd_ttm_engine", "cpd_set_tensor",
     "cpd_last_sweep_status",
-    "cpd_mttv", "cpd_gen_tensor_block", "cpd_get_filler_counters", "cpd_local_group_create", "cpd_local_group_destroy", "cpd_set_profile_level",
+    "cpd_mttv", "cpd_gen_tensor_block", "cpd_get_filler_counters", "cpd_get_memory", "cpd_local_group_create", "cpd_local_group_destroy", "cpd_set_profile_level",
 ]
 
 
@@ -36,7 +36,7 @@ class cpd_opts(C.Structure):
                 ("nccl_unique_id", C.c_void_p), ("stream", C.c_void_p), ("pp_eps", C.c_double),
                 ("reuse_root_in_pp_init", C.c_int), ("profile_phases", C.c_int), ("local_group", C.c_void_p),
                 ("ttm_impl", C.c_int), ("grid", C.c_int * CPD_MAX_ORDER),
-                ("fused_rs", C.c_int)]
+                ("fused_rs", C.c_int), ("msdt_levels", C.c_int)]
 
 
 _lib = None
@@ -70,6 +70,7 @@ def load_library():
         "cpd_get_counters": (C.c_int, [_P, _D]),
         "cpd_reset_counters": (C.c_int, [_P]),
         "cpd_get_filler_counters": (C.c_int, [_P, _D]),
+        "cpd_get_memory": (C.c_int, [_P, _D]),
         "cpd_set_profile_level": (C.c_int, [_P, C.c_int]),
         "cpd_debug_get_pp_operator": (C.c_int, [_P, C.c_int, C.c_int, _D]),
         "cpd_last_error": (C.c_char_p, [_P]),

@@ -53,7 +53,7 @@ struct Node {
 };
 
 struct Subtree {
-  int j = -1;                              // contracted mode of the root
+  int j = -1;                              // contracted mode of the root (-1: a block of modes)
   std::vector<int> served;                 // service order
   std::map<std::pair<int, int>, Node> cache;
   bool active = false;
@@ -173,6 +173,11 @@ struct cpd_ctx {
   uint8_t* Td = nullptr;     // T's 7 int8 digit planes (computed once; null -> convert T per TTM)
   size_t ws_i8_bytes = 0;
   int engine = CPD_ENGINE_DMMA;  // first-level TTM engine chosen at init
+  // upper-level fusion (opts.msdt_levels): each MSDT root contracts lv modes at once
+  int lv = 1;
+  // auxiliary memory ledger (cpd_get_memory): bytes of live dalloc blocks (tree nodes, PP operators,
+  // block-contraction Khatri-Rao products) and their high-water mark since init / reset
+  double node_live = 0.0, node_peak = 0.0;
 };
 
 // scalar slots
@@ -302,6 +307,8 @@ cpd_status dalloc(cpd_ctx* ctx, double** p, int64_t elems) {
   if (it != ctx->node_cache.end()) {
     *p = (double*)it->second;
     ctx->node_cache.erase(it);
+    ctx->node_live += (double)bytes;
+    ctx->node_peak = std::max(ctx->node_peak, ctx->node_live);
     return CPD_OK;  // node_bytes[*p] already recorded
   }
   static const bool dbg = getenv("CPD_DEBUG_ALLOC") != nullptr;
@@ -316,6 +323,8 @@ cpd_status dalloc(cpd_ctx* ctx, double** p, int64_t elems) {
   }
   CU(e);
   ctx->node_bytes[(void*)*p] = bytes;
+  ctx->node_live += (double)bytes;
+  ctx->node_peak = std::max(ctx->node_peak, ctx->node_live);
   if (dbg) {
     double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     if (ms > 0.5) fprintf(stderr, "[cpd] cudaMallocAsync %.3f GB took %.2f ms\n", 1e-9 * bytes, ms);
@@ -326,7 +335,11 @@ cpd_status dalloc(cpd_ctx* ctx, double** p, int64_t elems) {
 cudaError_t palloc(cpd_ctx* c, void** p, size_t bytes) { return cudaMallocFromPoolAsync(p, bytes, c->pool, c->st); }
 
 void dfree(cpd_ctx* c, double*& p) {
-  if (p) c->node_cache.emplace(c->node_bytes[(void*)p], (void*)p);
+  if (p) {
+    const size_t b = c->node_bytes[(void*)p];
+    c->node_cache.emplace(b, (void*)p);
+    c->node_live -= (double)b;
+  }
   p = nullptr;
 }
 
@@ -376,6 +389,137 @@ cpd_status mttv(cpd_ctx* ctx, const double* X, const std::vector<int>& kept, int
   return CPD_OK;
 }
 
+// Upper-level fusion ("combining several upper level contractions"): T contracted with the
+// Khatri-Rao product of the factors of a cyclic block C of lv modes in ONE pass over T, giving the node
+// that keeps the other modes (s^(N-lv) R elements instead of the s^(N-1) R of a first-level TTM).
+// C is [c0, c0+lv) or, wrapping, [0, b) + [N-a, N) (a + b = lv).  int8 digit engine: one GEMM whose K
+// index is (prefix p, padded suffix q) over the digit planes (launch_ttm_i8_block; a middle block is a
+// plain TTM with the KRP as factor); DMMA engine: the FP64 TTM with the KRP as factor, a wrapping
+// block as a TTM over the suffix then an mTTV over the prefix.
+cpd_status ttm_block(cpd_ctx* ctx, const std::vector<int>& Cin, double* out) {
+  const int N = ctx->N, R = ctx->R, l = (int)Cin.size();
+  if (l == 1) return ttm(ctx, Cin[0], out);
+  std::vector<int> C(Cin);
+  std::sort(C.begin(), C.end());
+  const bool contiguous = C.back() - C.front() == l - 1;
+  if (!contiguous && (C.front() != 0 || C.back() != N - 1)) return fail(ctx, CPD_ERR_INTERNAL, "ttm_block: not a cyclic block");
+  // wrapping: prefix [0, b), suffix [s0, N); contiguous: block [c0, c0 + l)
+  int b = 0, s0 = C.front();
+  if (!contiguous) {
+    while (b < l && C[b] == b) b++;
+    s0 = C[b];
+  }
+  auto prodx = [&](int lo, int hi) {
+    int64_t p = 1;
+    for (int m = lo; m < hi; m++) p *= ext(ctx, m);
+    return p;
+  };
+  PhaseScope ps(ctx, PH_TTM);
+  const double flops = 2.0 * (double)prodx(0, N) * R;
+  auto account = [&]() {
+    ctx->counters[0] += flops;
+    ctx->counters[1] += 1;
+    ctx->counters[4] += 1;
+    return CPD_OK;
+  };
+  auto krp = [&](const std::vector<int>& modes, const std::vector<int64_t>& stride, double* dst, int64_t rows,
+                 bool pad) -> cudaError_t {
+    cpd::KrpSpec sp{};
+    sp.n = (int)modes.size();
+    for (int c = 0; c < sp.n; c++) {
+      sp.A[c] = ctx->A[modes[c]];
+      sp.ext[c] = ext(ctx, modes[c]);
+      sp.stride[c] = stride[c];
+    }
+    return cpd::launch_krp_block(sp, R, dst, rows, pad, ctx->st);
+  };
+  // row-major strides of a plain KRP over consecutive modes
+  auto plain = [&](const std::vector<int>& modes) {
+    std::vector<int64_t> st(modes.size());
+    int64_t acc = 1;
+    for (int c = (int)modes.size() - 1; c >= 0; c--) {
+      st[c] = acc;
+      acc *= ext(ctx, modes[c]);
+    }
+    return st;
+  };
+  const bool tail = !contiguous || C.back() == N - 1;  // the block holds the innermost mode
+  if (ctx->engine == CPD_ENGINE_INT8_DIGITS) {
+    cpd::DigitView dv;
+    dv.planes = ctx->Td;
+    dv.w = ext(ctx, N - 1);
+    dv.ipad = cpd::digit_inner_pad(dv.w);
+    dv.plane_stride = cpd::digit_plane_bytes(ctx->T_elems, dv.w);
+    if (tail) {
+      // K = (p, q): the prefix modes [0, b) slowest, then the suffix [s0, N) with the innermost padded
+      const int64_t P = prodx(0, b), Mrows = prodx(b, s0), Qp = prodx(s0, N - 1) * dv.ipad;
+      const int64_t Ks = (Qp + 31) / 32 * 32;
+      std::vector<int> modes;
+      std::vector<int64_t> stride;
+      for (int m = 0; m < b; m++) modes.push_back(m);
+      for (int m = s0; m < N; m++) modes.push_back(m);
+      stride.assign(modes.size(), 0);
+      int64_t acc = 1;
+      for (int c = (int)modes.size() - 1; c >= 0; c--) {
+        const int m = modes[c];
+        if (m == b - 1) acc = Ks;  // the last prefix mode steps over one padded suffix slab
+        stride[c] = acc;
+        acc *= (m == N - 1) ? dv.ipad : ext(ctx, m);
+      }
+      double* kb = nullptr;
+      TRY(dalloc(ctx, &kb, P * Ks * R));
+      CU(krp(modes, stride, kb, P * Ks, true));
+      cudaError_t e = cpd::launch_ttm_i8_block(P, Mrows, Qp, kb, R, out, 0, ctx->texp, ctx->ws_i8,
+                                               ctx->ws_i8_bytes, ctx->st, dv);
+      dfree(ctx, kb);
+      if (e == cudaSuccess) return account();
+      if (e != cudaErrorNotSupported) CU(e);
+      cudaGetLastError();
+    } else {
+      const int64_t pre = prodx(0, C.front()), K = prodx(C.front(), C.back() + 1), post = prodx(C.back() + 1, N);
+      double* kb = nullptr;
+      TRY(dalloc(ctx, &kb, K * R));
+      CU(krp(C, plain(C), kb, K, false));
+      cudaError_t e = cpd::launch_ttm_i8(ctx->T, pre, K, post, kb, R, out, 0, ctx->texp, ctx->ws_i8,
+                                         ctx->ws_i8_bytes, ctx->st, &dv);
+      dfree(ctx, kb);
+      if (e == cudaSuccess) return account();
+      cudaGetLastError();  // no digit layout for this view and K too long for the converting kernel
+    }
+  }
+  if (contiguous) {
+    const int64_t pre = prodx(0, C.front()), K = prodx(C.front(), C.back() + 1), post = prodx(C.back() + 1, N);
+    double* kb = nullptr;
+    TRY(dalloc(ctx, &kb, K * R));
+    CU(krp(C, plain(C), kb, K, false));
+    if (ctx->engine != CPD_ENGINE_DMMA && K <= cpd::kMaxKI8)
+      CU(cpd::launch_ttm_i8(ctx->T, pre, K, post, kb, R, out, 0, ctx->texp, ctx->ws_i8, ctx->ws_i8_bytes, ctx->st,
+                            nullptr));
+    else
+      CU(cpd::launch_ttm(ctx->T, pre, K, post, kb, R, out, 0, ctx->st));
+    dfree(ctx, kb);
+    return account();
+  }
+  // wrapping block on the FP64 engine: X[p, m, r] = T x_suffix KRP(suffix), then out = X x_p KRP(prefix)
+  std::vector<int> pm, sm;
+  for (int m = 0; m < b; m++) pm.push_back(m);
+  for (int m = s0; m < N; m++) sm.push_back(m);
+  const int64_t P = prodx(0, b), Mrows = prodx(b, s0), Q = prodx(s0, N);
+  double *ks = nullptr, *kp = nullptr, *X = nullptr;
+  TRY(dalloc(ctx, &ks, Q * R));
+  TRY(dalloc(ctx, &kp, P * R));
+  TRY(dalloc(ctx, &X, P * Mrows * R));
+  CU(krp(sm, plain(sm), ks, Q, false));
+  CU(krp(pm, plain(pm), kp, P, false));
+  CU(cpd::launch_ttm(ctx->T, P * Mrows, Q, 1, ks, R, X, 0, ctx->st));
+  cpd::MttvSpec sp{X, kp, 1, P, Mrows};
+  CU(cpd::launch_mttv_multi(&sp, 1, R, nullptr, out, 0, ctx->ws_mttv, kMttvWs, ctx->st));
+  dfree(ctx, X);
+  dfree(ctx, kp);
+  dfree(ctx, ks);
+  return account();
+}
+
 // contract the modes `drop` of a node in `order`, returning a new node (input not freed)
 // `map` (fused reduce-scatter): the contraction that produces the final node stores it into the
 // owners' receive slots instead (the node buffer is then left unwritten)
@@ -411,14 +555,17 @@ void clear_subtree(cpd_ctx* c) {
   c->sub.j = -1;
 }
 
-// start a subtree: root T x_j, then contract `pre` (in order), served list
-cpd_status start_subtree(cpd_ctx* ctx, int j, const std::vector<int>& pre, const std::vector<int>& served) {
+// start a subtree: root T x_C (one mode, or a block of modes with upper-level fusion), then contract
+// `pre` (in order), served list
+cpd_status start_subtree(cpd_ctx* ctx, const std::vector<int>& C, const std::vector<int>& pre,
+                         const std::vector<int>& served) {
   clear_subtree(ctx);
   Node root;
   for (int m = 0; m < ctx->N; m++)
-    if (m != j) root.kept.push_back(m);
+    if (std::find(C.begin(), C.end(), m) == C.end()) root.kept.push_back(m);
   TRY(dalloc(ctx, &root.buf, node_elems(ctx, root.kept)));
-  TRY(ttm(ctx, j, root.buf));
+  TRY(ttm_block(ctx, C, root.buf));
+  const int j = C.size() == 1 ? C[0] : -1;
   if (!pre.empty()) {
     Node nx;
     TRY(contract_modes(ctx, root, pre, pre, &nx));
@@ -785,14 +932,19 @@ cpd_status regular_sweep(cpd_ctx* ctx, bool msdt, double* f_out) {
   ctx->pp_regime = false;
   if (msdt) {
     ctx->sub_is_msdt = true;
+    // root k serves the S = N - lv updates [kS, (k+1)S) (modes f, .., f+S-1 mod N, f = kS mod N) and
+    // contracts the lv modes that follow them cyclically (not updated while it is in use); lv = 1:
+    // j = ((k+1)(N-1)) mod N, T x_N, T x_{N-1}, ... (R4)
+    const int S = N - ctx->lv;
     for (int n = 0; n < N; n++) {
-      int64_t k = ctx->t / (N - 1);
-      int q = (int)(ctx->t % (N - 1));
+      int64_t k = ctx->t / S;
+      int q = (int)(ctx->t % S);
       if (q == 0 || !ctx->sub.active) {
-        int j = (int)(((k + 1) * (N - 1)) % N);
-        std::vector<int> served;
-        for (int d = 1; d < N; d++) served.push_back((j + d) % N);
-        TRY(start_subtree(ctx, j, {}, served));
+        const int f = (int)((k * S) % N);
+        std::vector<int> served, C;
+        for (int d = 0; d < S; d++) served.push_back((f + d) % N);
+        for (int d = S; d < N; d++) C.push_back((f + d) % N);
+        TRY(start_subtree(ctx, C, {}, served));
       }
       if (ctx->sub.served[q] != n) return fail(ctx, CPD_ERR_INTERNAL, "MSDT schedule out of phase");
       const double* leaf;
@@ -812,12 +964,12 @@ cpd_status regular_sweep(cpd_ctx* ctx, bool msdt, double* f_out) {
         std::vector<int> pre, served;
         for (int m = h; m < N - 1; m++) pre.push_back(m);
         for (int m = 0; m < h; m++) served.push_back(m);
-        TRY(start_subtree(ctx, N - 1, pre, served));
+        TRY(start_subtree(ctx, {N - 1}, pre, served));
       } else if (n == h) {
         std::vector<int> pre, served;
         for (int m = 1; m < h; m++) pre.push_back(m);
         for (int m = h; m < N; m++) served.push_back(m);
-        TRY(start_subtree(ctx, 0, pre, served));
+        TRY(start_subtree(ctx, {0}, pre, served));
       }
       int q = n < h ? n : n - h;
       const double* leaf;
@@ -983,6 +1135,8 @@ cpd_status prepare_tensor(cpd_ctx* ctx) {
       for (int n = 0; n < N; n++) kmax = std::max(kmax, ext(ctx, n));
       // the workspace depends only on the shape and R, so a later cpd_set_tensor reuses it
       if (!ctx->ws_i8) {
+        // block contractions (upper-level fusion) run K chunks of up to kMaxKI8 rows
+        if (ctx->lv > 1) kmax = cpd::kMaxKI8;
         ctx->ws_i8_bytes = cpd::ttm_i8_workspace_bytes(std::min(kmax, cpd::kMaxKI8), R);
         CU(palloc(ctx, &ctx->ws_i8, ctx->ws_i8_bytes));
       }
@@ -1143,6 +1297,9 @@ cpd_status cp_als_init(cpd_ctx** out, int N, const int64_t* shape, int R, const 
   if (o.world < 1 || o.rank < 0 || o.rank >= o.world) return fail(ctx, CPD_ERR_INVALID_ARG, "bad rank/world");
   if (o.ttm_impl != CPD_TTM_DMMA && o.ttm_impl != CPD_TTM_INT8 && o.ttm_impl != CPD_TTM_AUTO)
     return fail(ctx, CPD_ERR_INVALID_ARG, "bad ttm_impl");
+  if (o.msdt_levels == 0) o.msdt_levels = 1;
+  if (o.msdt_levels < 1 || o.msdt_levels > N - 2)
+    return fail(ctx, CPD_ERR_INVALID_ARG, "msdt_levels must be in [1, N-2] (P:700-702: l <= N-2)");
   if (o.world > 1 && !o.nccl_unique_id && !o.local_group)
     return fail(ctx, CPD_ERR_INVALID_ARG, "world > 1 needs nccl_unique_id or local_group");
   if (o.local_group && cpd::local_group_world((cpd::LocalGroup*)o.local_group) != o.world)
@@ -1173,6 +1330,7 @@ cpd_status cp_als_init(cpd_ctx** out, int N, const int64_t* shape, int R, const 
 
   ctx = new cpd_ctx();
   ctx->N = N;
+  ctx->lv = o.msdt_levels;
   ctx->R = R;
   for (int n = 0; n < N; n++) ctx->shape[n] = shape[n];
   ctx->rank = o.rank;
@@ -1765,6 +1923,14 @@ cpd_status cpd_get_counters(cpd_ctx* ctx, double out[6]) {
   return CPD_OK;
 }
 
+cpd_status cpd_get_memory(cpd_ctx* ctx, double out[3]) {
+  if (!ctx || !out) return CPD_ERR_INVALID_ARG;
+  out[0] = ctx->node_peak;
+  out[1] = ctx->node_live;
+  out[2] = ctx->Td ? 7.0 * (double)cpd::digit_plane_bytes(ctx->T_elems, ext(ctx, ctx->N - 1)) : 0.0;
+  return CPD_OK;
+}
+
 cpd_status cpd_get_filler_counters(cpd_ctx* ctx, double out[2]) {
   if (!ctx || !out) return CPD_ERR_INVALID_ARG;
   out[0] = ctx->filler[0];
@@ -1788,6 +1954,7 @@ cpd_status cpd_reset_counters(cpd_ctx* ctx) {
   drain_timers(ctx, true);
   for (int i = 0; i < 5; i++) ctx->phase_ms[i] = ctx->counters[i] = 0.0;
   ctx->filler[0] = ctx->filler[1] = 0.0;
+  ctx->node_peak = ctx->node_live;
   return CPD_OK;
 }
 

@@ -21,8 +21,9 @@ cudaError_t launch_ttm(const double* X, int64_t pre, int64_t K, int64_t post, co
 
 // ---- the same first-level TTM on the INT8 tensor cores (tcgen05 kind::i8, exact integer
 // slicing of both FP64 operands; ttm_i8.cu).  Xexp: device int with 2^Xexp > max|X|
-// (launch_absmax_exp); ws: ttm_i8_workspace_bytes(K, ncols) bytes (sliced B + exponents).
-// K <= kMaxKI8 (int32 accumulators), ncols <= 1024.
+// (launch_absmax_exp); ws: ttm_i8_workspace_bytes(min(K, kMaxKI8), ncols) bytes (sliced B + exponents).
+// K <= kMaxKI8 (int32 accumulators) per launch: longer K only on the digit planes, as chunks accumulated
+// with beta = 1; ncols <= 1024.
 constexpr int64_t kMaxKI8 = 16384;
 size_t ttm_i8_workspace_bytes(int64_t K, int ncols);
 // X's 7 int8 digit planes (launch_slice_digits): X viewed as [n / w, w] (w = innermost extent),
@@ -40,6 +41,25 @@ inline int64_t digit_inner_pad(int64_t w) {
 cudaError_t launch_ttm_i8(const double* X, int64_t pre, int64_t K, int64_t post, const double* B, int ncols,
                           double* out, int beta, const int* Xexp, void* ws, size_t ws_bytes, cudaStream_t st,
                           const DigitView* dv = nullptr);
+// Contraction of T with a Khatri-Rao product over a block of modes (upper-level fusion) on the
+// digit planes, as ONE GEMM whose K index is (slab p, q): the digit view is [P][Mrows][Qp] (Qp bytes per row,
+// a multiple of 16: the flattened, innermost-padded suffix of the block; P = the flattened prefix of a
+// block that wraps around from mode N to mode 1, else 1), Bpad is [P][32*ceil(Qp/32)][ncols] with zero
+// rows at pad positions (launch_krp_block).  out (Mrows x ncols) = beta*out + Σ_{p,q} digits(p,i,q) Bpad.
+// Launches of <= kMaxKI8 K rows accumulate with beta = 1.  cudaErrorNotSupported: layout not served.
+// ws: ttm_i8_workspace_bytes(kMaxKI8, ncols) bytes.
+cudaError_t launch_ttm_i8_block(int64_t P, int64_t Mrows, int64_t Qp, const double* Bpad, int ncols, double* out,
+                                int beta, const int* Xexp, void* ws, size_t ws_bytes, cudaStream_t st,
+                                const DigitView& dv);
+// Khatri-Rao product of the factors of a block of modes, scattered into a zero-padded row layout:
+// out[(Σ_c y_c stride_c) * R + r] = Π_c A_c[y_c * R + r] for y_c < ext_c (the first mode slowest in the
+// enumeration; the row strides place it).  rows_total: rows of out (zeroed first when `pad`).
+struct KrpSpec {
+  int n;
+  const double* A[8];
+  int64_t ext[8], stride[8];
+};
+cudaError_t launch_krp_block(const KrpSpec& sp, int R, double* out, int64_t rows_total, bool pad, cudaStream_t st);
 // bytes between digit planes (a multiple of 64); the planes buffer holds 7 * digit_plane_bytes(n, w)
 inline int64_t digit_plane_stride(int64_t n) { return (n + 63) / 64 * 64; }
 inline int64_t digit_plane_bytes(int64_t n, int64_t w) { return digit_plane_stride(n / w * digit_inner_pad(w)); }

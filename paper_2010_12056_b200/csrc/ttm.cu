@@ -318,4 +318,36 @@ cudaError_t launch_ttm(const double* X, int64_t pre, int64_t K, int64_t post, co
   return cudaErrorInvalidValue;
 }
 
+
+namespace {
+__global__ void krp_block_kernel(KrpSpec sp, int R, double* __restrict__ out, int64_t total) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e % R);
+    int64_t rest = e / R, row = 0;
+    double v = 1.0;
+    for (int c = sp.n - 1; c >= 0; c--) {  // last mode fastest
+      const int64_t y = rest % sp.ext[c];
+      rest /= sp.ext[c];
+      row += y * sp.stride[c];
+      v *= sp.A[c][y * R + r];
+    }
+    out[row * R + r] = v;
+  }
+}
+}  // namespace
+
+cudaError_t launch_krp_block(const KrpSpec& sp, int R, double* out, int64_t rows_total, bool pad, cudaStream_t st) {
+  if (sp.n < 1 || sp.n > 8 || R < 1) return cudaErrorInvalidValue;
+  int64_t total = R;
+  for (int c = 0; c < sp.n; c++) total *= sp.ext[c];
+  if (pad) {
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double) * (size_t)rows_total * R, st);
+    if (e != cudaSuccess) return e;
+  }
+  g_launches++;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  krp_block_kernel<<<blocks, 256, 0, st>>>(sp, R, out, total);
+  return cudaGetLastError();
+}
+
 }  // namespace cpd

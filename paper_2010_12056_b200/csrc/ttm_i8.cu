@@ -147,6 +147,7 @@ __device__ __forceinline__ double pow2(int e) {  // 2^e for normal range
 struct Geo {
   int64_t pre, K, post, Mrows;
   int ncols, Rn, Rp, ntn;   // columns, columns per N tile, padded, number of N tiles
+  int bstride;              // bytes of one (N tile, K32 step) block of the B digit image
   int64_t nmt, ntiles;      // M tiles, total tiles
   int nkc;                  // K32 steps
   // padded-digit MC tiling (D_MCP): rows (p, mo, m), m < w in blocks of 128
@@ -158,6 +159,13 @@ struct Geo {
   // digit kernel: CTAs per cluster (1, or 2: a pair takes two N tiles of one M tile and the A box
   // is TMA-multicast to both -- T's digits leave HBM/L2 once per pair)
   int cl = 1;
+  // K chunks (a contraction longer than kMaxKI8 runs as several launches accumulating with beta = 1):
+  // kofs = first K index of this launch (added to the K coordinate of every box), Kfull = K extent of
+  // the tensor map (0: K).  D_KCW (block contraction, upper-level fusion): the digit view is
+  // [P2 slabs][Mrows][Qp bytes] and K step kc reads slab p0 + kc / nkq at offset kofs + 32 (kc % nkq)
+  int64_t kofs = 0, Kfull = 0;
+  int nkq = 0;
+  int64_t p0 = 0, P2 = 1, Qp = 0;
 };
 
 // tile tt of this CTA (digit kernel) -> M tile, N tile
@@ -547,10 +555,18 @@ __global__ void b_image_kernel(const double* __restrict__ B, int64_t K, Geo g, c
       const double x = B[k * g.ncols + c] * pow2(54 - F[c]);
       u = (unsigned long long)(__double2ll_rn(x) + (long long)kBias);
     }
-    uint8_t* base = img + (((int64_t)nt * g.nkc + kc) * kND) * (g.Rp * 32);
+    uint8_t* base = img + ((int64_t)nt * g.nkc + kc) * g.bstride;
     const int off = (r >> 3) * 256 + (kb >> 4) * 128 + (r & 7) * 16 + (kb & 15);
 #pragma unroll
     for (int b = 0; b < kND; b++) base[b * (g.Rp * 32) + off] = (uint8_t)(((u >> (8 * b)) & 0xFF) ^ 0x80);
+  }
+  // Rp % 16 == 8: 8 zero rows after plane 6 -- the last MMA of each T digit is rounded up to a
+  // multiple of 16 columns and reads them (zero products on the next diagonal's columns)
+  const int pad = g.bstride - kND * g.Rp * 32;
+  if (pad > 0) {
+    const int64_t nb = (int64_t)g.ntn * g.nkc * pad;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nb; e += (int64_t)gridDim.x * blockDim.x)
+      img[(e / pad) * g.bstride + kND * g.Rp * 32 + e % pad] = 0;
   }
 }
 
@@ -596,7 +612,9 @@ int sm_count() {
   return n;
 }
 
-Geo make_geo(int64_t pre, int64_t K, int64_t post, int ncols) {
+// rp8: the digit kernel also takes N tiles padded to a multiple of 8 (Rp = 40, 56) instead of 16
+// (R = 100 as 2 x 52 columns, R = 200 as 4 x 52: 56-column tiles do 11 % fewer MMA columns than 64)
+Geo make_geo(int64_t pre, int64_t K, int64_t post, int ncols, bool rp8) {
   Geo g;
   g.pre = pre;
   g.K = K;
@@ -609,6 +627,9 @@ Geo make_geo(int64_t pre, int64_t K, int64_t post, int ncols) {
   if (g.ntn > 1) g.Rn = std::min(rpmax, (g.Rn + 3) / 4 * 4);  // 32-byte aligned column blocks
   g.ntn = (ncols + g.Rn - 1) / g.Rn;
   g.Rp = (g.Rn + 15) / 16 * 16;
+  static const bool no_rp8 = getenv("CPD_I8_NO_RP8") != nullptr;  // experiment switch
+  if (rp8 && !no_rp8 && (g.Rn + 7) / 8 * 8 < g.Rp && g.Rp > 32) g.Rp = (g.Rn + 7) / 8 * 8;
+  g.bstride = kND * g.Rp * 32 + (g.Rp % 16 ? 256 : 0);
   g.nmt = (g.Mrows + kBM - 1) / kBM;
   g.ntiles = g.nmt * g.ntn;
   g.nkc = (int)((K + 31) / 32);
@@ -696,7 +717,9 @@ cudaError_t dispatch_i8(int L, int grid, const double* X, const Geo& g, const ui
 // D_MCF: MC over padded digit rows with Mo = post / w > 1 and Mo * ipad % 128 == 0: the same boxes as
 // D_MC128 over the flattened (Mo, ipad) extent -- 4 % of pad rows instead of D_MCP's per-row 128-blocks
 // (C3, w = 200, ipad = 208: 208 MMA rows per 200 instead of 256)
-enum { D_KC = 0, D_MC128 = 1, D_MC64 = 2, D_MC32 = 3, D_MCP = 4, D_MCF = 5 };
+// D_KCW: KC over a [P2][Mrows][Qp] view -- the K index is (slab p, q): the contraction of a block of
+// modes with a Khatri-Rao product (upper-level fusion), wrapping blocks included
+enum { D_KC = 0, D_MC128 = 1, D_MC64 = 2, D_MC32 = 3, D_MCP = 4, D_MCF = 5, D_KCW = 6 };
 constexpr int kStagesD = 5;
 constexpr int kEpiWarps = 16;                        // 4 per TMEM lane quarter
 constexpr int kThreadsD = 32 * (2 + kEpiWarps);
@@ -802,7 +825,8 @@ __global__ void __launch_bounds__(kThreadsD, 1)
                    const int* __restrict__ Xexp, double* __restrict__ out, int beta,
                    const __grid_constant__ CUtensorMap tmap, int dbg) {
   constexpr int Rp = RP;
-  constexpr int Bbytes = kND * Rp * 32;
+  constexpr int Bbytes = kND * Rp * 32 + (Rp % 16 ? 256 : 0);  // + 8 zero rows when Rp % 16 == 8
+  static_assert(Bbytes <= kBStage, "B stage");
   constexpr int NDS = kStagesD;
   // TMEM accumulator buffers: 7 diagonals x Rp columns each; two (ping-pong) when they fit
   constexpr int NACC = (2 * kND * Rp <= 512 && kND * Rp <= 256) ? 2 : 1;
@@ -867,13 +891,19 @@ __global__ void __launch_bounds__(kThreadsD, 1)
         } else if constexpr (L == D_MCF) {
           p = (int)(i0 / g.postF);
           m0 = (int)(i0 - (int64_t)p * g.postF);
-        } else if constexpr (L != D_KC) {
+        } else if constexpr (L != D_KC && L != D_KCW) {
           p = (int)(i0 / g.post);
           m0 = (int)(i0 - (int64_t)p * g.post);
         }
         for (int kc = 0; kc < g.nkc; kc++) {
           mbar_wait(empty0 + 8 * s, par);
           const uint32_t st = su32(smem + s * kDStage), bar = full0 + 8 * s;
+          int kk = (int)g.kofs + kc * 32;  // K coordinate of this step
+          if constexpr (L == D_KCW) {
+            const int sl = kc / g.nkq;
+            kk = (int)g.kofs + (kc - sl * g.nkq) * 32;
+            p = (int)g.p0 + sl;
+          }
           if (dbg & 2) {  // profiling: no loads
             mbar_arrive(bar);
             if (++s == NDS) {
@@ -892,20 +922,26 @@ __global__ void __launch_bounds__(kThreadsD, 1)
                 asm volatile(
                     "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster "
                     "[%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(st),
-                    "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(kc * 32), "r"((int)i0), "r"(0), "r"(bar), "h"(cmask)
+                    "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(kk), "r"((int)i0), "r"(0), "r"(bar), "h"(cmask)
+                    : "memory");
+              } else if constexpr (L == D_KCW) {
+                asm volatile(
+                    "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster "
+                    "[%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(st),
+                    "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(kk), "r"((int)i0), "r"(p), "r"(0), "r"(bar), "h"(cmask)
                     : "memory");
               } else if (L == D_MCP && g.Mo > 1) {
                 asm volatile(
                     "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster "
                     "[%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(st),
-                    "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(m0), "r"(mo), "r"(kc * 32), "r"(p), "r"(0), "r"(bar),
+                    "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(m0), "r"(mo), "r"(kk), "r"(p), "r"(0), "r"(bar),
                     "h"(cmask)
                     : "memory");
               } else {
                 asm volatile(
                     "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster "
                     "[%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(st),
-                    "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(m0), "r"(kc * 32), "r"(p), "r"(0), "r"(bar), "h"(cmask)
+                    "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(m0), "r"(kk), "r"(p), "r"(0), "r"(bar), "h"(cmask)
                     : "memory");
               }
             }
@@ -913,25 +949,31 @@ __global__ void __launch_bounds__(kThreadsD, 1)
             asm volatile(
                 "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
                 "%4}], [%5];" ::"r"(st),
-                "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(kc * 32), "r"((int)i0), "r"(0), "r"(bar)
+                "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(kk), "r"((int)i0), "r"(0), "r"(bar)
+                : "memory");
+          } else if constexpr (L == D_KCW) {
+            asm volatile(
+                "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+                "%4, %5}], [%6];" ::"r"(st),
+                "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(kk), "r"((int)i0), "r"(p), "r"(0), "r"(bar)
                 : "memory");
           } else if (L == D_MCP && g.Mo == 1) {
             asm volatile(
                 "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
                 "%4, %5}], [%6];" ::"r"(st),
-                "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(m0), "r"(kc * 32), "r"(p), "r"(0), "r"(bar)
+                "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(m0), "r"(kk), "r"(p), "r"(0), "r"(bar)
                 : "memory");
           } else if constexpr (L == D_MCP) {
             asm volatile(
                 "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
                 "%4, %5, %6}], [%7];" ::"r"(st),
-                "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(m0), "r"(mo), "r"(kc * 32), "r"(p), "r"(0), "r"(bar)
+                "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(m0), "r"(mo), "r"(kk), "r"(p), "r"(0), "r"(bar)
                 : "memory");
           } else {
             asm volatile(
                 "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
                 "%4, %5}], [%6];" ::"r"(st),
-                "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(m0), "r"(kc * 32), "r"(p), "r"(0), "r"(bar)
+                "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(m0), "r"(kk), "r"(p), "r"(0), "r"(bar)
                 : "memory");
           }
           const uint8_t* bsrc = Bimg + ((int64_t)nt * g.nkc + kc) * Bbytes;
@@ -965,10 +1007,11 @@ __global__ void __launch_bounds__(kThreadsD, 1)
       uint32_t par = 0;
       // A: KC K-major SW32 (8-row groups of 256 B); MC MN-major, swizzle = MN atom width:
       // LBO = stride between the G atoms (one prefix index each), SBO = 8 k-rows of the atom
-      constexpr uint32_t A_LBO = L == D_KC ? 16 : 32 * MCW;
-      constexpr uint32_t A_SBO = L == D_KC ? 256 : 8 * MCW;
-      constexpr uint32_t A_LAYOUT = (L == D_KC || L == D_MC32) ? 6 : L == D_MC64 ? 4 : 2;
-      constexpr uint32_t AMAJ = L == D_KC ? 0u : (1u << 15);
+      constexpr bool KMAJ = L == D_KC || L == D_KCW;
+      constexpr uint32_t A_LBO = KMAJ ? 16 : 32 * MCW;
+      constexpr uint32_t A_SBO = KMAJ ? 256 : 8 * MCW;
+      constexpr uint32_t A_LAYOUT = (KMAJ || L == D_MC32) ? 6 : L == D_MC64 ? 4 : 2;
+      constexpr uint32_t AMAJ = KMAJ ? 0u : (1u << 15);
       for (int64_t tt = 0; tt < my_tiles; tt++) {
         const int ab = NACC == 2 ? (int)(tt & 1) : 0;
         const uint32_t use = NACC == 2 ? (uint32_t)(tt >> 1) : (uint32_t)tt;  // uses of this buffer so far
@@ -985,7 +1028,9 @@ __global__ void __launch_bounds__(kThreadsD, 1)
           for (int a = kND - 1; a >= 0; a--) {
             if (dbg & 1) break;  // profiling: no MMAs
             const uint32_t acc = (kc > 0 || a < kND - 1) ? 1u : 0u;
-            const int n = (a + 1) * Rp;  // diagonals 0..a
+            // diagonals 0..a; N rounded up to 16 (Rp % 16 == 8): the extra 8 columns multiply the zero rows
+            // after plane 6 into diagonal a+1's first columns (+0; a = 6 initialises them at kc = 0)
+            const int n = ((a + 1) * Rp + 15) / 16 * 16;
             const uint64_t ad = ad0 + (uint64_t)((a * kAPlane) >> 4);
             const uint64_t bd = bd0 + (uint64_t)(((kND - 1 - a) * Rp * 32) >> 4);  // B planes 6-a..6
             // N > 256 is split in two: at 256 (dbg 64) or in halves (multiples of 16), which keeps
@@ -1152,23 +1197,30 @@ bool make_tmap_digits(int L, const DigitView& dv, const Geo& g, CUtensorMap* tm)
                                                            : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   uint8_t* base = const_cast<uint8_t*>(dv.planes);
   const cuuint64_t ps = (cuuint64_t)dv.plane_stride;
+  const cuuint64_t KF = (cuuint64_t)(g.Kfull ? g.Kfull : g.K);  // K extent of the map (K chunks)
   CUresult r;
-  if (L == D_KC) {  // rows of ipad bytes (K = w)
-    cuuint64_t dims[3] = {(cuuint64_t)g.K, (cuuint64_t)g.Mrows, (cuuint64_t)kND};
+  if (L == D_KCW) {  // [P2][Mrows][Qp]: slabs of Mrows rows of Qp bytes
+    cuuint64_t dims[4] = {(cuuint64_t)g.Qp, (cuuint64_t)g.Mrows, (cuuint64_t)g.P2, (cuuint64_t)kND};
+    cuuint64_t strides[3] = {(cuuint64_t)g.Qp, (cuuint64_t)g.Qp * g.Mrows, ps};
+    cuuint32_t box[4] = {32, (cuuint32_t)kBM, 1, (cuuint32_t)kND}, es[4] = {1, 1, 1, 1};
+    r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else if (L == D_KC) {  // rows of ipad bytes (K = w)
+    cuuint64_t dims[3] = {KF, (cuuint64_t)g.Mrows, (cuuint64_t)kND};
     cuuint64_t strides[2] = {(cuuint64_t)dv.ipad, ps};
     cuuint32_t box[3] = {32, (cuuint32_t)kBM, (cuuint32_t)kND}, es[3] = {1, 1, 1};
     r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   } else if (L == D_MCP) {
     if (g.Mo == 1) {
-      cuuint64_t dims[4] = {(cuuint64_t)dv.ipad, (cuuint64_t)g.K, (cuuint64_t)g.pre, (cuuint64_t)kND};
-      cuuint64_t strides[3] = {(cuuint64_t)dv.ipad, (cuuint64_t)dv.ipad * g.K, ps};
+      cuuint64_t dims[4] = {(cuuint64_t)dv.ipad, KF, (cuuint64_t)g.pre, (cuuint64_t)kND};
+      cuuint64_t strides[3] = {(cuuint64_t)dv.ipad, (cuuint64_t)dv.ipad * KF, ps};
       cuuint32_t box[4] = {(cuuint32_t)kBM, 32, 1, (cuuint32_t)kND}, es[4] = {1, 1, 1, 1};
       r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
               CU_TENSOR_MAP_SWIZZLE_128B, promo_mc, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     } else {
-      cuuint64_t dims[5] = {(cuuint64_t)dv.ipad, (cuuint64_t)g.Mo, (cuuint64_t)g.K, (cuuint64_t)g.pre, (cuuint64_t)kND};
-      cuuint64_t strides[4] = {(cuuint64_t)dv.ipad, (cuuint64_t)dv.ipad * g.Mo, (cuuint64_t)dv.ipad * g.Mo * g.K, ps};
+      cuuint64_t dims[5] = {(cuuint64_t)dv.ipad, (cuuint64_t)g.Mo, KF, (cuuint64_t)g.pre, (cuuint64_t)kND};
+      cuuint64_t strides[4] = {(cuuint64_t)dv.ipad, (cuuint64_t)dv.ipad * g.Mo, (cuuint64_t)dv.ipad * g.Mo * KF, ps};
       cuuint32_t box[5] = {(cuuint32_t)kBM, 1, 32, 1, (cuuint32_t)kND}, es[5] = {1, 1, 1, 1, 1};
       r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
               CU_TENSOR_MAP_SWIZZLE_128B, promo_mc, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -1176,8 +1228,8 @@ bool make_tmap_digits(int L, const DigitView& dv, const Geo& g, CUtensorMap* tm)
   } else {  // unpadded: post contiguous (D_MCF: the flattened padded extent postF)
     const int mcw = (L == D_MC128 || L == D_MCF) ? 128 : L == D_MC64 ? 64 : 32;
     const cuuint64_t pe = (cuuint64_t)(L == D_MCF ? g.postF : g.post);
-    cuuint64_t dims[4] = {pe, (cuuint64_t)g.K, (cuuint64_t)g.pre, (cuuint64_t)kND};
-    cuuint64_t strides[3] = {pe, (cuuint64_t)g.K * pe, ps};
+    cuuint64_t dims[4] = {pe, KF, (cuuint64_t)g.pre, (cuuint64_t)kND};
+    cuuint64_t strides[3] = {pe, KF * pe, ps};
     cuuint32_t box[4] = {(cuuint32_t)mcw, 32, (cuuint32_t)(kBM / mcw), (cuuint32_t)kND}, es[4] = {1, 1, 1, 1};
     const CUtensorMapSwizzle sw =
         mcw == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : mcw == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
@@ -1219,8 +1271,8 @@ cudaError_t run_i8d(int grid, const Geo& g, const uint8_t* Bimg, const int* F, c
 }  // namespace
 
 size_t ttm_i8_workspace_bytes(int64_t K, int ncols) {
-  Geo g = make_geo(1, K, 1, ncols);
-  return (size_t)g.ntn * g.nkc * kND * g.Rp * 32 + kMaxColsI8 * sizeof(int);
+  Geo g = make_geo(1, K, 1, ncols, false);  // the 16-column padding bounds the 8-column one
+  return (size_t)g.ntn * g.nkc * g.bstride + kMaxColsI8 * sizeof(int);
 }
 
 cudaError_t launch_absmax_exp(const double* x, int64_t n, double* partial, int* e_out, cudaStream_t st,
@@ -1260,73 +1312,109 @@ int digit_layout(int64_t pre, int64_t K, int64_t post, int64_t w, int64_t ipad) 
   return ipad >= kBM ? D_MCP : -1;  // tiles of 128 rows over the innermost mode (no box overhang)
 }
 
-cudaError_t launch_ttm_i8(const double* X, int64_t pre, int64_t K, int64_t post, const double* B, int ncols,
-                          double* out, int beta, const int* Xexp, void* ws, size_t ws_bytes, cudaStream_t st,
-                          const DigitView* dv) {
-  if (pre <= 0 || post <= 0 || ncols <= 0) return cudaSuccess;
-  if (K <= 0 || K > kMaxKI8 || ncols > kMaxColsI8) return cudaErrorInvalidValue;
-  Geo g = make_geo(pre, K, post, ncols);
-  const size_t img = (size_t)g.ntn * g.nkc * kND * g.Rp * 32;
-  if (ws_bytes < img + kMaxColsI8 * sizeof(int)) return cudaErrorInvalidValue;
-  uint8_t* Bimg = static_cast<uint8_t*>(ws);
-  int* F = reinterpret_cast<int*>(static_cast<uint8_t*>(ws) + img);
-  g_launches += 3;
-  col_exp_kernel<<<ncols, 256, 0, st>>>(B, K, ncols, F);
-  {
-    int64_t total = (int64_t)g.ntn * g.nkc * g.Rp * 32;
-    int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
-    b_image_kernel<<<blocks, 256, 0, st>>>(B, K, g, F, Bimg);
+namespace {
+// one digit-kernel launch of layout Ld over the geometry g (its B image already in Bimg): tile counts of
+// the padded layouts, the CTA-pair cluster, the tensor map.  *launched = false: no tensor map (caller
+// falls back)
+cudaError_t launch_digit_geo(int Ld, Geo gd, const DigitView& dv, const uint8_t* Bimg, const int* F,
+                             const int* Xexp, double* out, int beta, cudaStream_t st, bool* launched) {
+  *launched = false;
+  if (Ld == D_MCP) {
+    gd.w = dv.w;
+    gd.ipad = dv.ipad;
+    gd.Mo = gd.post / dv.w;
+    gd.wb = (int)((dv.w + kBM - 1) / kBM);
+    gd.nmt = gd.pre * gd.Mo * gd.wb;
+    gd.ntiles = gd.nmt * gd.ntn;
+  } else if (Ld == D_MCF) {
+    gd.w = dv.w;
+    gd.ipad = dv.ipad;
+    gd.Mo = gd.post / dv.w;
+    gd.postF = gd.Mo * dv.ipad;
+    gd.nmt = gd.pre * gd.postF / kBM;
+    gd.ntiles = gd.nmt * gd.ntn;
   }
-  const int grid0 = (int)std::min<int64_t>(g.ntiles, sm_count());
-  static const bool no_digits = getenv("CPD_I8_NO_DIGITS") != nullptr;
-  const int Ld = dv && dv->planes ? digit_layout(pre, K, post, dv->w, dv->ipad) : -1;
-  if (Ld >= 0 && !no_digits && ((uintptr_t)dv->planes % 16) == 0) {
-    Geo gd = g;
-    if (Ld == D_MCP) {
-      gd.w = dv->w;
-      gd.ipad = dv->ipad;
-      gd.Mo = post / dv->w;
-      gd.wb = (int)((dv->w + kBM - 1) / kBM);
-      gd.nmt = pre * gd.Mo * gd.wb;
-      gd.ntiles = gd.nmt * gd.ntn;
-    } else if (Ld == D_MCF) {
-      gd.w = dv->w;
-      gd.ipad = dv->ipad;
-      gd.Mo = post / dv->w;
-      gd.postF = gd.Mo * dv->ipad;
-      gd.nmt = pre * gd.postF / kBM;
-      gd.ntiles = gd.nmt * gd.ntn;
-    }
-    // N tiles of one M tile on one cluster with the A box multicast (2 or 4 N tiles)
-    static const bool no_mc = getenv("CPD_I8_NO_MULTICAST") != nullptr;
-    // pairs only: a 4-CTA cluster couples four MMA-bound CTAs to the slowest (C5: 53 -> 73 ms)
-    static const int cl_env = getenv("CPD_I8_CLUSTER") ? atoi(getenv("CPD_I8_CLUSTER")) : 2;
-    if (!no_mc && gd.ntn % 2 == 0 && (cl_env == 2 || cl_env == 4) && gd.ntn % cl_env == 0 &&
-        sm_count() % cl_env == 0)
-      gd.cl = cl_env;
-    const int gridd = gd.cl == 1 ? (int)std::min<int64_t>(gd.ntiles, sm_count())
-                                 : gd.cl * (int)std::min<int64_t>(gd.nmt * (gd.ntn / gd.cl), sm_count() / gd.cl);
-    CUtensorMap tmd;
-    if (make_tmap_digits(Ld, *dv, gd, &tmd)) {
-      switch (g.Rp) {
+  // N tiles of one M tile on one cluster with the A box multicast (2 or 4 N tiles)
+  static const bool no_mc = getenv("CPD_I8_NO_MULTICAST") != nullptr;
+  // pairs only: a 4-CTA cluster couples four MMA-bound CTAs to the slowest (C5: 53 -> 73 ms)
+  static const int cl_env = getenv("CPD_I8_CLUSTER") ? atoi(getenv("CPD_I8_CLUSTER")) : 2;
+  if (!no_mc && gd.ntn % 2 == 0 && (cl_env == 2 || cl_env == 4) && gd.ntn % cl_env == 0 &&
+      sm_count() % cl_env == 0)
+    gd.cl = cl_env;
+  const int gridd = gd.cl == 1 ? (int)std::min<int64_t>(gd.ntiles, sm_count())
+                               : gd.cl * (int)std::min<int64_t>(gd.nmt * (gd.ntn / gd.cl), sm_count() / gd.cl);
+  CUtensorMap tmd;
+  if (!make_tmap_digits(Ld, dv, gd, &tmd)) return cudaSuccess;
+  *launched = true;
+  g_launches++;
+  switch (gd.Rp) {
 #define CPD_I8D_CASE(RP_)                                                                         \
   case RP_:                                                                                       \
     switch (Ld) {                                                                                 \
       case D_KC: return run_i8d<D_KC, RP_>(gridd, gd, Bimg, F, Xexp, out, beta, tmd, st);         \
+      case D_KCW: return run_i8d<D_KCW, RP_>(gridd, gd, Bimg, F, Xexp, out, beta, tmd, st);       \
       case D_MC128: return run_i8d<D_MC128, RP_>(gridd, gd, Bimg, F, Xexp, out, beta, tmd, st);   \
       case D_MC64: return run_i8d<D_MC64, RP_>(gridd, gd, Bimg, F, Xexp, out, beta, tmd, st);     \
       case D_MC32: return run_i8d<D_MC32, RP_>(gridd, gd, Bimg, F, Xexp, out, beta, tmd, st);     \
       case D_MCF: return run_i8d<D_MCF, RP_>(gridd, gd, Bimg, F, Xexp, out, beta, tmd, st);       \
       default: return run_i8d<D_MCP, RP_>(gridd, gd, Bimg, F, Xexp, out, beta, tmd, st);         \
     }
-        CPD_I8D_CASE(16)
-        CPD_I8D_CASE(32)
-        CPD_I8D_CASE(48)
-        CPD_I8D_CASE(64)
+    CPD_I8D_CASE(16)
+    CPD_I8D_CASE(32)
+    CPD_I8D_CASE(40)
+    CPD_I8D_CASE(48)
+    CPD_I8D_CASE(56)
+    CPD_I8D_CASE(64)
 #undef CPD_I8D_CASE
+  }
+  return cudaErrorInvalidValue;
+}
+
+// column exponents and the B digit image of rows [0, K) of B (one K chunk)
+void factor_image(const double* B, int64_t K, const Geo& g, int* F, uint8_t* Bimg, cudaStream_t st) {
+  g_launches += 2;
+  col_exp_kernel<<<g.ncols, 256, 0, st>>>(B, K, g.ncols, F);
+  const int64_t total = (int64_t)g.ntn * g.nkc * g.Rp * 32;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
+  b_image_kernel<<<blocks, 256, 0, st>>>(B, K, g, F, Bimg);
+}
+}  // namespace
+
+cudaError_t launch_ttm_i8(const double* X, int64_t pre, int64_t K, int64_t post, const double* B, int ncols,
+                          double* out, int beta, const int* Xexp, void* ws, size_t ws_bytes, cudaStream_t st,
+                          const DigitView* dv) {
+  if (pre <= 0 || post <= 0 || ncols <= 0) return cudaSuccess;
+  if (K <= 0 || ncols > kMaxColsI8) return cudaErrorInvalidValue;
+  static const bool no_digits = getenv("CPD_I8_NO_DIGITS") != nullptr;
+  const int Ld = dv && dv->planes ? digit_layout(pre, K, post, dv->w, dv->ipad) : -1;
+  const bool digits = Ld >= 0 && !no_digits && ((uintptr_t)dv->planes % 16) == 0;
+  if (K > kMaxKI8 && !digits) return cudaErrorInvalidValue;
+  const int64_t Kc0 = std::min<int64_t>(K, kMaxKI8);
+  const size_t img_max = ttm_i8_workspace_bytes(Kc0, ncols) - kMaxColsI8 * sizeof(int);
+  if (ws_bytes < img_max + kMaxColsI8 * sizeof(int)) return cudaErrorInvalidValue;
+  uint8_t* Bimg = static_cast<uint8_t*>(ws);
+  int* F = reinterpret_cast<int*>(static_cast<uint8_t*>(ws) + img_max);
+  if (digits) {
+    // K chunks of <= kMaxKI8 (|D_d| < 2^31), each its own exponents and image, accumulated with beta = 1
+    for (int64_t k0 = 0; k0 < K; k0 += kMaxKI8) {
+      const int64_t Kc = std::min<int64_t>(kMaxKI8, K - k0);
+      Geo g = make_geo(pre, Kc, post, ncols, true);
+      g.kofs = k0;
+      g.Kfull = K;
+      factor_image(B + k0 * ncols, Kc, g, F, Bimg, st);
+      bool launched = false;
+      cudaError_t e = launch_digit_geo(Ld, g, *dv, Bimg, F, Xexp, out, beta || k0 > 0, st, &launched);
+      if (e != cudaSuccess) return e;
+      if (!launched) {
+        if (k0 > 0 || K > kMaxKI8) return cudaErrorInvalidValue;
+        break;  // converting kernel below
       }
+      if (k0 + Kc >= K) return cudaSuccess;
     }
   }
+  Geo g = make_geo(pre, K, post, ncols, false);
+  factor_image(B, K, g, F, Bimg, st);
+  g_launches++;
   // loader: TMA when the layout allows it (16-byte aligned strides; MC tiles must not straddle
   // the prefix index, i.e. post % 128 == 0), else register loads
   static const bool no_tma = getenv("CPD_I8_NO_TMA") != nullptr;
@@ -1347,6 +1435,50 @@ cudaError_t launch_ttm_i8(const double* X, int64_t pre, int64_t K, int64_t post,
     case 64: return dispatch_i8<64>(L, grid, X, g, Bimg, F, Xexp, out, beta, tm, st);
   }
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_ttm_i8_block(int64_t P, int64_t Mrows, int64_t Qp, const double* Bpad, int ncols, double* out,
+                                int beta, const int* Xexp, void* ws, size_t ws_bytes, cudaStream_t st,
+                                const DigitView& dv) {
+  if (P <= 0 || Mrows <= 0 || ncols <= 0) return cudaSuccess;
+  if (!dv.planes || Qp <= 0 || Qp % 16 || ((uintptr_t)dv.planes % 16) || ncols > kMaxColsI8)
+    return cudaErrorNotSupported;
+  const int64_t nkq = (Qp + 31) / 32, Ks = 32 * nkq;  // K rows of Bpad per slab
+  const size_t img_max = ttm_i8_workspace_bytes(kMaxKI8, ncols) - kMaxColsI8 * sizeof(int);
+  if (ws_bytes < img_max + kMaxColsI8 * sizeof(int)) return cudaErrorInvalidValue;
+  uint8_t* Bimg = static_cast<uint8_t*>(ws);
+  int* F = reinterpret_cast<int*>(static_cast<uint8_t*>(ws) + img_max);
+  auto one = [&](int64_t p0, int64_t np, int64_t q0, int64_t K, int nk, bool first) -> cudaError_t {
+    Geo g = make_geo(Mrows, K, 1, ncols, true);
+    g.nkq = nk;
+    g.p0 = p0;
+    g.kofs = q0;
+    g.P2 = P;
+    g.Qp = Qp;
+    const double* Bc = Bpad + (p0 * Ks + q0) * ncols;
+    factor_image(Bc, K, g, F, Bimg, st);
+    bool launched = false;
+    cudaError_t e = launch_digit_geo(D_KCW, g, dv, Bimg, F, Xexp, out, beta || !first, st, &launched);
+    if (e == cudaSuccess && !launched) e = cudaErrorNotSupported;
+    (void)np;
+    return e;
+  };
+  if (Ks <= kMaxKI8) {  // whole slabs per launch
+    const int64_t spc = kMaxKI8 / Ks;
+    for (int64_t p0 = 0; p0 < P; p0 += spc) {
+      const int64_t np = std::min(spc, P - p0);
+      cudaError_t e = one(p0, np, 0, np * Ks, (int)nkq, p0 == 0);
+      if (e != cudaSuccess) return e;
+    }
+  } else {  // slabs longer than one launch: K chunks inside each slab
+    for (int64_t p = 0; p < P; p++)
+      for (int64_t q0 = 0; q0 < Ks; q0 += kMaxKI8) {
+        const int64_t K = std::min<int64_t>(kMaxKI8, Ks - q0);
+        cudaError_t e = one(p, 1, q0, K, (int)(K / 32), p == 0 && q0 == 0);
+        if (e != cudaSuccess) return e;
+      }
+  }
+  return cudaSuccess;
 }
 
 }  // namespace cpd

@@ -24,7 +24,7 @@ class CPDecomposition:
 
     def __init__(self, T, shape, R, A0, *, device=0, rank=0, world=1, nccl_id=None, stream=None,
                  pp_eps=0.1, reuse_root_in_pp_init=True, profile_phases=False, local_group=None,
-                 ttm_impl=2, grid=None, fused_rs=False):
+                 ttm_impl=2, grid=None, fused_rs=False, msdt_levels=1):
         lib = load_library()
         self.N = len(shape)
         self.shape = tuple(int(s) for s in shape)
@@ -45,6 +45,7 @@ class CPDecomposition:
         o.local_group = local_group.value if local_group is not None else None
         o.ttm_impl = int(ttm_impl)
         o.fused_rs = int(bool(fused_rs))
+        o.msdt_levels = int(msdt_levels)
         self.grid = tuple(grid) if grid is not None else (1,) * (self.N - 1) + (world,)
         if grid is not None:
             for n, g in enumerate(grid):
@@ -118,6 +119,13 @@ class CPDecomposition:
         out = np.zeros(2)
         check(self._lib.cpd_get_filler_counters(self._ctx, dptr(out)), self._ctx)
         return {"bytes": float(out[0]), "launches": int(out[1])}
+
+    def get_memory(self):
+        """cpd_get_memory: auxiliary device memory (peak and live bytes of tree nodes / PP operators /
+        block KRPs since init or reset_counters) and the bytes of T's digit planes."""
+        out = np.zeros(3)
+        check(self._lib.cpd_get_memory(self._ctx, dptr(out)), self._ctx)
+        return {"peak": float(out[0]), "live": float(out[1]), "digits": float(out[2])}
 
     def set_profile_level(self, level):
         check(self._lib.cpd_set_profile_level(self._ctx, int(level)), self._ctx)

@@ -196,6 +196,58 @@ def test_msdt_and_dt_sweeps_order_N(cpd, N, s, R, ttm_impl):
         m.close()
 
 
+@pytest.mark.parametrize("ttm_impl", [0, 1])
+@pytest.mark.parametrize("dims,R,l", [((6, 7, 5, 9), 5, 2), ((5, 4, 6, 3, 7), 4, 2), ((5, 4, 6, 3, 7), 4, 3),
+                                      ((3, 4, 2, 3, 5, 4), 3, 2), ((3, 4, 2, 3, 5, 4), 3, 4), ((4, 4, 130, 130), 3, 2),
+                                      ((130, 3, 2, 3, 130), 3, 2), ((2, 130, 130, 2, 64), 3, 2), ((20, 12, 16, 32), 50, 2)])
+def test_msdt_fused_levels(cpd, dims, R, l, ttm_impl):
+    """Upper-level fusion (opts.msdt_levels = l): every root contracts a cyclic block of l
+    modes in one pass over T with the Khatri-Rao product of their factors.  N - l state-synchronised
+    MSDT sweeps (one full cycle: N roots) against the oracle's ALS sweep (explicit unfolding and KRP),
+    every M^(n) and the fitness at 1e-10.  The shapes exercise middle, trailing and wrapping blocks,
+    padded innermost modes (w = 5, 7, 9, 130), K chunks on the digit planes (a trailing block of
+    130 x 144 padded K rows, a middle block of K = 16900, a wrapping block of 130 slabs of 160 K rows)
+    and 56-column N tiles (R = 50)."""
+    cfg = synth.custom(len(dims), 0, R, noise_var=1e-4, seed=sum(dims) % 89 + l, dims=dims)
+    N = cfg.N
+    T = dev_tensor(cpd, cfg)
+    To = O.make_tensor(cfg)
+    nt2 = O.norm2(To)
+    m = _model(cpd, cfg, T, ttm_impl=ttm_impl, msdt_levels=l)
+    A = synth.init_factors(cfg)
+    for sweep in range(N - l):
+        f = m.msdt_sweep()
+        out = O.als_sweep(To, A, nt2)
+        for n in range(N):
+            assert rel(m.get_last_mttkrp(n), out["M"][n]) <= TOL, (sweep, n, rel(m.get_last_mttkrp(n), out["M"][n]))
+        assert abs(f - out["f"]) <= TOL * abs(out["f"])
+        A = [m.get_factor(n) for n in range(N)]
+    assert m.counters()["roots"] == N
+    m.close()
+
+
+@pytest.mark.parametrize("N,s,R", [(5, 8, 4), (6, 6, 3)])
+def test_msdt_fused_levels_memory(cpd, N, s, R):
+    """The trade-off of P:700-702: with the upper l levels combined the largest tree node holds
+    s^(N-l) R elements, so cpd_get_memory's high-water mark falls with l (l <= N/2: beyond that the
+    block's Khatri-Rao product, s^l R, is the larger buffer), for N/(N-l) passes over T per sweep (the
+    roots ledger: N roots in N - l sweeps); the fitness equals the l = 1 run's at 1e-10."""
+    cfg = synth.custom(N, s, R, noise_var=1e-4, seed=N + s)
+    T = dev_tensor(cpd, cfg)
+    peaks = []
+    for l in range(1, N // 2 + 1):
+        m = _model(cpd, cfg, T, msdt_levels=l)
+        fl = [m.msdt_sweep() for _ in range(N - l)]
+        peaks.append(m.get_memory()["peak"])
+        assert m.counters()["roots"] == N
+        m.close()
+        m1 = _model(cpd, cfg, T)
+        f1 = [m1.msdt_sweep() for _ in range(N - l)]
+        assert abs(fl[-1] - f1[-1]) <= TOL * abs(f1[-1])
+        m1.close()
+    assert all(b < a for a, b in zip(peaks, peaks[1:])), peaks
+
+
 @pytest.mark.parametrize("N,s,R", [(4, 10, 4), (5, 6, 3), (6, 4, 2), (8, 3, 2), (3, 48, 64), (4, 20, 128)])
 def test_pp_order_N_state_synchronised(cpd, N, s, R):
     cfg = synth.custom(N, s, R, noise_var=1e-3, seed=N + 40)
@@ -339,10 +391,12 @@ def test_full_size_sampled_rows(cpd, c, ttm_impl):
                                      ((64, 64, 64), 64), ((40, 33, 257), 32), ((3, 256, 128), 48), ((130, 48, 256), 64),
                                      ((64, 64, 64), 32), ((12, 48, 32), 16), ((6, 8, 64, 64), 24),
                                      ((9, 30, 200), 64), ((5, 7, 6, 100), 40), ((3, 130, 72), 20),
-                                     ((4, 8, 200), 20), ((3, 16, 24), 12), ((2, 16, 8, 200), 100)])
+                                     ((4, 8, 200), 20), ((3, 16, 24), 12), ((2, 16, 8, 200), 100),
+                                     ((7, 9, 5, 24), 50), ((20, 6, 16), 80), ((8, 16, 56), 56), ((4, 9, 208), 200)])
 def test_ttm_i8_all_positions(cpd, shape, R, digits):
     """cpd_ttm_i8 (int8 digit slicing on tcgen05) against the oracle's T x_j A at every
-    contraction position: ragged M tiles, K tails (odd K, K % 32 != 0), 1-4 N tiles."""
+    contraction position: ragged M tiles, K tails (odd K, K % 32 != 0), 1-4 N tiles, N tiles
+    padded to 16 columns and to 8 (Rp = 40, 56: the zero rows after the last plane)."""
     rng = np.random.default_rng(sum(shape) + R + 1)
     Tn = rng.standard_normal(shape)
     T = torch.from_numpy(Tn).cuda()

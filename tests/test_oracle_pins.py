@@ -227,6 +227,53 @@ def test_msdt_and_dt_equal_direct(N, s):
         assert m.n_ttm == expect
 
 
+def test_block_contract_brute_force():
+    """block_contract (upper-level fusion) against nested loops over the definition
+    Σ_{i_c, c in C} T[i] Π_c A^(c)(i_c, r), for a middle block, a trailing block and a block that wraps
+    around from mode N to mode 1; a one-mode block equals the first-level TTM."""
+    T = rnd((3, 2, 4, 3), 17)
+    A = [rnd((s, 2), 30 + i) for i, s in enumerate(T.shape)]
+    for C in ([1, 2], [2, 3], [3, 0], [3, 0, 1], [0, 1, 2]):
+        got = O.block_contract(T, A, C)
+        kept = [m for m in range(4) if m not in C]
+        ref = np.zeros([T.shape[m] for m in kept] + [2])
+        for idx in itertools.product(*[range(s) for s in T.shape]):
+            for r in range(2):
+                w = T[idx]
+                for c in C:
+                    w *= A[c][idx[c], r]
+                ref[tuple(idx[m] for m in kept) + (r,)] += w
+        assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max(), C
+    for j in range(4):
+        assert np.allclose(O.block_contract(T, A, [j]), O.ttm(T, A[j], j), rtol=1e-14, atol=0)
+
+
+@pytest.mark.parametrize("N,s,l", [(4, 4, 2), (5, 3, 2), (5, 3, 3), (6, 2, 2), (6, 2, 3), (6, 2, 4)])
+def test_msdt_fused_levels_equal_direct(N, s, l):
+    """MSDT with the upper l levels combined is still exact: every MTTKRP equals the
+    direct one under arbitrary factor updates; N roots per N-l sweeps (the paper's cost
+    2N/(N-l) s^N R per sweep: one pass over T per root); each root contracts the l modes that
+    follow its served block cyclically, and its largest node keeps N-l modes."""
+    T = rnd((s,) * N, 9)
+    rng = np.random.default_rng(2)
+    A = [rnd((s, 3), 60 + i) for i in range(N)]
+    m = O.MSDTModel(T, levels=l)
+    n_sweeps = N - l
+    for t in range(N * n_sweeps):
+        n = t % N
+        ref = O.mttkrp(T, A, n)
+        got = m.next_mttkrp(A)
+        assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max(), (t, n)
+        A[n] = A[n] + rng.standard_normal(A[n].shape)
+    assert m.n_ttm == N
+    for C, served in m.trace:
+        assert len(C) == l and len(served) == N - l
+        assert sorted(set(C) | set(served)) == list(range(N))
+        assert (served[-1] + 1) % N == C[0]
+    with pytest.raises(ValueError):
+        O.MSDTModel(T, levels=N - 1)
+
+
 def test_msdt_fig2_schedule_N4():
     """Fig. 2: roots T×4, T×3, T×2, T×1 serving (1,2,3), (4,1,2), (3,4,1), (2,3,4)."""
     T = rnd((2, 2, 2, 2), 1)
