@@ -455,6 +455,9 @@ def main():
                     "secondary": sec, "bytes_per_launch": ttm_bytes,
                     "fp64_equiv_tflops": ttm_tf, "fp64_equiv_over_dmma_peak": (ttm_tf / fp64) if ttm_tf else None,
                     "avg_launch_ms": ttm_ms, "launches": int(ctr["ttm_launches"])}
+        if args.msdt_levels > 1:
+            ttm_roof["note"] = ("msdt_levels > 1: the MSDT roots are block contractions (output s^(N-l) R, not "
+                                "s^(N-1) R); the byte model above is the first-level TTM's (pp_init, dt_sweep)")
         engines = {engine: {"msdt_ms_per_sweep": msdt_ms, "ttm_ms": ttm_ms, "ttm_fp64_equiv_tflops": ttm_tf}}
         if not args.no_dmma_compare:
             engines["dmma"] = dmma_compare(cpd, torch, cfg, T, m, local, rank, world, nccl_id, stream, fp64, fp64_src)
