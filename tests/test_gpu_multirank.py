@@ -65,7 +65,7 @@ def block(cpd, cfg, rank, grid):
     return T
 
 
-def run_group(cpd, cfg, P, grid=None, fused_rs=False):
+def run_group(cpd, cfg, P, grid=None, fused_rs=False, msdt_levels=1):
     group = cpd.cpd_local_group_create(P)
     Ts = [slab(cpd, cfg, r, P) if grid is None else block(cpd, cfg, r, grid) for r in range(P)]
     out, errs = [None] * P, []
@@ -74,7 +74,8 @@ def run_group(cpd, cfg, P, grid=None, fused_rs=False):
         try:
             torch.cuda.set_device(0)
             m = cpd.cp_als_init(Ts[r], cfg.shape, cfg.R, synth.init_factors(cfg), rank=r, world=P,
-                                local_group=group, stream=torch.cuda.Stream(), grid=grid, fused_rs=fused_rs)
+                                local_group=group, stream=torch.cuda.Stream(), grid=grid, fused_rs=fused_rs,
+                                msdt_levels=msdt_levels)
             out[r] = schedule(m, cfg.N)
             m.close()
         except Exception as e:  # pragma: no cover - reported below
@@ -192,3 +193,24 @@ def test_grid_validation(cpd):
                         grid=(1, 1, 4))
     assert e.value.status == 1
     cpd.cpd_local_group_destroy(g)
+
+
+@pytest.mark.parametrize("cfg,grid,fused_rs", [(synth.custom(4, 8, 3, noise_var=1e-3, seed=38), None, False),
+                                               (synth.custom(4, 8, 3, noise_var=1e-3, seed=38), (2, 2, 1, 2), False),
+                                               (synth.custom(5, 4, 3, noise_var=1e-3, seed=39), (1, 2, 1, 1, 2), True)])
+def test_fused_levels_partitioned(cpd, cfg, grid, fused_rs):
+    """Upper-level fusion (msdt_levels = 2) on the partitioned path: every rank contracts its
+    own block of T with the Khatri-Rao product of its factor blocks (the block contraction is local,
+    Table 1), the leaves are reduce-scattered as in Alg. 3; the whole schedule equals P = 1 with l = 1."""
+    P = 2 if grid is None else int(np.prod(grid))
+    ref = run_group(cpd, cfg, 1)[0]
+    got = run_group(cpd, cfg, P, grid=grid, fused_rs=fused_rs, msdt_levels=2)
+    for r in range(P):
+        for a, b in zip(got[r]["f"], ref["f"]):
+            assert abs(a - b) <= TOL * abs(b)
+        for Ms, Mr in zip(got[r]["M"], ref["M"]):
+            for a, b in zip(Ms, Mr):
+                assert np.linalg.norm(a - b) <= TOL * np.linalg.norm(b)
+        for As, Ar in zip(got[r]["A"], ref["A"]):
+            for a, b in zip(As, Ar):
+                assert np.linalg.norm(a - b) <= TOL * np.linalg.norm(b)
