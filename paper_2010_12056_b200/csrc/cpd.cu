@@ -753,13 +753,17 @@ cpd_status acquire_solve(cpd_ctx* ctx, int n, bool pp, int* buf, bool fused) {
 // overwritten): reduce-scatter in Proc-Slice(x_n) to the own rows (Alg. 3 line 14), solve them
 // (line 15; pp: V = A^(n) W added first, Eq. 7), dA, statistics, S (and dS) of the own rows, then
 // exchange_mode (all-reduce, all-gather of the block).
-cpd_status update_mode(cpd_ctx* ctx, int n, double* Mloc, bool pp, bool scattered = false) {
+// pend: the K-split reduction of the mTTV that produced Mloc, left to the fused update (PP critical chain)
+cpd_status update_mode(cpd_ctx* ctx, int n, double* Mloc, bool pp, bool scattered = false,
+                       const cpd::MPending* pend = nullptr) {
   const int R = ctx->R;
   const int64_t RR = (int64_t)R * R;
   const int64_t ro = rows_own(ctx, n), off = own_off(ctx, n);
   double* Mown = Mloc + off * R;
   const bool last = n == ctx->N - 1;
   const bool fused = use_fused(ctx, n, pp);
+  if (pend && pend->slots > 0 && (scattered || ctx->slice[n].world > 1 || !fused || !pp))
+    return fail(ctx, CPD_ERR_INTERNAL, "deferred mTTV reduction without a fused single-slice PP update");
   if (scattered) {
     // fused reduce-scatter: every slice rank stored its partial rows into its slot of the owner's
     // receive buffer; after the stream-ordered barrier the owner sums the slots in rank order
@@ -793,7 +797,7 @@ cpd_status update_mode(cpd_ctx* ctx, int n, double* Mloc, bool pp, bool scattere
                                 ctx->scal + SC_DA2 + n, ctx->scal + SC_A2 + n, last ? ctx->scal + SC_MA : nullptr,
                                 loc ? nullptr : ctx->pf_status + b, loc ? nullptr : ctx->status + n, ctx->st,
                                 loc ? ctx->S_all : nullptr, loc ? ctx->dS_all : nullptr, ctx->N, n,
-                                loc ? ctx->status + n : nullptr));
+                                loc ? ctx->status + n : nullptr, pend));
   } else {
     if (pp) {
       // V^(n) = A^(n) W^(n) with the current (pre-update) A^(n): Eq. 7; M~ += V (Eq. 5)
@@ -1783,6 +1787,10 @@ cpd_status pp_approx_sweep(cpd_ctx* ctx, double* fitness_out, int* still_valid) 
     cpd::MttvSpec sp[CPD_MAX_ORDER];
     int J = 0;
     double bytes = 0.0;
+    // the critical stream's K-split reduction is done by the fused update that consumes M~ (one launch
+    // and its gap fewer on the serial chain); experiment switch CPD_NO_DEFER_REDUCE
+    static const bool no_defer = getenv("CPD_NO_DEFER_REDUCE") != nullptr;
+    cpd::MPending pend;
     // the launch that completes M~_loc^(n) stores it into the owners' slots under the fused RS
     const cpd::OutMap* mp = rs_map_of(ctx, n);
     if (n == 0 && ctx->pp_spec0) {
@@ -1801,12 +1809,14 @@ cpd_status pp_approx_sweep(cpd_ctx* ctx, double* fitness_out, int* still_valid) 
       sp[J++] = spec(n, n - 1, &bytes);
       CU(cudaStreamWaitEvent(ctx->st, ctx->ev_pp_side[n], 0));
       PhaseScope ps(ctx, PH_MTTV);
-      CU(cpd::launch_mttv_multi(sp, J, ctx->R, nullptr, Mt, 1, ctx->ws_mttv, kMttvWs, ctx->st, mp));
+      const bool defer = !no_defer && !mp && ctx->slice[n].world == 1 && use_fused(ctx, n, true);
+      CU(cpd::launch_mttv_multi(sp, J, ctx->R, nullptr, Mt, 1, ctx->ws_mttv, kMttvWs, ctx->st, mp, false, 0,
+                                defer ? &pend : nullptr));
       ctx->counters[2] += 8.0 * 2 * ext(ctx, n) * ctx->R;
     }
     ctx->counters[2] += bytes;
     ctx->counters[3] += 1;
-    TRY(update_mode(ctx, n, Mt, true, rs_map_of(ctx, n) != nullptr));
+    TRY(update_mode(ctx, n, Mt, true, rs_map_of(ctx, n) != nullptr, &pend));
   }
   // speculation: the next sweep's mode-1 independent streams need only this sweep's final dA,
   // so they start now and overlap the end of this sweep and the host round trip; this sweep's

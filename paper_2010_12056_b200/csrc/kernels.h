@@ -94,10 +94,22 @@ struct OutMap {
   int64_t chunk;
   int nq;
 };
+// The K-split partials of an mTTV launch whose fixed-order reduction (mttv_reduce_kernel's arithmetic:
+// out[e] = (base ? base[e] : beta ? out[e] : 0) + Σ_k ws[k n + e], k ascending) is left to the kernel that
+// consumes out -- the fused factor update on the PP critical chain (one launch fewer per mode).  slots = 0:
+// nothing pending (out is final).
+struct MPending {
+  const double* ws = nullptr;
+  int slots = 0;
+  int64_t n = 0;
+  const double* base = nullptr;
+  int beta = 0;
+};
 // occ3: at most 3 resident CTAs per SM (for launches that overlap latency-critical kernels)
+// defer (may be null): a K-split launch without OutMap leaves its reduction to the consumer (*defer)
 cudaError_t launch_mttv_multi(const MttvSpec* specs, int J, int R, const double* base, double* out, int beta,
                               double* ws, int64_t ws_elems, cudaStream_t st, const OutMap* map = nullptr,
-                              bool occ3 = false, int waves_override = 0);
+                              bool occ3 = false, int waves_override = 0, MPending* defer = nullptr);
 // Two single-mode contractions of one node in one read (PP-init multi-output descent):
 // X viewed as [P][K1][Q][K2][C] (C = trailing extents x R), out1 = contract K1 -> [P][Q][K2][C],
 // out2 = contract K2 -> [P][K1][Q][C]; ws: ceil(K1/32) x |out1| doubles of partials when K1 > 32.
@@ -182,6 +194,6 @@ cudaError_t launch_update_fused(int R, int64_t rows, const double* Ginv, const d
                                 const double* base, double* dA, double* S, double* dS, double* part, double* gpart,
                                 double* o_dA2, double* o_A2, double* o_MA, const int* st_src, int* st_dst,
                                 cudaStream_t st, const double* S_all = nullptr, const double* dS_all = nullptr,
-                                int N = 0, int nmode = 0, int* st_local = nullptr);
+                                int N = 0, int nmode = 0, int* st_local = nullptr, const MPending* pend = nullptr);
 
 }  // namespace cpd

@@ -455,8 +455,9 @@ cudaError_t launch_slot_sum(const double* src, int nq, int64_t n, double* dst, c
 
 cudaError_t launch_mttv_multi(const MttvSpec* specs, int J, int R, const double* base, double* out, int beta,
                               double* ws, int64_t ws_elems, cudaStream_t st, const OutMap* map, bool occ3,
-                              int waves_override) {
+                              int waves_override, MPending* defer) {
   if (J < 1 || J > 8) return cudaErrorInvalidValue;
+  if (defer) *defer = MPending{};
   OutMap om{};
   if (map) om = *map;
   MttvJobs jobs{};
@@ -538,6 +539,10 @@ cudaError_t launch_mttv_multi(const MttvSpec* specs, int J, int R, const double*
   bool pack = false;  // jobs of one launch share the output size, not C: any packed job selects the variant
   for (int q = 0; q < J; q++) pack = pack || jobs.j[q].ppc > 1;
   launch_mttv_variant(vec2, vv, pack, occ3, (unsigned)items, jobs, R, out, beta, w, km, st);
+  if (!direct && defer && om.nq == 0) {
+    *defer = MPending{ws, (int)slots, jobs.E, base, beta};
+    return cudaGetLastError();
+  }
   if (!direct) {
     g_launches++;
     int64_t blocks = (jobs.E + 255) / 256;

@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(UPD_THREADS)
                         double* __restrict__ o_dA2, double* __restrict__ o_A2, double* __restrict__ o_MA,
                         const int* __restrict__ st_src, int* __restrict__ st_dst,
                         const double* __restrict__ S_all, const double* __restrict__ dS_all, int N, int nmode,
-                        int* __restrict__ st_local) {
+                        int* __restrict__ st_local, MPending pend) {
   extern __shared__ double sm[];
   double* G = sm;                 // R x R: Γ^{-1}
   double* Ws = sm + R * R;        // R x R (PP only)
@@ -232,7 +232,16 @@ __global__ void __launch_bounds__(UPD_THREADS)
 #pragma unroll
     for (int u = 0; u < U; u++) {
       const int c = lane + 32 * u;
-      y[u] = c < R ? M[i * R + c] : 0.0;
+      if (pend.slots > 0 && c < R) {
+        // the mTTV's K-split reduction, in mttv_reduce_kernel's order, then M~ materialised
+        const int64_t e = i * R + c;
+        double s = pend.base ? pend.base[e] : (pend.beta ? M[e] : 0.0);
+        for (int k = 0; k < pend.slots; k++) s += pend.ws[k * pend.n + e];
+        y[u] = s;
+        if (!W) M[e] = s;
+      } else {
+        y[u] = c < R ? M[i * R + c] : 0.0;
+      }
       ao[u] = c < R ? A[i * R + c] : 0.0;
     }
     if (W) {  // y += a_old W
@@ -357,8 +366,9 @@ cudaError_t launch_update_fused(int R, int64_t rows, const double* Ginv, const d
                                 const double* base, double* dA, double* S, double* dS, double* part, double* gpart,
                                 double* o_dA2, double* o_A2, double* o_MA, const int* st_src, int* st_dst,
                                 cudaStream_t st, const double* S_all, const double* dS_all, int N, int nmode,
-                                int* st_local) {
+                                int* st_local, const MPending* pendp) {
   if (S_all && R > 32) return cudaErrorInvalidValue;
+  MPending pend = pendp ? *pendp : MPending{};
   if (R > kUpdMaxR || rows <= 0) return cudaErrorInvalidValue;
   const int blocks = update_fused_blocks(rows);
   int RB = (int)((rows + blocks - 1) / blocks);
@@ -366,7 +376,7 @@ cudaError_t launch_update_fused(int R, int64_t rows, const double* Ginv, const d
   if (smem > 227 * 1024 - 2048) return cudaErrorInvalidValue;
   void* args[] = {&R,     &rows,   &Ginv,   &W,      &M,      &A,    &base,  &dA,    &S,       &dS,
                   &part,  &gpart,  &RB,     &o_dA2,  &o_A2,   &o_MA, &st_src, &st_dst, &S_all, &dS_all,
-                  &N,     &nmode,  &st_local};
+                  &N,     &nmode,  &st_local, &pend};
   static const bool split = getenv("CPD_UPD_SPLIT") != nullptr;
   cudaError_t e = cudaErrorInvalidValue;
   switch ((R + 31) / 32) {
