@@ -5,6 +5,8 @@ and Figs. 5-6 compare the same three runs on CPU clusters):
   * DT ALS      plain CP-ALS on the standard dimension tree,
 all from the same seeded tensor and initial factors, stopping when the fitness of two
 neighbouring sweeps differs by <= delta or after max_sweeps.
+With LEVELS=l (environment, order >= 4) two more runs use upper-level fusion (msdt_levels = l,
+P:700-702): PP-CP-ALS and MSDT ALS at that l.
 usage: python tools/alg2_run.py [config] [max_sweeps] [delta] [any|regular]  -> one JSON line per run"""
 import json
 import os
@@ -30,9 +32,14 @@ with torch.cuda.stream(stream):
     T = bench.make_slab(cpd, torch, cfg, 0, 1, stream)
 torch.cuda.synchronize()
 A0 = synth.init_factors(cfg)
-for name, kw, regular in [("pp_cp_als", {"pp_eps": eps}, "msdt"),
-                          ("msdt_als", {"pp_eps": 1e-300}, "msdt"),
-                          ("dt_als", {"pp_eps": 1e-300}, "dt")]:
+runs = [("pp_cp_als", {"pp_eps": eps}, "msdt"),
+        ("msdt_als", {"pp_eps": 1e-300}, "msdt"),
+        ("dt_als", {"pp_eps": 1e-300}, "dt")]
+lv = int(os.environ.get("LEVELS", "1"))
+if lv > 1:
+    runs += [(f"pp_cp_als_l{lv}", {"pp_eps": eps, "msdt_levels": lv}, "msdt"),
+             (f"msdt_als_l{lv}", {"pp_eps": 1e-300, "msdt_levels": lv}, "msdt")]
+for name, kw, regular in runs:
     m = cpd.cp_als_init(T, cfg.shape, cfg.R, A0, stream=stream, **kw)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -44,7 +51,8 @@ for name, kw, regular in [("pp_cp_als", {"pp_eps": eps}, "msdt"),
         per.setdefault(r[1], []).append(r[4])
     fits = [r[3] for r in rows if r[3] is not None]
     print(json.dumps({
-        "config": cfg.name, "run": name, "stop_test": stop_test, "eps": kw["pp_eps"] if name == "pp_cp_als" else None, "delta": delta,
+        "config": cfg.name, "run": name, "stop_test": stop_test, "eps": kw["pp_eps"] if name.startswith("pp_cp_als") else None,
+        "msdt_levels": kw.get("msdt_levels", 1), "delta": delta,
         "sweeps": len(fits), "phase_counts": phase_counts(rows), "wall_s": wall,
         "ms_per_phase": {k: 1e3 * sum(v) / len(v) for k, v in per.items()},
         "final_fitness": fits[-1] if fits else None, "ttm_engine": m.ttm_engine(),
