@@ -432,8 +432,9 @@ def main():
         # roofs are computed; the primary `bound` is the one the launch is closer to (the binding
         # roof), the other is kept beside it.
         t_el = ttm_launch_flops / (2 * cfg.R)
-        k = cfg.s
-        ttm_bytes = (7.0 if engine == "int8-digits" else 8.0) * t_el + 8.0 * t_el / k * cfg.R + 7.0 * k * cfg.R
+        # algorithmic bytes per launch from the library's ledger (cpd_get_ttm_bytes): T's digits once,
+        # the FP64 output once, the factor's digit image -- first-level TTMs and block roots alike
+        ttm_bytes = ctr["ttm_bytes"] / max(ctr["ttm_launches"], 1)
         ttm_gbs = ttm_bytes / (ttm_ms * 1e-3) / 1e9 if ttm_ms > 0 else None
         hbm = {"bound": "hbm", "achieved": ttm_gbs, "peak": peaks.get("hbm_gbs"),
                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)", "unit": "GB/s",
@@ -456,8 +457,8 @@ def main():
                     "fp64_equiv_tflops": ttm_tf, "fp64_equiv_over_dmma_peak": (ttm_tf / fp64) if ttm_tf else None,
                     "avg_launch_ms": ttm_ms, "launches": int(ctr["ttm_launches"])}
         if args.msdt_levels > 1:
-            ttm_roof["note"] = ("msdt_levels > 1: the MSDT roots are block contractions (output s^(N-l) R, not "
-                                "s^(N-1) R); the byte model above is the first-level TTM's (pp_init, dt_sweep)")
+            ttm_roof["note"] = ("msdt_levels > 1: the MSDT roots are block contractions (output s^(N-l) R); the "
+                                "launch average mixes them with the first-level TTMs of pp_init and dt_sweep")
         engines = {engine: {"msdt_ms_per_sweep": msdt_ms, "ttm_ms": ttm_ms, "ttm_fp64_equiv_tflops": ttm_tf}}
         if not args.no_dmma_compare:
             engines["dmma"] = dmma_compare(cpd, torch, cfg, T, m, local, rank, world, nccl_id, stream, fp64, fp64_src)

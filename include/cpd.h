@@ -197,6 +197,12 @@ cpd_status cpd_get_phase_ms(cpd_ctx* ctx, double out[5]);
  * built, out[5]=kernels launched by libcpd.so in this process (all kernels, monotone; not reset). */
 cpd_status cpd_get_counters(cpd_ctx* ctx, double out[6]);
 
+/* Algorithmic HBM bytes of the first-level TTMs and block contractions since init or the last
+ * cpd_reset_counters (the roofline numerator of the TTM, DESIGN.md §6/§9): per launch, T read once (7 B per
+ * element on the digit planes, 8 B as FP64), the FP64 output written once, the factor (or the block's
+ * Khatri-Rao product) read.  Divide by cpd_get_counters' out[1] for bytes per launch. */
+cpd_status cpd_get_ttm_bytes(cpd_ctx* ctx, double* out);
+
 /* Auxiliary-memory ledger (Table 1's aux-memory column; the upper-level-fusion trade-off,
  * P:700-702): out[0] = high-water mark of the library's intermediate device buffers (dimension-tree
  * nodes, PP operators, block Khatri-Rao products) since init or the last cpd_reset_counters, in bytes;

@@ -21,7 +21,7 @@ EXPORTED_SYMBOLS = [
     "cpd_set_factors", "cpd_get_phase_ms", "cpd_get_counters", "cpd_reset_counters",
     "cpd_debug_get_pp_operator", "cpd_last_error", "cpd_destroy", "cpd_gen_tensor", "cpd_ttm", "cpd_ttm_i8", "cpd_ttm_engine", "cpd_set_tensor",
     "cpd_last_sweep_status",
-    "cpd_mttv", "cpd_gen_tensor_block", "cpd_get_filler_counters", "cpd_get_memory", "cpd_local_group_create", "cpd_local_group_destroy", "cpd_set_profile_level",
+    "cpd_mttv", "cpd_gen_tensor_block", "cpd_get_filler_counters", "cpd_get_memory", "cpd_get_ttm_bytes", "cpd_local_group_create", "cpd_local_group_destroy", "cpd_set_profile_level",
 ]
 
 
@@ -71,6 +71,7 @@ def load_library():
         "cpd_reset_counters": (C.c_int, [_P]),
         "cpd_get_filler_counters": (C.c_int, [_P, _D]),
         "cpd_get_memory": (C.c_int, [_P, _D]),
+        "cpd_get_ttm_bytes": (C.c_int, [_P, _D]),
         "cpd_set_profile_level": (C.c_int, [_P, C.c_int]),
         "cpd_debug_get_pp_operator": (C.c_int, [_P, C.c_int, C.c_int, _D]),
         "cpd_last_error": (C.c_char_p, [_P]),

@@ -178,6 +178,8 @@ struct cpd_ctx {
   // auxiliary memory ledger (cpd_get_memory): bytes of live dalloc blocks (tree nodes, PP operators,
   // block-contraction Khatri-Rao products) and their high-water mark since init / reset
   double node_live = 0.0, node_peak = 0.0;
+  // algorithmic HBM bytes of the first-level TTMs / block contractions since init or reset (cpd_get_ttm_bytes)
+  double ttm_bytes = 0.0;
 };
 
 // scalar slots
@@ -366,6 +368,11 @@ cpd_status ttm(cpd_ctx* ctx, int j, double* out) {
   ctx->counters[0] += 2.0 * (double)pre * post * ext(ctx, j) * ctx->R;
   ctx->counters[1] += 1;
   ctx->counters[4] += 1;
+  // T read once (7 B per element as digit planes, 8 B as FP64), the FP64 output written, the factor
+  // (its digit image or FP64) read
+  const bool dig = ctx->engine == CPD_ENGINE_INT8_DIGITS && ext(ctx, j) <= cpd::kMaxKI8;
+  ctx->ttm_bytes += (dig ? 7.0 : 8.0) * (double)pre * post * ext(ctx, j) + 8.0 * (double)pre * post * ctx->R +
+                    (dig ? 7.0 : 8.0) * (double)ext(ctx, j) * ctx->R;
   return CPD_OK;
 }
 
@@ -416,10 +423,18 @@ cpd_status ttm_block(cpd_ctx* ctx, const std::vector<int>& Cin, double* out) {
   };
   PhaseScope ps(ctx, PH_TTM);
   const double flops = 2.0 * (double)prodx(0, N) * R;
-  auto account = [&]() {
+  // algorithmic bytes: T read once (digit planes 7 B / FP64 8 B per element), the output (the kept modes
+  // x R) written once, the block's Khatri-Rao factor read (digit image 7 B / FP64 8 B per entry)
+  const double kelem = (double)prodx(0, N), oelem = kelem / [&] {
+    double k = 1;
+    for (int c : C) k *= (double)ext(ctx, c);
+    return k;
+  }();
+  auto account = [&](bool digits) {
     ctx->counters[0] += flops;
     ctx->counters[1] += 1;
     ctx->counters[4] += 1;
+    ctx->ttm_bytes += (digits ? 7.0 : 8.0) * kelem + 8.0 * oelem * R + (digits ? 7.0 : 8.0) * (kelem / oelem) * R;
     return CPD_OK;
   };
   auto krp = [&](const std::vector<int>& modes, const std::vector<int64_t>& stride, double* dst, int64_t rows,
@@ -472,7 +487,7 @@ cpd_status ttm_block(cpd_ctx* ctx, const std::vector<int>& Cin, double* out) {
       cudaError_t e = cpd::launch_ttm_i8_block(P, Mrows, Qp, kb, R, out, 0, ctx->texp, ctx->ws_i8,
                                                ctx->ws_i8_bytes, ctx->st, dv);
       dfree(ctx, kb);
-      if (e == cudaSuccess) return account();
+      if (e == cudaSuccess) return account(true);
       if (e != cudaErrorNotSupported) CU(e);
       cudaGetLastError();
     } else {
@@ -483,7 +498,7 @@ cpd_status ttm_block(cpd_ctx* ctx, const std::vector<int>& Cin, double* out) {
       cudaError_t e = cpd::launch_ttm_i8(ctx->T, pre, K, post, kb, R, out, 0, ctx->texp, ctx->ws_i8,
                                          ctx->ws_i8_bytes, ctx->st, &dv);
       dfree(ctx, kb);
-      if (e == cudaSuccess) return account();
+      if (e == cudaSuccess) return account(true);
       cudaGetLastError();  // no digit layout for this view and K too long for the converting kernel
     }
   }
@@ -498,7 +513,7 @@ cpd_status ttm_block(cpd_ctx* ctx, const std::vector<int>& Cin, double* out) {
     else
       CU(cpd::launch_ttm(ctx->T, pre, K, post, kb, R, out, 0, ctx->st));
     dfree(ctx, kb);
-    return account();
+    return account(false);
   }
   // wrapping block on the FP64 engine: X[p, m, r] = T x_suffix KRP(suffix), then out = X x_p KRP(prefix)
   std::vector<int> pm, sm;
@@ -517,7 +532,7 @@ cpd_status ttm_block(cpd_ctx* ctx, const std::vector<int>& Cin, double* out) {
   dfree(ctx, X);
   dfree(ctx, kp);
   dfree(ctx, ks);
-  return account();
+  return account(false);
 }
 
 // contract the modes `drop` of a node in `order`, returning a new node (input not freed)
@@ -1933,6 +1948,12 @@ cpd_status cpd_get_counters(cpd_ctx* ctx, double out[6]) {
   return CPD_OK;
 }
 
+cpd_status cpd_get_ttm_bytes(cpd_ctx* ctx, double* out) {
+  if (!ctx || !out) return CPD_ERR_INVALID_ARG;
+  *out = ctx->ttm_bytes;
+  return CPD_OK;
+}
+
 cpd_status cpd_get_memory(cpd_ctx* ctx, double out[3]) {
   if (!ctx || !out) return CPD_ERR_INVALID_ARG;
   out[0] = ctx->node_peak;
@@ -1965,6 +1986,7 @@ cpd_status cpd_reset_counters(cpd_ctx* ctx) {
   for (int i = 0; i < 5; i++) ctx->phase_ms[i] = ctx->counters[i] = 0.0;
   ctx->filler[0] = ctx->filler[1] = 0.0;
   ctx->node_peak = ctx->node_live;
+  ctx->ttm_bytes = 0.0;
   return CPD_OK;
 }
 

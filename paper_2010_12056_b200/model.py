@@ -110,9 +110,11 @@ class CPDecomposition:
     def counters(self):
         out = np.zeros(6)
         check(self._lib.cpd_get_counters(self._ctx, dptr(out)), self._ctx)
+        tb = np.zeros(1)
+        check(self._lib.cpd_get_ttm_bytes(self._ctx, dptr(tb)), self._ctx)
         return dict(zip(["ttm_flops", "ttm_launches", "stream_bytes", "stream_launches", "roots",
-                         "kernel_launches"],
-                        out.tolist()))
+                         "kernel_launches", "ttm_bytes"],
+                        out.tolist() + [float(tb[0])]))
 
     def filler_counters(self):
         """cpd_get_filler_counters: PP operator streams on the filler stream (bytes, launches)."""

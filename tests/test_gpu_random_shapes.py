@@ -83,3 +83,31 @@ def test_random_shape_schedule(cpd, seed):
             A = A1
     finally:
         m.close()
+
+
+@pytest.mark.parametrize("seed", range(16, 32))
+def test_random_shape_fused_levels(cpd, seed):
+    """Upper-level fusion (msdt_levels) on random shapes: a random l in [2, N-2] (orders 4-6),
+    N - l + 1 MSDT sweeps (a full cycle of roots and the start of the next), every M^(n) against the
+    oracle's direct MTTKRP at the GPU's current factors."""
+    N, dims, R, impl = case(seed)
+    if N < 4:
+        N, dims = 4, dims + (3,) * (4 - len(dims))
+    cfg = synth.custom(N, 0, R, noise_var=1e-3, seed=500 + seed, dims=dims)
+    To = O.make_tensor(cfg)
+    if O.norm2(To) == 0.0:
+        pytest.skip("zero tensor")
+    l = int(np.random.default_rng(seed).integers(2, N - 1))
+    T = torch.from_numpy(np.ascontiguousarray(To)).cuda()
+    A = synth.init_factors(cfg)
+    m = cpd.cp_als_init(T, cfg.shape, R, A, ttm_impl=impl, msdt_levels=l)
+    try:
+        for _ in range(N - l + 1):
+            m.msdt_sweep()
+            A1 = [m.get_factor(n) for n in range(N)]
+            for n in range(N):
+                ref = O.mttkrp(To, A1[:n] + A[n:], n)
+                assert rel(m.get_last_mttkrp(n), ref) <= TOL, (n, dims, R, l)
+            A = A1
+    finally:
+        m.close()

@@ -1,7 +1,8 @@
 """Per-rank work ledger of the 1-D vs the N-D processor grid (Table 1) on ONE
 GPU through the local group: P ranks (one host thread each), the same global tensor split either
 1 x .. x 1 x P or on `grid`; per rank the PP-approximated sweep's operator-stream bytes (main +
-filler streams) and the MSDT sweep's TTM flops / stream bytes from the library's ledger.
+filler streams), the MSDT sweep's TTM flops / stream bytes from the library's ledger, and the aux-memory
+high-water marks (cpd_get_memory) of the MSDT sweeps and of pp_init (Table 1's aux-memory column).
 usage: python tools/grid_ledger.py s R g1,g2,g3 [ttm_impl]   (order 3; e.g. 1024 200 2,2,2)"""
 import json
 import os
@@ -50,13 +51,18 @@ def run(g):
         m.msdt_sweep()
         m.msdt_sweep()
         c = m.counters()
+        mem_msdt = m.get_memory()["peak"]
+        m.reset_counters()
         m.pp_init()
+        mem_pp = m.get_memory()["peak"]
         m.pp_approx_sweep()
         m.reset_counters()
         m.pp_approx_sweep()
         cp, fl = m.counters(), m.filler_counters()
+        # aux memory: high-water marks of the library's intermediates (Table 1's aux-memory column)
         out[r] = {"msdt_ttm_gflop_per_sweep": c["ttm_flops"] / 2e9, "msdt_stream_gb_per_sweep": c["stream_bytes"] / 2e9,
-                  "pp_operator_gb_per_sweep": (cp["stream_bytes"] + fl["bytes"]) / 1e9, "block": list(T.shape)}
+                  "pp_operator_gb_per_sweep": (cp["stream_bytes"] + fl["bytes"]) / 1e9, "block": list(T.shape),
+                  "msdt_aux_gb": mem_msdt / 1e9, "pp_init_aux_gb": mem_pp / 1e9}
         m.close()
 
     th = [threading.Thread(target=worker, args=(r,)) for r in range(P)]
