@@ -419,14 +419,23 @@ void carveout(K kern) {
 
 void launch_mttv_variant(bool vec2, bool vv, bool pack, bool occ3, unsigned grid, const MttvJobs& jobs, int R,
                          double* out, int beta, double* ws, const OutMap& om, cudaStream_t st) {
+  // experiment switch CPD_FILLER_PAD_KB = k: the filler-stream (occ3) launches use the 64-register build
+  // with k KB of unused dynamic shared memory per CTA, so the shared memory (not the registers) caps them at
+  // 3 CTAs per SM and 16K registers stay free for a main-stream mTTV CTA beside them
+  static const int pad_kb = getenv("CPD_FILLER_PAD_KB") ? atoi(getenv("CPD_FILLER_PAD_KB")) : 0;
+  const size_t dyn = (occ3 && pad_kb > 0) ? (size_t)pad_kb * 1024 : 0;
+  if (dyn) occ3 = false;
 #define CPD_MTTV_V(V2, VV_, PK, O)                                                             \
   do {                                                                                         \
     static bool set_ = false;                                                                  \
     if (!set_) {                                                                               \
       carveout(mttv_kernel<V2, VV_, PK, O>);                                                   \
+      if (pad_kb > 0)                                                                          \
+        cudaFuncSetAttribute(mttv_kernel<V2, VV_, PK, O>,                                      \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, pad_kb * 1024);       \
       set_ = true;                                                                             \
     }                                                                                          \
-    mttv_kernel<V2, VV_, PK, O><<<grid, MT_THREADS, 0, st>>>(jobs, R, out, beta, ws, om);     \
+    mttv_kernel<V2, VV_, PK, O><<<grid, MT_THREADS, dyn, st>>>(jobs, R, out, beta, ws, om);   \
   } while (0)
   if (pack) {
     if (vec2 && vv) CPD_MTTV_V(true, true, true, 3);
