@@ -383,6 +383,37 @@ def test_full_size_sampled_rows(cpd, c, ttm_impl):
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("c", [3, 4])
+def test_full_size_fused_levels_sampled_rows(cpd, c):
+    """Upper-level fusion at full size, in the launch configuration `bench.py --msdt-levels 2` times (C3:
+    block roots of K = 200 x 208 padded rows in 3 K chunks; C4: K = 4096, a wrapping block): one full MSDT
+    cycle (N roots in N - 2 sweeps), sampled rows of every M^(n) against the oracle's explicit-KRP rows with
+    the GPU's input factors."""
+    cfg = synth.config(c)
+    torch.cuda.empty_cache()
+    free, total = torch.cuda.mem_get_info()
+    need = 15 * cfg.numel + 4e9   # T + digit planes + (small) block roots and workspaces
+    if free < need:
+        pytest.skip(f"not enough free device memory ({free / 1e9:.1f} GB < {need / 1e9:.1f} GB)")
+    T = dev_tensor(cpd, cfg)
+    m = _model(cpd, cfg, T, msdt_levels=2)
+    A0 = synth.init_factors(cfg)
+    rng = np.random.default_rng(c + 10)
+    for _ in range(cfg.N - 2):
+        m.msdt_sweep()
+        A1 = [m.get_factor(n) for n in range(cfg.N)]
+        for n in range(cfg.N):
+            rows = rng.choice(cfg.s, 3, replace=False)
+            ref = O.mttkrp_rows(cfg, A1[:n] + A0[n:], n, rows)
+            got = m.get_last_mttkrp(n)[rows]
+            assert rel(got, ref) <= TOL, (n, rel(got, ref))
+        A0 = A1
+    assert m.counters()["roots"] == cfg.N
+    m.close()
+    del T
+    torch.cuda.empty_cache()
+
+
 # ------------------------------- INT8 tensor-core TTM -----------------------------------
 
 @pytest.mark.parametrize("digits", [True, False])
