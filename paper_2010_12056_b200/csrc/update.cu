@@ -160,12 +160,16 @@ __global__ void __launch_bounds__(UPD_THREADS)
                         double* __restrict__ o_dA2, double* __restrict__ o_A2, double* __restrict__ o_MA,
                         const int* __restrict__ st_src, int* __restrict__ st_dst,
                         const double* __restrict__ S_all, const double* __restrict__ dS_all, int N, int nmode,
-                        int* __restrict__ st_local, MPending pend) {
+                        int* __restrict__ st_local, MPending pend, int shfl) {
   extern __shared__ double sm[];
   double* G = sm;                 // R x R: Γ^{-1}
   double* Ws = sm + R * R;        // R x R (PP only)
   double* Xs = Ws + (W ? R * R : 0);  // RB x R: this CTA's new rows
   double* Ds = Xs + RB * R;           // RB x R: their dA
+  // DMMA row phase: y (and a_old) of the CTA's rows, RBp = RB rounded up to 8, row stride LDY
+  const int RBp = (RB + 7) & ~7, Rq = (R + 7) & ~7, LDY = Rq + 4;
+  double* Ys = Ds + RB * R;           // RBp x LDY
+  double* Ao = Ys + RBp * LDY;        // RBp x LDY
   __shared__ double red[3][UPD_THREADS / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // the side stream's SPD verdict for this Γ^{-1}, handed to the main stream's status slot
@@ -226,7 +230,85 @@ __global__ void __launch_bounds__(UPD_THREADS)
   // this CTA owns rows [r0, r0 + RB); warp w solves rows r0 + w, r0 + w + 8, ...
   const int64_t r0 = (int64_t)blockIdx.x * RB;
   const int nrows = (int)max((int64_t)0, min((int64_t)RB, rows - r0));
-  for (int lr = warp; lr < nrows; lr += UPD_THREADS / 32) {
+  if (!shfl) {
+    // Row phase on the FP64 tensor cores: the CTA's rows are m8 tiles, (M [+ A_old W]) Γ^{-1} as two small
+    // GEMMs of mma.m8n8k4.f64 (one warp per 8 x 8 output tile, k in steps of 4), then the elementwise
+    // dA / statistics / writes.  (CPD_UPD_SHFL: the warp-per-row shuffle mat-vecs below.)
+    const int fr = lane >> 2, fc = lane & 3;
+    for (int e = tid; e < RBp * Rq; e += UPD_THREADS) {
+      const int lr = e / Rq, c = e - lr * Rq;
+      double y = 0.0, ao = 0.0;
+      if (lr < nrows && c < R) {
+        const int64_t g = (r0 + lr) * R + c;
+        if (pend.slots > 0) {  // the mTTV's K-split reduction, in mttv_reduce_kernel's order
+          double sv = pend.base ? pend.base[g] : (pend.beta ? M[g] : 0.0);
+          for (int k = 0; k < pend.slots; k++) sv += pend.ws[k * pend.n + g];
+          y = sv;
+          if (!W) M[g] = sv;
+        } else {
+          y = M[g];
+        }
+        ao = A[g];
+      }
+      Ys[lr * LDY + c] = y;
+      Ao[lr * LDY + c] = ao;
+    }
+    __syncthreads();
+    const int nt = (RBp / 8) * (Rq / 8);
+    // C(8x8 tile) += X(rows, k) Mat(k, cols) over k < R; X from shared memory (stride LDY), Mat R x R
+    auto tile_mma = [&](const double* X, const double* Mat, int m0, int n0, double& c0, double& c1) {
+      for (int k0 = 0; k0 < R; k0 += 4) {
+        const int k = k0 + fc;
+        const double a = k < R ? X[(m0 + fr) * LDY + k] : 0.0;
+        const double b = (k < R && n0 + fr < R) ? Mat[k * R + n0 + fr] : 0.0;
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c0), "+d"(c1)
+                     : "d"(a), "d"(b));
+      }
+    };
+    if (W) {  // y += a_old W (Eq. 7's V), written back so M~ = M_p + ΣU + V stays readable
+      for (int t = warp; t < nt; t += UPD_THREADS / 32) {
+        const int m0 = (t / (Rq / 8)) * 8, n0 = (t % (Rq / 8)) * 8;
+        const int lr = m0 + fr, c = n0 + 2 * fc;
+        double c0 = Ys[lr * LDY + c], c1 = Ys[lr * LDY + c + 1];
+        tile_mma(Ao, Ws, m0, n0, c0, c1);
+        __syncwarp();
+        Ys[lr * LDY + c] = c0;
+        Ys[lr * LDY + c + 1] = c1;
+        if (lr < nrows) {
+          if (c < R) M[(r0 + lr) * R + c] = c0;
+          if (c + 1 < R) M[(r0 + lr) * R + c + 1] = c1;
+        }
+      }
+      __syncthreads();
+    }
+    // x = y Γ^{-1} into Xs
+    for (int t = warp; t < nt; t += UPD_THREADS / 32) {
+      const int m0 = (t / (Rq / 8)) * 8, n0 = (t % (Rq / 8)) * 8;
+      double c0 = 0.0, c1 = 0.0;
+      tile_mma(Ys, G, m0, n0, c0, c1);
+      const int lr = m0 + fr, c = n0 + 2 * fc;
+      if (lr < nrows) {
+        if (c < R) Xs[lr * R + c] = c0;
+        if (c + 1 < R) Xs[lr * R + c + 1] = c1;
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < nrows * R; e += UPD_THREADS) {
+      const int lr = e / R, c = e - lr * R;
+      const int64_t g = (r0 + lr) * R + c;
+      const double x = Xs[e];
+      const double b = base ? base[g] : Ao[lr * LDY + c];
+      const double d = x - b;
+      A[g] = x;
+      dA[g] = d;
+      Ds[e] = d;
+      s0 = fma(d, d, s0);
+      s1 = fma(x, x, s1);
+      s2 = fma(Ys[lr * LDY + c], x, s2);
+    }
+  }
+  for (int lr = warp; shfl && lr < nrows; lr += UPD_THREADS / 32) {
     const int64_t i = r0 + lr;
     double y[U], ao[U];
 #pragma unroll
@@ -298,15 +380,26 @@ __global__ void __launch_bounds__(UPD_THREADS)
   const int64_t RR = (int64_t)R * R;
   const int64_t nout = S ? (dS ? 2 * RR : RR) : 0;
   __syncthreads();
-  for (int64_t e = tid; e < nout; e += UPD_THREADS) {
-    const bool second = e >= RR;
-    const int64_t f = second ? e - RR : e;
-    const int a = (int)(f / R), b = (int)(f - (int64_t)a * R);
-    const double* Y = second ? Ds : Xs;
-    double acc = 0.0;
+  // (a, b) of output e = tid + UPD_THREADS j stepped incrementally (one division per thread: the
+  // per-element e / R was ~14 % of the kernel's stall samples at R = 100)
+  {
+    const int step_a = UPD_THREADS / R, step_b = UPD_THREADS - step_a * R;
+    int a = tid / R, b = tid - (tid / R) * R;  // for f = e mod RR; a runs past R into the dS half
+    for (int64_t e = tid; e < nout; e += UPD_THREADS) {
+      const bool second = a >= R;
+      const double* Y = second ? Ds : Xs;
+      const int aa = second ? a - R : a;
+      double acc = 0.0;
 #pragma unroll 8
-    for (int r = 0; r < nrows; r++) acc = fma(Xs[r * R + a], Y[r * R + b], acc);
-    gpart[(int64_t)blockIdx.x * nout + e] = acc;
+      for (int r = 0; r < nrows; r++) acc = fma(Xs[r * R + aa], Y[r * R + b], acc);
+      gpart[(int64_t)blockIdx.x * nout + e] = acc;
+      a += step_a;
+      b += step_b;
+      if (b >= R) {
+        b -= R;
+        a++;
+      }
+    }
   }
   if constexpr (SPLIT) return;  // phase 2b in update_reduce_kernel (a second, ordinary launch)
   cg::this_grid().sync();
@@ -350,8 +443,9 @@ cudaError_t coop_launch(int blocks, size_t smem, void** args, cudaStream_t st, b
 }  // namespace
 
 size_t update_fused_smem(int R, bool pp, int RB) {
-  // Γ^{-1}, W (PP), this CTA's rows and their dA
-  return sizeof(double) * ((size_t)R * R + (pp ? (size_t)R * R : 0) + 2 * (size_t)RB * R);
+  // Γ^{-1}, W (PP), this CTA's rows and their dA, the DMMA row phase's y and a_old tiles
+  const size_t RBp = (RB + 7) & ~7, LDY = ((R + 7) & ~7) + 4;
+  return sizeof(double) * ((size_t)R * R + (pp ? (size_t)R * R : 0) + 2 * (size_t)RB * R + 2 * RBp * LDY);
 }
 
 int update_fused_blocks(int64_t rows) {
@@ -369,6 +463,7 @@ cudaError_t launch_update_fused(int R, int64_t rows, const double* Ginv, const d
                                 int* st_local, const MPending* pendp) {
   if (S_all && R > 32) return cudaErrorInvalidValue;
   MPending pend = pendp ? *pendp : MPending{};
+  static int shfl = getenv("CPD_UPD_SHFL") ? 1 : 0;  // experiment switch: the warp-per-row shuffle row phase
   if (R > kUpdMaxR || rows <= 0) return cudaErrorInvalidValue;
   const int blocks = update_fused_blocks(rows);
   int RB = (int)((rows + blocks - 1) / blocks);
@@ -376,7 +471,7 @@ cudaError_t launch_update_fused(int R, int64_t rows, const double* Ginv, const d
   if (smem > 227 * 1024 - 2048) return cudaErrorInvalidValue;
   void* args[] = {&R,     &rows,   &Ginv,   &W,      &M,      &A,    &base,  &dA,    &S,       &dS,
                   &part,  &gpart,  &RB,     &o_dA2,  &o_A2,   &o_MA, &st_src, &st_dst, &S_all, &dS_all,
-                  &N,     &nmode,  &st_local, &pend};
+                  &N,     &nmode,  &st_local, &pend, &shfl};
   static const bool split = getenv("CPD_UPD_SPLIT") != nullptr;
   cudaError_t e = cudaErrorInvalidValue;
   switch ((R + 31) / 32) {
