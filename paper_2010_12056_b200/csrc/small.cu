@@ -420,7 +420,28 @@ __global__ void __launch_bounds__(kGjThreads)
   const int tid = threadIdx.x;
   const int64_t RR = (int64_t)R * R;
   if (tid == 0) bad = 0;
-  // PP: the second-order Hadamard sum W^(n) of Eq. 7 (pp_w_kernel's arithmetic) in the same launch
+  // PP: the second-order Hadamard sum W^(n) of Eq. 7 (pp_w_kernel's arithmetic) in the same launch, by
+  // the CTAs 1.. (each a slice of the R^2 elements) while CTA 0 inverts Γ -- off the Γ^{-1} latency
+  if (W && gridDim.x > 1) {
+    if (blockIdx.x == 0) goto gj;
+    const int64_t per = (RR + gridDim.x - 2) / (gridDim.x - 1);
+    const int64_t lo = (blockIdx.x - 1) * per, hi = min(RR, lo + per);
+    for (int64_t e = lo + tid; e < hi; e += kGjThreads) {
+      double w = 0.0;
+      for (int i = 0; i < N; i++) {
+        if (i == n) continue;
+        for (int j = i + 1; j < N; j++) {
+          if (j == n) continue;
+          double term = dS_all[i * RR + e] * dS_all[j * RR + e];
+          for (int k = 0; k < N; k++)
+            if (k != i && k != j && k != n) term *= S_all[k * RR + e];
+          w += term;
+        }
+      }
+      W[e] = w;
+    }
+    return;
+  }
   if (W) {
     for (int64_t e = tid; e < RR; e += kGjThreads) {
       double w = 0.0;
@@ -437,6 +458,7 @@ __global__ void __launch_bounds__(kGjThreads)
       W[e] = w;
     }
   }
+gj:
 #pragma unroll 4
   for (int e = tid; e < Rp * Rp; e += kGjThreads) {
     const int i = e / Rp, j = e - i * Rp;
@@ -732,7 +754,10 @@ cudaError_t launch_gamma_inverse(const double* S_all, int N, int n, int R, doubl
   }
   g_launches++;
   static const int dbg = getenv("CPD_GJ_DBG") ? atoi(getenv("CPD_GJ_DBG")) : 0;  // profiling switches
-  gamma_inverse_kernel<<<1, kGjThreads, gamma_inverse_smem(R), st>>>(S_all, N, n, R, Ginv, status, dbg, dS_all, W);
+  // W (PP) by extra CTAs beside the inverting CTA 0 (experiment switch CPD_GJ_W1: all in CTA 0)
+  static const bool w1 = getenv("CPD_GJ_W1") != nullptr;
+  const int grid = (W && !w1) ? 1 + (int)std::min<int64_t>(16, ((int64_t)R * R + 2047) / 2048) : 1;
+  gamma_inverse_kernel<<<grid, kGjThreads, gamma_inverse_smem(R), st>>>(S_all, N, n, R, Ginv, status, dbg, dS_all, W);
   return cudaGetLastError();
 }
 
