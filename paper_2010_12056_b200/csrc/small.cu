@@ -422,8 +422,7 @@ __global__ void __launch_bounds__(kGjThreads)
   if (tid == 0) bad = 0;
   // PP: the second-order Hadamard sum W^(n) of Eq. 7 (pp_w_kernel's arithmetic) in the same launch, by
   // the CTAs 1.. (each a slice of the R^2 elements) while CTA 0 inverts Γ -- off the Γ^{-1} latency
-  if (W && gridDim.x > 1) {
-    if (blockIdx.x == 0) goto gj;
+  if (W && gridDim.x > 1 && blockIdx.x > 0) {
     const int64_t per = (RR + gridDim.x - 2) / (gridDim.x - 1);
     const int64_t lo = (blockIdx.x - 1) * per, hi = min(RR, lo + per);
     for (int64_t e = lo + tid; e < hi; e += kGjThreads) {
@@ -442,7 +441,7 @@ __global__ void __launch_bounds__(kGjThreads)
     }
     return;
   }
-  if (W) {
+  if (W && gridDim.x == 1) {
     for (int64_t e = tid; e < RR; e += kGjThreads) {
       double w = 0.0;
       for (int i = 0; i < N; i++) {
@@ -458,7 +457,6 @@ __global__ void __launch_bounds__(kGjThreads)
       W[e] = w;
     }
   }
-gj:
 #pragma unroll 4
   for (int e = tid; e < Rp * Rp; e += kGjThreads) {
     const int i = e / Rp, j = e - i * Rp;
