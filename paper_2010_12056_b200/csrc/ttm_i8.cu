@@ -1341,8 +1341,14 @@ cudaError_t launch_digit_geo(int Ld, Geo gd, const DigitView& dv, const uint8_t*
   if (!no_mc && gd.ntn % 2 == 0 && (cl_env == 2 || cl_env == 4) && gd.ntn % cl_env == 0 &&
       sm_count() % cl_env == 0)
     gd.cl = cl_env;
-  const int gridd = gd.cl == 1 ? (int)std::min<int64_t>(gd.ntiles, sm_count())
-                               : gd.cl * (int)std::min<int64_t>(gd.nmt * (gd.ntn / gd.cl), sm_count() / gd.cl);
+  // persistent grid: one CTA (pair) per SM, but one SM (pair) left free when that does not raise the most
+  // tiles any CTA runs -- the side stream's single-CTA Γ^{-1} launch then finds an SM without delaying a
+  // TTM CTA by its duration (C2: 8192 tiles need 56 rounds on 148 or 147 CTAs alike)
+  const int64_t units = gd.cl == 1 ? gd.ntiles : gd.nmt * (gd.ntn / gd.cl);
+  int64_t slots = sm_count() / gd.cl;
+  static const bool no_spare = getenv("CPD_I8_NO_SPARE_SM") != nullptr;  // experiment switch
+  if (!no_spare && slots > 1 && (units + slots - 2) / (slots - 1) == (units + slots - 1) / slots) slots--;
+  const int gridd = gd.cl * (int)std::min<int64_t>(units, slots);
   CUtensorMap tmd;
   if (!make_tmap_digits(Ld, dv, gd, &tmd)) return cudaSuccess;
   *launched = true;
