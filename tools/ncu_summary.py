@@ -37,6 +37,7 @@ def main(tag, reps):
         traffic = json.load(open(tpath))
     with open(f"profiles/{tag}_ncu_full.txt", "w") as f:
         for name, rep in reps:
+            per_launch = []  # DRAM bytes of each captured launch: the traffic entry is their mean
             for d, u in rows(rep):
                 f.write(f"== {name}: {d.get('Kernel Name', '')[:120]}\n")
                 for k in KEYS:
@@ -49,7 +50,9 @@ def main(tag, reps):
                 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
                 rb = float(d["dram__bytes_read.sum"]) * scale.get(u["dram__bytes_read.sum"], 1)
                 wb = float(d["dram__bytes_write.sum"]) * scale.get(u["dram__bytes_write.sum"], 1)
-                traffic[name] = rb + wb
+                per_launch.append(rb + wb)
+            if per_launch:
+                traffic[name] = sum(per_launch) / len(per_launch)
     json.dump(traffic, open(tpath, "w"), indent=1)
     print(open(f"profiles/{tag}_ncu_full.txt").read())
 
