@@ -15,6 +15,16 @@
 // columns of R (whole R when R <= 128), so T streams from HBM once; a 4-stage cp.async
 // pipeline stages T and factor tiles in padded shared memory (conflict-free 64-bit
 // fragment loads), 8 warps each issue 2*NF independent DMMAs per k4 step.
+//
+// Default staging (ttm_dmma_tma_kernel; aligned shapes): the T and factor tiles arrive by TMA
+// (cp.async.bulk.tensor, 128-byte swizzle, 16-double-wide boxes, out-of-range rows / k / columns
+// zero-filled by the copy engine) on full/empty mbarriers, issued by warp 0; the fragment rows and
+// columns a lane owns are permuted so that the swizzled tiles are read without bank conflicts.
+// The cp.async kernel below serves the unaligned shapes (odd K / ncols, post % 16 != 0, tiny tensors)
+// and CPD_DMMA_NO_TMA=1.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "kernels.h"
 
 namespace cpd {
@@ -244,6 +254,277 @@ __global__ void __launch_bounds__(Smem<NF>::THREADS, Smem<NF>::MIN_BLOCKS)
   }
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// TMA-staged variant.  Shared-memory stage = A boxes then B boxes, every box [rows][16 doubles]
+// with the 128-byte swizzle (16-byte chunk c of row r stored at chunk c ^ (r & 7)):
+//   KC (post == 1): BK/16 boxes [BM tile rows][16 k]    of the 2-D map {K, Mrows}
+//   MC (post  > 1): BM/16 boxes [BK k][16 m]            of the 3-D map {post, K, pre}; post % 16 == 0,
+//                   so a box never straddles two p (tile rows i = p*post + m)
+//   B:              ceil(BN/16) boxes [BK k][16 n]      of the 2-D map {ncols, K}
+// A DMMA step uses k = kk..kk+3 (lane t -> k = kk + t).  Which tile row is "fragment row g" and
+// which column is "fragment column g" is free as long as the epilogue stores to the same places:
+//   KC rows   r = 16 w + 2 g + h              (h = lo / hi fragment of warp w)
+//   MC rows   m = 16 w + 8 g1 + 4 h + 2 g2 + g0
+//   columns   n = 16 (f>>1) + 8 g1 + 4 (f&1) + 2 g2 + g0   (fragment pair f, f^1 = one 16-column box;
+//             the odd last fragment of an odd NF keeps n = 16 (f>>1) + g)
+// With these a half-warp (g < 4 or g >= 4, all t) touches 16 distinct 8-byte banks and the two
+// half-warps pair up on them: two wavefronts per 64-bit fragment load, the minimum.
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE_%=;\nbra WAIT_%=;\nDONE_%=:\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* tm, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(dst), "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* tm, int c0, int c1, int c2, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(dst), "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+
+template <int NF>
+struct SmemT {
+  using S = Smem<NF>;
+  static constexpr int BK = S::BK, BM = S::BM, STAGES = S::STAGES, THREADS = S::THREADS;
+  static constexpr int NB16 = (8 * NF + 15) / 16;        // B boxes per stage
+  static constexpr int A_BYTES = BM * BK * 8;
+  static constexpr int BBOX_BYTES = BK * 128;
+  static constexpr int STAGE_BYTES = A_BYTES + NB16 * BBOX_BYTES;  // a multiple of 1024
+  static constexpr size_t BYTES = (size_t)STAGE_BYTES * STAGES + 1024 /* alignment slack */ + 16 * STAGES;
+};
+
+template <int NF, bool MC>
+__global__ void __launch_bounds__(Smem<NF>::THREADS, Smem<NF>::MIN_BLOCKS)
+    ttm_dmma_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        int64_t pre, int64_t K, int64_t post, int ncols, int ntiles_n,
+                        double* __restrict__ out, int beta) {
+  using ST = SmemT<NF>;
+  constexpr int BK = ST::BK, BM = ST::BM, STAGES = ST::STAGES, BN = 8 * NF;
+  constexpr int NWARPS = ST::THREADS / 32;
+  constexpr int NA = MC ? BM / 16 : BK / 16;             // A boxes per stage
+  constexpr int ABOX_BYTES = MC ? BK * 128 : BM * 128;
+  constexpr int NFP = NF & ~1;                           // fragments with the paired column map
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
+  const uint32_t base = (raw + 1023u) & ~1023u;                  // swizzle atoms are 1024-byte aligned
+  const uint8_t* sbase = smem_raw + (base - raw);                // the same place, for the fragment loads
+  const uint32_t full0 = base + ST::STAGE_BYTES * STAGES, empty0 = full0 + 8 * STAGES;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int g0 = g & 1, g1 = (g >> 1) & 1, g2 = g >> 2;
+
+  const int64_t Mrows = pre * post;
+  const int64_t mtile = blockIdx.x / ntiles_n;
+  const int ntile = blockIdx.x % ntiles_n;
+  const int64_t i0 = mtile * BM;
+  const int n0 = ntile * BN;
+  const int nk = (int)((K + BK - 1) / BK);
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; s++) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, NWARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  // warp 0: lane l < NA + NB16 issues box l of stage kt
+  auto issue = [&](int kt) {
+    const int slot = kt % STAGES;
+    const uint32_t bar = full0 + 8 * slot, dst = base + slot * ST::STAGE_BYTES;
+    if (kt >= STAGES) mbar_wait(empty0 + 8 * slot, ((kt / STAGES) - 1) & 1);
+    if (lane == 0) mbar_arrive_expect_tx(bar, ST::STAGE_BYTES);
+    __syncwarp();
+    const int k0 = kt * BK;
+    if (lane < NA) {
+      if constexpr (!MC) {
+        tma_2d(dst + lane * ABOX_BYTES, &tmA, k0 + 16 * lane, (int)i0, bar);
+      } else {
+        const int64_t i = i0 + 16 * lane;
+        const int64_t p = i / post;
+        tma_3d(dst + lane * ABOX_BYTES, &tmA, (int)(i - p * post), k0, (int)p, bar);
+      }
+    } else if (lane < NA + ST::NB16) {
+      const int j = lane - NA;
+      tma_2d(dst + ST::A_BYTES + j * ST::BBOX_BYTES, &tmB, n0 + 16 * j, k0, bar);
+    }
+  };
+
+  double acc[2][NF][2];
+#pragma unroll
+  for (int h = 0; h < 2; h++)
+#pragma unroll
+    for (int f = 0; f < NF; f++) acc[h][f][0] = acc[h][f][1] = 0.0;
+
+  if (warp == 0)
+    for (int s = 0; s < STAGES - 1 && s < nk; s++) issue(s);
+
+  // per-thread parts of the swizzled fragment addresses (bytes inside a box)
+  //   KC A: row r = 16 w + 2 g + h, k = kk + t: chunk ((kk & 15) >> 1) + (t >> 1), half t & 1
+  //   MC A / B: row k = kk + t (k & 7 = (kk & 4) + t), 16-byte chunk of the column, half g0
+  const uint32_t a_kc = (uint32_t)((16 * warp + 2 * g) * 128 + ((t & 1) << 3));
+  const uint32_t rk = (uint32_t)(t * 128 + (g0 << 3));
+
+  for (int kt = 0; kt < nk; kt++) {
+    if (warp == 0 && kt + STAGES - 1 < nk) issue(kt + STAGES - 1);
+    const int slot = kt % STAGES;
+    mbar_wait(full0 + 8 * slot, (kt / STAGES) & 1);
+    const uint8_t* As = sbase + slot * ST::STAGE_BYTES;
+    const uint8_t* Bs = As + ST::A_BYTES;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double a[2];
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        uint32_t ad;
+        if constexpr (!MC) {
+          const uint32_t chunk = (uint32_t)((((kk & 15) >> 1) + (t >> 1)) ^ ((2 * g + h) & 7));
+          ad = (kk >> 4) * ABOX_BYTES + a_kc + h * 128 + (chunk << 4);
+        } else {
+          const uint32_t chunk = (uint32_t)((4 * g1 + 2 * h + g2) ^ ((kk & 4) + t));
+          ad = warp * ABOX_BYTES + kk * 128 + rk + (chunk << 4);
+        }
+        a[h] = *reinterpret_cast<const double*>(As + ad);
+      }
+      double b[NF];
+#pragma unroll
+      for (int f = 0; f < NF; f++) {
+        const uint32_t cn = f < NFP ? (uint32_t)(4 * g1 + 2 * (f & 1) + g2) : (uint32_t)(g >> 1);
+        const uint32_t chunk = cn ^ (uint32_t)((kk & 4) + t);
+        const uint32_t ad = (f >> 1) * ST::BBOX_BYTES + kk * 128 + rk + (chunk << 4);
+        b[f] = *reinterpret_cast<const double*>(Bs + ad);
+      }
+#pragma unroll
+      for (int f = 0; f < NF; f++) {
+        dmma(acc[0][f][0], acc[0][f][1], a[0], b[f]);
+        dmma(acc[1][f][0], acc[1][f][1], a[1], b[f]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8 * slot);
+  }
+
+  // ---- epilogue: the lane's rows (h = 0, 1) and column pairs under the permuted maps ----
+#pragma unroll
+  for (int h = 0; h < 2; h++) {
+    const int rloc = MC ? 16 * warp + 8 * g1 + 4 * h + 2 * g2 + g0 : 16 * warp + 2 * g + h;
+    const int64_t i = i0 + rloc;
+    if (i >= Mrows) continue;
+    double* orow = out + i * ncols;
+#pragma unroll
+    for (int f = 0; f < NF; f++) {
+      const int n = n0 + 16 * (f >> 1) + (f < NFP ? 8 * (t & 1) + 4 * (f & 1) + 2 * (t >> 1) : 2 * t);
+      double v0 = acc[h][f][0], v1 = acc[h][f][1];
+      if (n + 1 < ncols) {  // ncols even: n, n + 1 both valid, 16-byte aligned
+        double2* p2 = reinterpret_cast<double2*>(orow + n);
+        if (beta) {
+          double2 o = *p2;
+          v0 += o.x;
+          v1 += o.y;
+        }
+        *p2 = make_double2(v0, v1);
+      }
+    }
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+template <int NF, bool MC>
+cudaError_t run_tma(const CUtensorMap& tmA, const CUtensorMap& tmB, int64_t grid, int64_t pre, int64_t K,
+                    int64_t post, int ncols, int ntiles_n, double* out, int beta, cudaStream_t st) {
+  using ST = SmemT<NF>;
+  auto kern = ttm_dmma_tma_kernel<NF, MC>;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ST::BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  g_launches++;
+  kern<<<(unsigned)grid, ST::THREADS, ST::BYTES, st>>>(tmA, tmB, pre, K, post, ncols, ntiles_n, out, beta);
+  return cudaGetLastError();
+}
+
+// returns cudaErrorNotSupported when the shape does not qualify (the caller falls back to cp.async)
+template <int NF>
+cudaError_t launch_tma(const double* X, int64_t pre, int64_t K, int64_t post, const double* B, int ncols,
+                       int ntiles_n, double* out, int beta, cudaStream_t st) {
+  using ST = SmemT<NF>;
+  static const bool off = getenv("CPD_DMMA_NO_TMA") && atoi(getenv("CPD_DMMA_NO_TMA"));
+  const bool mc = post > 1;
+  const int64_t Mrows = pre * post;
+  if (off || (ncols & 1) || ncols < 16 || K < ST::BK || Mrows < ST::BM || Mrows > 0x7fffffff ||
+      K > 0x7fffffff || (reinterpret_cast<uintptr_t>(X) & 15) || (reinterpret_cast<uintptr_t>(B) & 15) ||
+      (reinterpret_cast<uintptr_t>(out) & 15))
+    return cudaErrorNotSupported;
+  if (mc ? (post % 16 != 0) : (K % 2 != 0)) return cudaErrorNotSupported;
+  auto enc = tmap_encoder();
+  if (!enc) return cudaErrorNotSupported;
+  CUtensorMap tmA, tmB;
+  CUresult r;
+  if (!mc) {
+    cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)Mrows};
+    cuuint64_t strides[1] = {(cuuint64_t)K * 8};
+    cuuint32_t box[2] = {16, (cuuint32_t)ST::BM}, es[2] = {1, 1};
+    r = enc(&tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(X), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    cuuint64_t dims[3] = {(cuuint64_t)post, (cuuint64_t)K, (cuuint64_t)pre};
+    cuuint64_t strides[2] = {(cuuint64_t)post * 8, (cuuint64_t)K * post * 8};
+    cuuint32_t box[3] = {16, (cuuint32_t)ST::BK, 1}, es[3] = {1, 1, 1};
+    r = enc(&tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(X), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  if (r != CUDA_SUCCESS) return cudaErrorNotSupported;
+  {
+    cuuint64_t dims[2] = {(cuuint64_t)ncols, (cuuint64_t)K};
+    cuuint64_t strides[1] = {(cuuint64_t)ncols * 8};
+    cuuint32_t box[2] = {16, (cuuint32_t)ST::BK}, es[2] = {1, 1};
+    r = enc(&tmB, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(B), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  if (r != CUDA_SUCCESS) return cudaErrorNotSupported;
+  const int64_t grid = (Mrows + ST::BM - 1) / ST::BM * ntiles_n;
+  if (grid > 0x7fffffff) return cudaErrorInvalidConfiguration;
+  return mc ? run_tma<NF, true>(tmA, tmB, grid, pre, K, post, ncols, ntiles_n, out, beta, st)
+            : run_tma<NF, false>(tmA, tmB, grid, pre, K, post, ncols, ntiles_n, out, beta, st);
+}
+
 template <int NF, bool MC, bool VEC2, bool BVEC2>
 cudaError_t launch_nf(const double* X, int64_t pre, int64_t K, int64_t post, const double* B,
                       int ncols, int ntiles_n, double* out, int beta, cudaStream_t st) {
@@ -267,6 +548,10 @@ cudaError_t launch_nf(const double* X, int64_t pre, int64_t K, int64_t post, con
 template <int NF>
 cudaError_t dispatch_layout(const double* X, int64_t pre, int64_t K, int64_t post, const double* B,
                             int ncols, int ntiles_n, double* out, int beta, cudaStream_t st) {
+  {
+    cudaError_t e = launch_tma<NF>(X, pre, K, post, B, ncols, ntiles_n, out, beta, st);
+    if (e != cudaErrorNotSupported) return e;
+  }
   const bool mc = post > 1;
   const bool bvec = (ncols % 2) == 0;
   const bool avec = mc ? (post % 2) == 0 : (K % 2) == 0;

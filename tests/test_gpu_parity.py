@@ -82,6 +82,27 @@ def test_ttm_all_positions(cpd, shape, R):
         assert rel(out.cpu().numpy(), ref) <= 1e-13, (j, rel(out.cpu().numpy(), ref))
 
 
+@pytest.mark.parametrize("shape,R", [((41, 48, 64), 64), ((41, 48, 50), 100), ((40, 32, 48), 200), ((33, 64, 80), 32),
+                                     ((35, 36, 96), 24), ((37, 40, 112), 18), ((9, 16, 10, 32), 100), ((130, 34, 16), 16),
+                                     ((3, 70, 128), 128), ((257, 64), 72)])
+def test_ttm_dmma_tma_staged_shapes(cpd, shape, R):
+    """FP64 DMMA engine, TMA-staged tiles (Eq. 4 with one contracted mode): shapes that take the
+    swizzled-box path -- even K (last mode), post % 16 == 0 (other modes), even R >= 16 -- with ragged row tiles,
+    K tails inside a 16-wide box, tiles that straddle two p, odd fragment counts (R = 24, 100, 200: the unpaired
+    last column fragment), R not a multiple of 8 (zero-filled columns), two N tiles (R = 200)."""
+    rng = np.random.default_rng(sum(shape) * 7 + R)
+    Tn = rng.standard_normal(shape)
+    T = torch.from_numpy(Tn).cuda()
+    for j in range(len(shape)):
+        A = rng.standard_normal((shape[j], R))
+        pre = int(np.prod(shape[:j])) if j else 1
+        post = int(np.prod(shape[j + 1:])) if j < len(shape) - 1 else 1
+        out = torch.full((pre * post, R), float("nan"), dtype=torch.float64, device="cuda")
+        cpd.cpd_ttm(T, pre, shape[j], post, torch.from_numpy(A).cuda(), R, out)
+        ref = O.ttm(Tn, A, j).reshape(pre * post, R)
+        assert rel(out.cpu().numpy(), ref) <= 1e-13, (j, rel(out.cpu().numpy(), ref))
+
+
 @pytest.mark.parametrize("shape,R", [((37, 29, 41), 8), ((16, 130), 64), ((33, 20, 17), 13), ((9, 10, 11, 5), 100),
                                      ((3, 1000, 2), 7), ((4, 5), 200)])
 def test_mttv_all_axes(cpd, shape, R):
