@@ -20,7 +20,7 @@
 // (cp.async.bulk.tensor, 128-byte swizzle, 16-double-wide boxes, out-of-range rows / k / columns
 // zero-filled by the copy engine) on full/empty mbarriers, issued by warp 0; the fragment rows and
 // columns a lane owns are permuted so that the swizzled tiles are read without bank conflicts.
-// The cp.async kernel below serves the unaligned shapes (odd K / ncols, post % 16 != 0, tiny tensors)
+// The cp.async kernel below serves the unaligned shapes (odd K / ncols / post, small post % 16 != 0, tiny tensors)
 // and CPD_DMMA_NO_TMA=1.
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -259,8 +259,8 @@ __global__ void __launch_bounds__(Smem<NF>::THREADS, Smem<NF>::MIN_BLOCKS)
 // TMA-staged variant.  Shared-memory stage = A boxes then B boxes, every box [rows][16 doubles]
 // with the 128-byte swizzle (16-byte chunk c of row r stored at chunk c ^ (r & 7)):
 //   KC (post == 1): BK/16 boxes [BM tile rows][16 k]    of the 2-D map {K, Mrows}
-//   MC (post  > 1): BM/16 boxes [BK k][16 m]            of the 3-D map {post, K, pre}; post % 16 == 0,
-//                   so a box never straddles two p (tile rows i = p*post + m)
+//   MC (post  > 1): BM/16 boxes [BK k][16 m]            of the 3-D map {post, K, pre}; tile rows in the
+//                   padded row space i' = p*post16 + m, so a box never straddles two p
 //   B:              ceil(BN/16) boxes [BK k][16 n]      of the 2-D map {ncols, K}
 // A DMMA step uses k = kk..kk+3 (lane t -> k = kk + t).  Which tile row is "fragment row g" and
 // which column is "fragment column g" is free as long as the epilogue stores to the same places:
@@ -315,8 +315,10 @@ struct SmemT {
 template <int NF, bool MC>
 __global__ void __launch_bounds__(Smem<NF>::THREADS, Smem<NF>::MIN_BLOCKS)
     ttm_dmma_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                        int64_t pre, int64_t K, int64_t post, int ncols, int ntiles_n,
+                        int64_t pre, int64_t K, int64_t post, int64_t post16, int ncols, int ntiles_n,
                         double* __restrict__ out, int beta) {
+  // MC: the tile rows live in a padded row space i' = p * post16 + m (post16 = post rounded up to 16), so a
+  // 16-row box never straddles two p; rows m >= post are zero-filled by TMA and skipped by the epilogue
   using ST = SmemT<NF>;
   constexpr int BK = ST::BK, BM = ST::BM, STAGES = ST::STAGES, BN = 8 * NF;
   constexpr int NWARPS = ST::THREADS / 32;
@@ -333,7 +335,7 @@ __global__ void __launch_bounds__(Smem<NF>::THREADS, Smem<NF>::MIN_BLOCKS)
   const int g = lane >> 2, t = lane & 3;
   const int g0 = g & 1, g1 = (g >> 1) & 1, g2 = g >> 2;
 
-  const int64_t Mrows = pre * post;
+  const int64_t Mrows = pre * (MC ? post16 : post);
   const int64_t mtile = blockIdx.x / ntiles_n;
   const int ntile = blockIdx.x % ntiles_n;
   const int64_t i0 = mtile * BM;
@@ -362,8 +364,8 @@ __global__ void __launch_bounds__(Smem<NF>::THREADS, Smem<NF>::MIN_BLOCKS)
         tma_2d(dst + lane * ABOX_BYTES, &tmA, k0 + 16 * lane, (int)i0, bar);
       } else {
         const int64_t i = i0 + 16 * lane;
-        const int64_t p = i / post;
-        tma_3d(dst + lane * ABOX_BYTES, &tmA, (int)(i - p * post), k0, (int)p, bar);
+        const int64_t p = i / post16;
+        tma_3d(dst + lane * ABOX_BYTES, &tmA, (int)(i - p * post16), k0, (int)p, bar);
       }
     } else if (lane < NA + ST::NB16) {
       const int j = lane - NA;
@@ -429,8 +431,13 @@ __global__ void __launch_bounds__(Smem<NF>::THREADS, Smem<NF>::MIN_BLOCKS)
 #pragma unroll
   for (int h = 0; h < 2; h++) {
     const int rloc = MC ? 16 * warp + 8 * g1 + 4 * h + 2 * g2 + g0 : 16 * warp + 2 * g + h;
-    const int64_t i = i0 + rloc;
+    int64_t i = i0 + rloc;
     if (i >= Mrows) continue;
+    if constexpr (MC) {
+      const int64_t p = i / post16, m = i - p * post16;
+      if (m >= post) continue;
+      i = p * post + m;
+    }
     double* orow = out + i * ncols;
 #pragma unroll
     for (int f = 0; f < NF; f++) {
@@ -463,7 +470,7 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 
 template <int NF, bool MC>
 cudaError_t run_tma(const CUtensorMap& tmA, const CUtensorMap& tmB, int64_t grid, int64_t pre, int64_t K,
-                    int64_t post, int ncols, int ntiles_n, double* out, int beta, cudaStream_t st) {
+                    int64_t post, int64_t post16, int ncols, int ntiles_n, double* out, int beta, cudaStream_t st) {
   using ST = SmemT<NF>;
   auto kern = ttm_dmma_tma_kernel<NF, MC>;
   static bool attr_set = false;  // per instantiation
@@ -473,7 +480,7 @@ cudaError_t run_tma(const CUtensorMap& tmA, const CUtensorMap& tmB, int64_t grid
     attr_set = true;
   }
   g_launches++;
-  kern<<<(unsigned)grid, ST::THREADS, ST::BYTES, st>>>(tmA, tmB, pre, K, post, ncols, ntiles_n, out, beta);
+  kern<<<(unsigned)grid, ST::THREADS, ST::BYTES, st>>>(tmA, tmB, pre, K, post, post16, ncols, ntiles_n, out, beta);
   return cudaGetLastError();
 }
 
@@ -484,12 +491,14 @@ cudaError_t launch_tma(const double* X, int64_t pre, int64_t K, int64_t post, co
   using ST = SmemT<NF>;
   static const bool off = getenv("CPD_DMMA_NO_TMA") && atoi(getenv("CPD_DMMA_NO_TMA"));
   const bool mc = post > 1;
-  const int64_t Mrows = pre * post;
+  const int64_t post16 = (post + 15) / 16 * 16;
+  const int64_t Mrows = pre * (mc ? post16 : post);  // MC: padded row space (see the kernel)
   if (off || (ncols & 1) || ncols < 16 || K < ST::BK || Mrows < ST::BM || Mrows > 0x7fffffff ||
       K > 0x7fffffff || (reinterpret_cast<uintptr_t>(X) & 15) || (reinterpret_cast<uintptr_t>(B) & 15) ||
       (reinterpret_cast<uintptr_t>(out) & 15))
     return cudaErrorNotSupported;
-  if (mc ? (post % 16 != 0) : (K % 2 != 0)) return cudaErrorNotSupported;
+  // TMA strides are multiples of 16 bytes; MC rows padded per p to 16: at most 25 % zero rows
+  if (mc ? ((post & 1) || (post % 16 != 0 && post < 64)) : (K % 2 != 0)) return cudaErrorNotSupported;
   auto enc = tmap_encoder();
   if (!enc) return cudaErrorNotSupported;
   CUtensorMap tmA, tmB;
@@ -521,8 +530,8 @@ cudaError_t launch_tma(const double* X, int64_t pre, int64_t K, int64_t post, co
   if (r != CUDA_SUCCESS) return cudaErrorNotSupported;
   const int64_t grid = (Mrows + ST::BM - 1) / ST::BM * ntiles_n;
   if (grid > 0x7fffffff) return cudaErrorInvalidConfiguration;
-  return mc ? run_tma<NF, true>(tmA, tmB, grid, pre, K, post, ncols, ntiles_n, out, beta, st)
-            : run_tma<NF, false>(tmA, tmB, grid, pre, K, post, ncols, ntiles_n, out, beta, st);
+  return mc ? run_tma<NF, true>(tmA, tmB, grid, pre, K, post, post16, ncols, ntiles_n, out, beta, st)
+            : run_tma<NF, false>(tmA, tmB, grid, pre, K, post, post16, ncols, ntiles_n, out, beta, st);
 }
 
 template <int NF, bool MC, bool VEC2, bool BVEC2>

@@ -84,12 +84,13 @@ def test_ttm_all_positions(cpd, shape, R):
 
 @pytest.mark.parametrize("shape,R", [((41, 48, 64), 64), ((41, 48, 50), 100), ((40, 32, 48), 200), ((33, 64, 80), 32),
                                      ((35, 36, 96), 24), ((37, 40, 112), 18), ((9, 16, 10, 32), 100), ((130, 34, 16), 16),
-                                     ((3, 70, 128), 128), ((257, 64), 72)])
+                                     ((3, 70, 128), 128), ((257, 64), 72), ((20, 34, 200), 64), ((6, 40, 72), 100),
+                                     ((5, 33, 100), 32), ((3, 4, 36, 66), 200)])
 def test_ttm_dmma_tma_staged_shapes(cpd, shape, R):
     """FP64 DMMA engine, TMA-staged tiles (Eq. 4 with one contracted mode): shapes that take the
     swizzled-box path -- even K (last mode), post % 16 == 0 (other modes), even R >= 16 -- with ragged row tiles,
     K tails inside a 16-wide box, tiles that straddle two p, odd fragment counts (R = 24, 100, 200: the unpaired
-    last column fragment), R not a multiple of 8 (zero-filled columns), two N tiles (R = 200)."""
+    last column fragment), R not a multiple of 8 (zero-filled columns), two N tiles (R = 200), post % 16 != 0 (rows padded per p to 16: post = 200, 72, 100, 66)."""
     rng = np.random.default_rng(sum(shape) * 7 + R)
     Tn = rng.standard_normal(shape)
     T = torch.from_numpy(Tn).cuda()
