@@ -38,6 +38,20 @@ def test_sass_uses_fp64_tensor_cores():
     assert "DMMA.8x8x4" in r.stdout
 
 
+def test_sass_dmma_ttm_is_tma_staged():
+    """The FP64 DMMA TTM stages its tiles by TMA: the ttm_dmma_tma_kernel functions carry both DMMA.8x8x4
+    and TMA tensor loads (UTMALDG.2D / .3D) waited on by mbarrier phase checks, and no LDGSTS (cp.async)."""
+    from paper_2010_12056_b200 import build
+    lib = build.build()
+    r = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", lib], capture_output=True, text=True)
+    funcs = re.split(r"\n\s*Function : ", r.stdout)
+    tma = [f for f in funcs if "ttm_dmma_tma_kernel" in f.split("\n", 1)[0]]
+    assert len(tma) >= 32, len(tma)            # NF = 1..16 x {KC, MC}
+    for f in tma:
+        assert "DMMA.8x8x4" in f and "UTMALDG" in f and "SYNCS" in f and "LDGSTS" not in f
+    assert any("UTMALDG.3D" in f for f in tma) and any("UTMALDG.2D" in f for f in tma)
+
+
 def test_sass_uses_tcgen05_and_tma():
     """The default first-level TTM is Blackwell-native: tcgen05.mma kind::i8 (UTCIMMA), TMEM loads
     (LDTM), TMA tensor loads (UTMALDG) with cluster multicast, bulk copies (UBLKCP)."""
