@@ -588,8 +588,13 @@ cudaError_t launch_ttm(const double* X, int64_t pre, int64_t K, int64_t post, co
 #ifndef CPD_TTM_MAXNF
 #define CPD_TTM_MAXNF 16
 #endif
+  // N tiles of at most maxnf 8-column fragments (CPD_DMMA_MAXNF, experiment switch; default CPD_TTM_MAXNF)
+  static const int maxnf = [] {
+    int v = getenv("CPD_DMMA_MAXNF") ? atoi(getenv("CPD_DMMA_MAXNF")) : CPD_TTM_MAXNF;
+    return v < 1 ? 1 : (v > 16 ? 16 : v);
+  }();
   int nf_total = (ncols + 7) / 8;
-  int ntiles = (nf_total + CPD_TTM_MAXNF - 1) / CPD_TTM_MAXNF;
+  int ntiles = (nf_total + maxnf - 1) / maxnf;
   int nf = (nf_total + ntiles - 1) / ntiles;
   switch (nf) {
     case 1: return dispatch_layout<1>(X, pre, K, post, B, ncols, ntiles, out, beta, st);
