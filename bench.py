@@ -523,7 +523,7 @@ def pp_sweep_roof(cfg, world, pp_ms, peaks):
 
 
 def dmma_roof(ttm_tf, fp64, fp64_src, flops, ms, ctr):
-    return {"kernel": "ttm_dmma (first-level TTM, DMMA.8x8x4)", "bound": "tensor", "achieved": ttm_tf,
+    return {"kernel": "ttm_dmma_tma (first-level TTM, DMMA.8x8x4, TMA-staged swizzled tiles)", "bound": "tensor", "achieved": ttm_tf,
             "peak": fp64, "peak_source": fp64_src, "unit": "TFLOP/s", "frac": (ttm_tf / fp64) if ttm_tf else None,
             "traffic": ncu_traffic("ttm_dmma"), "flops_per_launch": flops, "avg_launch_ms": ms,
             "launches": int(ctr["ttm_launches"])}
