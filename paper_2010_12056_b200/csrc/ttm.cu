@@ -301,10 +301,16 @@ __device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* tm, int 
       : "memory");
 }
 
-template <int NF>
+template <int NF, bool O3 = false>
 struct SmemT {
   using S = Smem<NF>;
-  static constexpr int BK = S::BK, BM = S::BM, STAGES = S::STAGES, THREADS = S::THREADS;
+  // O3 (NF 9..14, e.g. R = 100, 200: NF = 13; grids of several waves): 3 stages and 3 CTAs/SM = 12 warps/SM
+  // (4 stages x 2 CTAs = 8 warps/SM left the DMMA pipe 87 % active on C5).  Small grids (the R x R update
+  // GEMMs) keep the 4-stage configuration: they are latency-bound and measured slower with 3 stages.
+  static constexpr bool OCC3 = O3 && NF > 8 && NF <= 14;
+  static constexpr int BK = S::BK, BM = S::BM, THREADS = S::THREADS;
+  static constexpr int STAGES = OCC3 ? 3 : S::STAGES;
+  static constexpr int MIN_BLOCKS = OCC3 ? 3 : S::MIN_BLOCKS;
   static constexpr int NB16 = (8 * NF + 15) / 16;        // B boxes per stage
   static constexpr int A_BYTES = BM * BK * 8;
   static constexpr int BBOX_BYTES = BK * 128;
@@ -312,14 +318,14 @@ struct SmemT {
   static constexpr size_t BYTES = (size_t)STAGE_BYTES * STAGES + 1024 /* alignment slack */ + 16 * STAGES;
 };
 
-template <int NF, bool MC>
-__global__ void __launch_bounds__(Smem<NF>::THREADS, Smem<NF>::MIN_BLOCKS)
+template <int NF, bool MC, bool O3>
+__global__ void __launch_bounds__(SmemT<NF, O3>::THREADS, SmemT<NF, O3>::MIN_BLOCKS)
     ttm_dmma_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         int64_t pre, int64_t K, int64_t post, int64_t post16, int ncols, int ntiles_n,
                         double* __restrict__ out, int beta) {
   // MC: the tile rows live in a padded row space i' = p * post16 + m (post16 = post rounded up to 16), so a
   // 16-row box never straddles two p; rows m >= post are zero-filled by TMA and skipped by the epilogue
-  using ST = SmemT<NF>;
+  using ST = SmemT<NF, O3>;
   constexpr int BK = ST::BK, BM = ST::BM, STAGES = ST::STAGES, BN = 8 * NF;
   constexpr int NWARPS = ST::THREADS / 32;
   constexpr int NA = MC ? BM / 16 : BK / 16;             // A boxes per stage
@@ -468,11 +474,11 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
   return fn;
 }
 
-template <int NF, bool MC>
+template <int NF, bool MC, bool O3>
 cudaError_t run_tma(const CUtensorMap& tmA, const CUtensorMap& tmB, int64_t grid, int64_t pre, int64_t K,
                     int64_t post, int64_t post16, int ncols, int ntiles_n, double* out, int beta, cudaStream_t st) {
-  using ST = SmemT<NF>;
-  auto kern = ttm_dmma_tma_kernel<NF, MC>;
+  using ST = SmemT<NF, O3>;
+  auto kern = ttm_dmma_tma_kernel<NF, MC, O3>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ST::BYTES);
@@ -530,8 +536,14 @@ cudaError_t launch_tma(const double* X, int64_t pre, int64_t K, int64_t post, co
   if (r != CUDA_SUCCESS) return cudaErrorNotSupported;
   const int64_t grid = (Mrows + ST::BM - 1) / ST::BM * ntiles_n;
   if (grid > 0x7fffffff) return cudaErrorInvalidConfiguration;
-  return mc ? run_tma<NF, true>(tmA, tmB, grid, pre, K, post, post16, ncols, ntiles_n, out, beta, st)
-            : run_tma<NF, false>(tmA, tmB, grid, pre, K, post, post16, ncols, ntiles_n, out, beta, st);
+  if constexpr (NF > 8 && NF <= 14) {
+    static const bool no_occ3 = getenv("CPD_DMMA_NO_OCC3") && atoi(getenv("CPD_DMMA_NO_OCC3"));
+    if (!no_occ3 && grid >= 4 * 148 * 3)  // several waves of 3 CTAs/SM
+      return mc ? run_tma<NF, true, true>(tmA, tmB, grid, pre, K, post, post16, ncols, ntiles_n, out, beta, st)
+                : run_tma<NF, false, true>(tmA, tmB, grid, pre, K, post, post16, ncols, ntiles_n, out, beta, st);
+  }
+  return mc ? run_tma<NF, true, false>(tmA, tmB, grid, pre, K, post, post16, ncols, ntiles_n, out, beta, st)
+            : run_tma<NF, false, false>(tmA, tmB, grid, pre, K, post, post16, ncols, ntiles_n, out, beta, st);
 }
 
 template <int NF, bool MC, bool VEC2, bool BVEC2>
